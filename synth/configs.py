@@ -1,0 +1,100 @@
+"""The five BASELINE.json workloads as seeded synthetic inputs.
+
+Every config is a voxel mask + Kuhn split (synth.meshes) with its lattice,
+periodic flags, AIM grid and material.  ``coarsen=c`` multiplies h by c and
+divides the grid by c (same geometry, ~c^3 fewer nodes): the "tiny analogues"
+the oracle finishes in seconds.
+Units: CGS (cm).  1 nm = 1e-7 cm.
+"""
+import math
+import numpy as np
+from .meshes import kuhn_voxel_mesh
+
+NM = 1e-7
+
+CONFIGS = {
+    # name: description (BASELINE.json configs[i])
+    "C1": "3D-periodic cube, ~1k nodes filling the cell (touching), 16^3 AIM grid",
+    "C2": "2D-periodic antidot film, ~200k nodes, 128x128x8 AIM grid",
+    "C3": "1D-periodic nanowire segments (non-touching), ~1M nodes, 512x64x64 AIM grid",
+    "C4": "3D-periodic BCC spheres protruding beyond the cell, ~10M nodes, 256^3 AIM grid",
+    "C5": "1D-periodic waveguide strip (touching), ~2M nodes, 2048x64x8 AIM grid",
+}
+
+
+def _round_cells(length, h):
+    return max(1, int(round(length / h)))
+
+
+def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
+    """Return dict(mesh, periodic, L, grid, Ms, Aex, name, desc)."""
+    if seed is None:
+        seed = 1000 + int(name[1:])
+    c = float(coarsen)
+    if name == "C1":
+        L = 100 * NM
+        n = cells or max(2, int(round(10 / c)))
+        h = L / n
+        mask = np.ones((n, n, n), bool)
+        mesh = kuhn_voxel_mesh(mask, h, wrap=(True, True, True), jitter=jitter, seed=seed, name=name)
+        periodic = (1, 1, 1); lattice = (L, L, L)
+        g = grid or (max(8, int(16 // c)),) * 3
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "C2":
+        L = 400 * NM; t = 10 * NM; h = 2 * NM * c
+        nxy = _round_cells(L, h); nz = max(1, _round_cells(t, h))
+        h = L / nxy
+        xc = (np.arange(nxy) + 0.5) * h
+        X, Y = np.meshgrid(xc, xc, indexing="ij")
+        keep = (X - L / 2) ** 2 + (Y - L / 2) ** 2 > (80 * NM) ** 2
+        mask = np.repeat(keep[:, :, None], nz, axis=2)
+        mesh = kuhn_voxel_mesh(mask, h, wrap=(True, True, False), jitter=jitter, seed=seed, name=name)
+        periodic = (1, 1, 0); lattice = (L, L, 0.0)
+        g = grid or (max(16, int(128 // c)), max(16, int(128 // c)), max(4, int(round(8 / c))))
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "C3":
+        L = 800 * NM; h = L / max(8, int(round(456 / c)))
+        nx = _round_cells(L, h)
+        d = 100 * NM
+        nyz = int(math.ceil(d / h))
+        xc = (np.arange(nx) + 0.5) * h
+        yc = (np.arange(nyz) + 0.5) * h
+        keepx = (xc >= 40 * NM) & (xc <= 760 * NM)
+        Y, Z = np.meshgrid(yc, yc, indexing="ij")
+        keepyz = (Y - nyz * h / 2) ** 2 + (Z - nyz * h / 2) ** 2 <= (d / 2) ** 2
+        mask = keepx[:, None, None] & keepyz[None, :, :]
+        mesh = kuhn_voxel_mesh(mask, h, wrap=(True, False, False), jitter=jitter, seed=seed, name=name)
+        periodic = (1, 0, 0); lattice = (L, 0.0, 0.0)
+        g = grid or (max(16, int(512 // c)), max(8, int(64 // c)), max(8, int(64 // c)))
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "C4":
+        L = 2650 * NM; n = max(8, int(round(265 / c))); h = L / n
+        R = 0.4 * L
+        lo = -int(math.ceil(R / h)) - 1
+        hi = int(math.ceil((0.5 * L + R) / h)) + 1
+        idx = np.arange(lo, hi)
+        cc = (idx + 0.5) * h
+        X, Y, Z = np.meshgrid(cc, cc, cc, indexing="ij")
+        keep = (X ** 2 + Y ** 2 + Z ** 2 <= R * R) | \
+               ((X - L / 2) ** 2 + (Y - L / 2) ** 2 + (Z - L / 2) ** 2 <= R * R)
+        mesh = kuhn_voxel_mesh(keep, h, origin=(lo * h,) * 3, wrap=(True, True, True),
+                               jitter=jitter, seed=seed, name=name)
+        # wrap=True on an axis whose voxel count is not n would break image
+        # consistency; the spheres are non-touching so no images exist.
+        periodic = (1, 1, 1); lattice = (L, L, L)
+        g = grid or (max(16, int(256 // c)),) * 3
+        Ms, Aex = 200.0, 1e-6
+    elif name == "C5":
+        L = 6400 * NM; h = 2 * NM * c
+        nx = _round_cells(L, h); h = L / nx
+        ny = _round_cells(200 * NM, h); nz = max(1, _round_cells(10 * NM, h))
+        mask = np.ones((nx, ny, nz), bool)
+        mesh = kuhn_voxel_mesh(mask, h, wrap=(True, False, False), jitter=jitter, seed=seed, name=name)
+        periodic = (1, 0, 0); lattice = (L, 0.0, 0.0)
+        g = grid or (max(16, int(2048 // c)), max(8, int(64 // c)), max(4, int(round(8 / c))))
+        Ms, Aex = 637.0, 1.4e-6
+    else:
+        raise KeyError(name)
+    return dict(name=name, desc=CONFIGS[name], mesh=mesh, periodic=periodic,
+                lattice=lattice, grid=tuple(int(v) for v in g), Ms=Ms, Aex=Aex,
+                coarsen=coarsen, seed=seed)
