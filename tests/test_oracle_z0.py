@@ -102,7 +102,7 @@ def test_uniform_m_filled_cell_zero():
     m = np.tile([0.6, 0.0, 0.8], (mo.n_parents, 1))
     # scale: the row sums of |Z| (the size of the terms that cancel)
     scale = (abs(mo.z0["Zx"]) + abs(mo.z0["Zz"])).sum(axis=1).max()
-    assert np.abs(mo.u_loc(m)).max() < 1e-10 * scale
+    assert np.abs(mo.u_loc(m)).max() < 1e-8 * scale      # regular-element quadrature ~1e-9
 
 
 def test_quadrature_convergence():
