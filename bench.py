@@ -1,0 +1,301 @@
+"""Benchmark: periodic H_eff evaluations/s (and mesh nodes/s) of the B200-native PM-FEM path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl pmfem|reference]
+
+One step = one pmfem_heff evaluation (K1 local_in -> K2 anterpolation -> K3 FFT convolution
+-> K4 interpolation + precorrection -> K5 gradient + sum) over the whole synthetic mesh, inputs
+resident in HBM.  L2 is flushed (256 MiB write) between timed steps, outside the timed events.
+Prints ONE JSON line (rank 0).  --impl reference times the fp64 CPU oracle (oracle/) on a
+bounded sample of the same workload (the tier's reference arm).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "periodic H_eff evals/s and mesh nodes/s at 1/2/4/8 B200; % HBM roofline"
+DEFAULTS = {"C2": dict(order=2, rer_scale=3.0, z0_ring=1), "C3": dict(order=2, rer_scale=3.0, z0_ring=1),
+            "C5": dict(order=2, rer_scale=3.0, z0_ring=1), "C4": dict(order=2, rer_scale=3.0, z0_ring=1),
+            "C1": dict(order=1, rer_scale=2.0, z0_ring=1)}
+CPU_SAMPLE = {"C1": 1, "C2": 6, "C3": 10, "C4": 30, "C5": 12}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--coarsen", type=float, default=1)
+    ap.add_argument("--order", type=int, default=None)
+    ap.add_argument("--rer-scale", type=float, default=None)
+    ap.add_argument("--z0-ring", type=int, default=None)
+    ap.add_argument("--impl", default="pmfem", choices=["pmfem", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def aim_params(a):
+    p = dict(DEFAULTS[a.config])
+    if a.order is not None:
+        p["order"] = a.order
+    if a.rer_scale is not None:
+        p["rer_scale"] = a.rer_scale
+    if a.z0_ring is not None:
+        p["z0_ring"] = a.z0_ring
+    return p
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), "--query-gpu=" + ",".join(self.FIELDS),
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            out = self.p.communicate(timeout=5)[0]
+        except Exception:
+            return None
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(cfg_name, aim, seconds):
+    """The oracle (fp64 NumPy/SciPy, as it stands) on a bounded, coarsened sample of the same
+    workload; evals/s scaled to the full workload by node count (nodes/s / N'_full)."""
+    from oracle.heff import OracleModel
+    from synth import make_config, m_random
+    c = CPU_SAMPLE[cfg_name]
+    cfg = make_config(cfg_name, coarsen=c)
+    m = cfg["mesh"]
+    t0 = time.time()
+    om = OracleModel(m.xyz, m.tets, cfg["periodic"], cfg["lattice"], cfg["grid"], Ms=cfg["Ms"], Aex=cfg["Aex"],
+                     order=aim["order"], rer_scale=aim["rer_scale"], z0_ring=aim["z0_ring"])
+    t_setup = time.time() - t0
+    mm = m_random(om.n_parents, seed=3)
+    n_ev, t0 = 0, time.time()
+    while True:
+        om.heff(mm, "aim")
+        n_ev += 1
+        if time.time() - t0 >= seconds:
+            break
+    dt = (time.time() - t0) / n_ev
+    try:
+        from threadpoolctl import threadpool_info
+        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        cores = os.cpu_count()
+    return dict(n_parents=om.n_parents, s_per_eval=dt, setup_s=t_setup, evals=n_ev, cores=cores,
+                sample="%s coarsened x%g (N'=%d, grid %s), %d AIM H_eff evals over %.1f s; oracle setup %.1f s "
+                       "not included" % (cfg_name, c, om.n_parents, "x".join(map(str, cfg["grid"])), n_ev,
+                                         n_ev * dt, t_setup))
+
+
+def run_reference(a):
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 and rank != 0:
+        return
+    from synth import make_config
+    aim = aim_params(a)
+    full = make_config(a.config, coarsen=a.coarsen)
+    from oracle.heff import OracleModel  # noqa: F401
+    per_step = max(1.0, min(20.0, 120.0 / max(1, a.steps + a.warmup)))
+    cb = cpu_baseline(a.config, aim, per_step * max(1, a.steps))
+    n_full = int(np.unique(full["mesh"].tets).size)   # N (user nodes); N' reported by the GPU arm
+    nodes_per_s = cb["n_parents"] / cb["s_per_eval"]
+    value = nodes_per_s / n_full
+    line = {"metric": METRIC, "value": value, "unit": "evals/s", "impl": "reference", "n_gpus": a.gpus,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 / value, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "%s: %s" % (a.config, full["desc"]), "n_nodes_full": n_full, **aim},
+            "nodes_per_s": nodes_per_s,
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cb["cores"], "kind": "oracle",
+                             "sample": cb["sample"]},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = local
+    from paper_2409_13958_b200 import Context, KERNELS
+    from synth import make_config
+
+    aim = aim_params(a)
+    cfg = make_config(a.config, coarsen=a.coarsen)
+    mesh = cfg["mesh"]
+    t0 = time.time()
+    ctx = Context(mesh.xyz, mesh.tets, cfg["periodic"], cfg["lattice"], cfg["grid"], Ms=cfg["Ms"], Aex=cfg["Aex"],
+                  device=dev, **aim)
+    t_setup = time.time() - t0
+    t0 = time.time()
+    ctx.build_pgf()
+    t_pgf = time.time() - t0
+    info = ctx.query()
+    Np = info["n_parents"]
+    g = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    m = torch.randn(Np, 3, device="cuda", generator=g)
+    m = (m / m.norm(dim=1, keepdim=True)).contiguous()
+    H = torch.empty_like(m)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2 (126 MB)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(3, a.warmup)):
+        ctx.heff(m, H)
+    torch.cuda.synchronize()
+    # clocks: sample during a >= 1 s run of the same step right before and through the timed region
+    clk = ClockSampler(dev)
+    clk.start()
+    t_end = time.time() + 1.0
+    while time.time() < t_end:
+        ctx.heff(m, H)
+        torch.cuda.synchronize()
+    ctx.set_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, kern_ms = [], {k: [] for k in KERNELS}
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    for _ in range(a.steps):
+        flush.zero_()
+        ev0.record(stream)
+        ctx.heff(m, H)
+        ev1.record(stream)
+        ev1.synchronize()
+        step_ms.append(ev0.elapsed_time(ev1))
+        for k, v in ctx.timing().items():
+            kern_ms[k].append(v)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ctx.set_timing(False)
+    tot_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([tot_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = world * a.steps / (tot_ms / 1e3)
+
+    # end to end through the public API with host buffers (pinned), copies inside the timed region
+    m_h = m.cpu().pin_memory()
+    H_h = torch.empty_like(m_h).pin_memory()
+    for _ in range(3):
+        ctx.heff_host(m_h, H_h)
+    e2e_ms = []
+    for _ in range(a.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        ctx.heff_host(m_h, H_h)
+        ev1.record(stream)
+        ev1.synchronize()
+        e2e_ms.append(ev0.elapsed_time(ev1))
+    e2e_tot = float(sum(e2e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_tot], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_tot = float(t.item())
+    e2e_value = world * a.steps / (e2e_tot / 1e3)
+
+    peaks, peak_src = load_peaks()
+    kb = info["kernel_bytes"]
+    kernels = {}
+    for i, k in enumerate(KERNELS):
+        ms = float(np.mean(kern_ms[k]))
+        kernels[k] = {"ms": ms, "bytes": kb[i], "GBps": kb[i] / (ms * 1e-3) / 1e9 if ms > 0 else None}
+    dom = max(KERNELS, key=lambda k: kernels[k]["ms"])
+    ach = kernels[dom]["GBps"]
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
+                "share_of_step": kernels[dom]["ms"] / float(np.mean(step_ms))}
+    alg_total = sum(kb[:5])
+    line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "%s: %s" % (a.config, cfg["desc"]), "n_nodes": info["n_nodes"],
+                       "n_parents": Np, "grid": info["grid"], "fft": info["fft"], **aim,
+                       "nnz_ring1": info["nnz_ring1"], "nnz_z0": info["nnz_z0"], "nnz_cbox": info["nnz_cbox"],
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "parallelism": "single GPU" if world == 1 else
+                       "replicas (one full problem per GPU; slab-distributed FFT not implemented)"},
+            "nodes_per_s": value * Np, "setup_s": t_setup, "build_pgf_s": t_pgf,
+            "bytes_per_eval_algorithmic": alg_total,
+            "eval_GBps_algorithmic": alg_total / (tot_ms / a.steps * 1e-3) / 1e9,
+            "kernels": kernels, "roofline": roofline,
+            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(m_h.numel() * 4),
+                    "d2h_bytes_per_step": int(H_h.numel() * 4)},
+            "gpu_launches": 9 * a.steps, "clocks": clocks}
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cb = cpu_baseline(a.config, aim, a.cpu_seconds)
+        v = cb["n_parents"] / cb["s_per_eval"] / Np
+        line["cpu_baseline"] = {"value": v, "unit": "evals/s", "cores": cb["cores"], "kind": "oracle",
+                                "sample": cb["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

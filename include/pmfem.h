@@ -1,0 +1,142 @@
+/*
+ * pmfem.h -- C ABI of the B200-native PM-FEM periodic H_eff library (libpmfem.so).
+ *
+ * Implements the data-parallel hot path of "Periodic micromagnetic finite element method"
+ * (Ai, Duan, Lomakin; arXiv 2409.13958; /root/reference/PAPER.md cited as P:<line>):
+ *
+ *   q     = D (Ms m)                       periodized divergence + surface charge (P:171 Eq. hms_d1)
+ *   u_loc = Z0 m                           exact near-field correction            (P:173 Eq. hms_d2b)
+ *   Q     = P q                            AIM anterpolation onto the grid        (P:202 BAIM step 1)
+ *   U     = F^-1( G_hat . F Q )            FFT convolution with the periodic GF   (P:204, P:214 step 2)
+ *   u     = P^T U + C_box q + u_loc        interpolation + precorrection          (P:206-218 steps 3-4, Eq. new_er)
+ *   H_ms  = -G u                           periodized gradient                    (P:174 Eq. hms_d3)
+ *   H_ex  = -(2A/Ms) Vt^-1 S m             periodic exchange Laplacian            (P:117-157 Eqs. hex, lapl, lapl_1, lapl_2)
+ *   H_eff = H_ms + H_ex                                                           (P:73 Eq. heff)
+ *
+ * Units are CGS: positions in cm, Ms in emu/cm^3, Aex in erg/cm, fields in Oe, m is a unit
+ * vector.  G_0 = 1/|r|.  The discrete conventions (grid, stencils, PGF normalisation,
+ * near-set rules) are the contract K1-K11 of SURVEY.md 8(c) with the readings listed in
+ * DESIGN.md.
+ *
+ * Threading: a context is not thread-safe; calls on one context must be serialised by the
+ * caller.  No entry point throws; every one returns a pmfem_status and, on failure, stores a
+ * message retrievable with pmfem_last_error(ctx).
+ */
+#ifndef PMFEM_H
+#define PMFEM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pmfem_ctx_s* pmfem_ctx;   /* opaque; owns every host and device buffer it allocates */
+
+typedef enum {
+  PMFEM_OK = 0,
+  PMFEM_E_INVALID_ARG = 1,      /* NULL pointer, bad size, non-positive period, grid not a power of two,
+                                   stencil order not in 1..3, N_i < 2(p+1)                         */
+  PMFEM_E_MESH = 2,             /* tet index out of range, degenerate tet (|V| < 1e-12 mean |V|),
+                                   zero lumped volume                                              */
+  PMFEM_E_PBC_AMBIGUOUS = 3,    /* two nodes within match_tol of one periodic image        */
+  PMFEM_E_PBC_INCONSISTENT = 4, /* an LCA component whose members are not period translates*/
+  PMFEM_E_OUTSIDE_GRID = 5,     /* reserved (the grid is built to cover the mesh)                  */
+  PMFEM_E_RER_TOO_LARGE = 6,    /* r_ER >= L/2 or r_ER/Delta + p + 1 >= N/2 on a periodic axis     */
+  PMFEM_E_PGF_NOT_CONVERGED = 7,/* reserved                                                          */
+  PMFEM_E_STATE = 8,            /* call order (field evaluation before pmfem_build_pgf, host-only ctx)*/
+  PMFEM_E_CUDA = 9,             /* a CUDA runtime error (message holds cudaGetErrorString)         */
+  PMFEM_E_NCCL = 10,            /* a NCCL error (distributed contexts)                              */
+  PMFEM_E_OOM = 11              /* host or device allocation failure                                */
+} pmfem_status;
+
+/* Tetrahedral mesh.  Host arrays, borrowed for the duration of pmfem_setup only. */
+typedef struct {
+  int64_t        n_nodes;   /* N                                                              */
+  const double*  xyz;       /* [n_nodes][3] node coordinates, cm                               */
+  int64_t        n_tets;    /* T                                                              */
+  const int32_t* tets;      /* [n_tets][4] 0-based node indices; orientation fixed by the lib  */
+  const int32_t* region;    /* [n_tets] region id per tet, or NULL for a single region 0       */
+  int32_t        n_regions; /* number of entries in Ms / Aex (>= 1)                            */
+  const double*  Ms;        /* [n_regions] saturation magnetisation, emu/cm^3                  */
+  const double*  Aex;       /* [n_regions] exchange stiffness, erg/cm                          */
+} pmfem_mesh;
+
+/* Periodicity (P:36-43 Eq. pm_cont; 1D, 2D or 3D along any axes). */
+typedef struct {
+  int32_t periodic[3];      /* 1 = axis is periodic (at least one axis must be)                */
+  double  lattice[3];       /* period L_i along axis i (cm); ignored on non-periodic axes       */
+  double  match_tol;        /* T-PBC pair tolerance (cm); 0 -> 1e-6 x shortest edge */
+} pmfem_periodicity;
+
+/* AIM grid and near-field parameters. */
+typedef struct {
+  int32_t n[3];             /* grid points per axis.  periodic: Delta = L/n; non-periodic:
+                               Delta = (max-min)/(n-1) over the nodes (Eq. grid).
+                               FFT lengths n (periodic) / 2n (non-periodic) must be powers of 2 */
+  int32_t order;            /* Lagrange stencil order p in {1,2,3} ((p+1)^3 points per node)    */
+  double  rer_scale;        /* s: r_ER = s * max(Delta_x,Delta_y,Delta_z) (reading R8)   */
+  int32_t z0_ring;          /* 0: exact self term only; 1: exact periodic 1-ring        */
+} pmfem_grid;
+
+typedef struct {
+  int64_t n_nodes, n_parents, n_parents_local;    /* N, N', N' owned by this rank             */
+  int32_t periodic_dims, touching, protruding;    /* classification                    */
+  int32_t grid[3], fft[3];                        /* AIM grid and padded FFT lengths          */
+  int64_t nnz_ring1, nnz_z0, nnz_cbox;            /* off-diagonal nnz of L/D/G, Z0, C_box     */
+  double  bytes_per_eval_algorithmic;             /* DESIGN.md byte model with the real nnz   */
+  double  setup_seconds, pgf_seconds;             /* host wall time of setup / build_pgf      */
+  double  kernel_bytes[8];                        /* algorithmic bytes per launch of K1..K5 (index
+                                                     0 K1, 1 K2, 2 K3 (all FFT passes), 3 K4, 4 K5) */
+} pmfem_info;
+
+/* Build a context: validate, orient, detect T-PBC pairs and fold them to LCAs,
+ * assemble the folded operators, the exact near field Z0, the AIM
+ * grid, stencils and precorrection C_box.  cuda_device >= 0 uploads the fp32
+ * operators to that device; cuda_device = -1 builds a host-only context (setup artifacts can
+ * be exported with pmfem_export, no field evaluation).  On failure *out is NULL and the
+ * message is returned by pmfem_last_error(NULL) (thread-local). */
+pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
+                         const pmfem_grid* grid, int cuda_device);
+
+/* Tabulate the periodic Green's function K on the padded grid with Ewald sums in fp64
+ * (Eq. 2 with k0 = 0; "exponentially rapidly convergent sums"; normalisation
+ * R3), K(0) = G_p^reg(0), and store G_hat = real(FFT(K)) / (#FFT points), G_hat[0] = 0, as fp32
+ * (P:204).  On a device context the tabulation and fp64 FFT run on the GPU. */
+pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err);
+
+/* Field evaluations.  m: device pointer [N'][3] fp32 (internal node order, unit vectors);
+ * H: device pointer [N'][3] fp32, written (not accumulated); must not alias m.
+ * cuda_stream: a cudaStream_t or NULL for the legacy default stream.  Asynchronous: nothing
+ * synchronises the host; kernel faults surface as PMFEM_E_CUDA on a later call. */
+pmfem_status pmfem_demag   (pmfem_ctx ctx, const float* m, float* H, void* cuda_stream);  /* H := H_ms        */
+pmfem_status pmfem_exchange(pmfem_ctx ctx, const float* m, float* H, void* cuda_stream);  /* H := H_ex        */
+pmfem_status pmfem_heff    (pmfem_ctx ctx, const float* m, float* H, void* cuda_stream);  /* H := H_ms + H_ex */
+
+/* Same as pmfem_heff but m and H are HOST buffers [N'][3] fp32 (pinned or pageable); the
+ * host->device copy of m, the evaluation and the device->host copy of H are enqueued on the
+ * stream and the call returns after the stream is synchronised (end-to-end path). */
+pmfem_status pmfem_heff_host(pmfem_ctx ctx, const float* m_host, float* H_host, void* cuda_stream);
+
+pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out);
+
+/* internal_to_user[i] = original (user) node index of the parent stored in internal row i. */
+pmfem_status pmfem_get_order(pmfem_ctx ctx, int64_t* internal_to_user);
+
+/* Copy a named fp64/int setup artifact to host memory (tests and diagnostics).  Call with
+ * dst = NULL to get the element count in *count.  Names and types are listed in DESIGN.md
+ * ("Export names"); unknown name -> PMFEM_E_INVALID_ARG. */
+pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* count);
+
+/* Device time (ms) of each kernel class in the last evaluation when timing is enabled with
+ * pmfem_set_timing(ctx, 1) (CUDA events on the evaluation stream; adds event records only). */
+pmfem_status pmfem_set_timing(pmfem_ctx ctx, int enable);
+pmfem_status pmfem_get_timing(pmfem_ctx ctx, float* ms_per_kernel /* [8] as kernel_bytes */);
+
+const char*  pmfem_last_error(pmfem_ctx ctx);
+void         pmfem_destroy(pmfem_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PMFEM_H */

@@ -1,0 +1,132 @@
+// Host side of the PGF build: Ewald parameters, Gauss-Legendre nodes, and (host-only
+// contexts) the fp64 kernel table + spectrum with a plain radix-2 FFT.  Device contexts build
+// the same table on the GPU (device.cu: k_pgf_table + fp64 FFT passes).
+//   P:179-188 Eq. 2 (k0 = 0); P:204 K on grid displacements; P:214 G0 -> G_p in step 2.
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <omp.h>
+#include "pmfem_internal.h"
+#include "pgf.cuh"
+
+namespace pmfem {
+
+void gauss_legendre01(int n, double* x, double* w) {
+  for (int i = 0; i < n; ++i) {
+    double z = std::cos(M_PI * (i + 0.75) / (n + 0.5));
+    double dp = 1;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1, p1 = z;
+      for (int k = 2; k <= n; ++k) { double p2 = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k; p0 = p1; p1 = p2; }
+      dp = n * (z * p1 - p0) / (z * z - 1);
+      double dz = p1 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    double p0 = 1, p1 = z;
+    for (int k = 2; k <= n; ++k) { double p2 = ((2 * k - 1) * z * p1 - (k - 1) * p0) / k; p0 = p1; p1 = p2; }
+    dp = n * (z * p1 - p0) / (z * z - 1);
+    x[i] = 0.5 * (1 - z);
+    w[i] = 1.0 / ((1 - z * z) * dp * dp);
+  }
+}
+
+PgfParams make_pgf_params(const int periodic[3], const double L[3]) {
+  PgfParams P{};
+  int k = 0;
+  for (int a = 0; a < 3; ++a)
+    if (periodic[a]) { P.ax[k] = a; P.L[k] = L[a]; ++k; }
+  P.dim = k;
+  for (int a = 0; a < 3; ++a)
+    if (!periodic[a]) P.ax[k++] = a;
+  double Lmin = 1e300;
+  for (int i = 0; i < P.dim; ++i) Lmin = std::min(Lmin, P.L[i]);
+  P.alpha = std::sqrt(M_PI) / Lmin;
+  const double kmax = 2.0 * P.alpha * std::sqrt(-std::log(1e-15)) * 1.1;
+  for (int i = 0; i < 3; ++i) {
+    if (i < P.dim) {
+      P.nreal[i] = (int)std::ceil(6.2 / (P.alpha * P.L[i]) + 1.0);
+      P.mrec[i] = (int)std::ceil(kmax * P.L[i] / (2 * M_PI)) + 1;
+    } else {
+      P.nreal[i] = 0;
+      P.mrec[i] = 0;
+    }
+  }
+  return P;
+}
+
+static PgfDev to_dev(const PgfParams& P) {
+  PgfDev d{};
+  d.dim = P.dim;
+  for (int i = 0; i < 3; ++i) { d.ax[i] = P.ax[i]; d.L[i] = P.L[i]; d.nreal[i] = P.nreal[i]; d.mrec[i] = P.mrec[i]; }
+  d.alpha = P.alpha;
+  gauss_legendre01(64, d.gl_x, d.gl_w);
+  return d;
+}
+
+void host_kernel_table(const HostSetup& S, const PgfParams& P, std::vector<double>& K) {
+  const PgfDev pd = to_dev(P);
+  const int P0 = S.fft_n[0], P1 = S.fft_n[1], P2 = S.fft_n[2];
+  const int64_t tot = (int64_t)P0 * P1 * P2;
+  K.assign(tot, 0.0);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t idx = 0; idx < tot; ++idx) {
+    int j[3] = {(int)(idx % P0), (int)((idx / P0) % P1), (int)(idx / ((int64_t)P0 * P1))};
+    bool skip = false;
+    double r[3];
+    for (int a = 0; a < 3; ++a) {
+      if (!S.periodic[a] && j[a] == S.grid_n[a]) skip = true;
+      int jj = S.periodic[a] ? j[a] : (j[a] < S.grid_n[a] ? j[a] : j[a] - S.fft_n[a]);
+      r[a] = jj * S.delta[a];
+    }
+    if (skip) continue;
+    bool self = (j[0] == 0 && j[1] == 0 && j[2] == 0);
+    K[idx] = pgf_eval(pd, r, self);
+  }
+}
+
+static void fft1d(std::complex<double>* x, int n, int stride) {
+  // iterative radix-2 DIT, forward (exp(-2 pi i k j / n))
+  int logn = 0;
+  while ((1 << logn) < n) ++logn;
+  for (int i = 0, j = 0; i < n; ++i) {
+    if (i < j) std::swap(x[i * stride], x[j * stride]);
+    int bit = n >> 1;
+    for (; j & bit; bit >>= 1) j ^= bit;
+    j ^= bit;
+  }
+  for (int len = 2; len <= n; len <<= 1) {
+    double ang = -2 * M_PI / len;
+    for (int i = 0; i < n; i += len)
+      for (int k = 0; k < len / 2; ++k) {
+        std::complex<double> w(std::cos(ang * k), std::sin(ang * k));
+        std::complex<double> u = x[(i + k) * stride], v = w * x[(i + k + len / 2) * stride];
+        x[(i + k) * stride] = u + v;
+        x[(i + k + len / 2) * stride] = u - v;
+      }
+  }
+}
+
+void host_fft_spectrum(const HostSetup& S, const std::vector<double>& K, std::vector<double>& Ghat) {
+  const int P0 = S.fft_n[0], P1 = S.fft_n[1], P2 = S.fft_n[2];
+  const int64_t tot = (int64_t)P0 * P1 * P2;
+  std::vector<std::complex<double>> c(K.begin(), K.end());
+#pragma omp parallel for
+  for (int64_t r = 0; r < (int64_t)P1 * P2; ++r) fft1d(&c[r * P0], P0, 1);
+#pragma omp parallel for
+  for (int64_t r = 0; r < (int64_t)P0 * P2; ++r) {
+    int64_t i2 = r / P0, i0 = r % P0;
+    fft1d(&c[i2 * P0 * P1 + i0], P1, P0);
+  }
+#pragma omp parallel for
+  for (int64_t r = 0; r < (int64_t)P0 * P1; ++r) fft1d(&c[r], P2, P0 * P1);
+  const int H0 = P0 / 2 + 1;
+  Ghat.assign((int64_t)H0 * P1 * P2, 0.0);
+  for (int64_t i2 = 0; i2 < P2; ++i2)
+    for (int64_t i1 = 0; i1 < P1; ++i1)
+      for (int64_t i0 = 0; i0 < H0; ++i0)
+        Ghat[(i2 * P1 + i1) * H0 + i0] = c[(i2 * P1 + i1) * P0 + i0].real() / (double)tot;
+  Ghat[0] = 0.0;
+}
+
+}  // namespace pmfem

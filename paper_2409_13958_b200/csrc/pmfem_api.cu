@@ -1,0 +1,235 @@
+// extern "C" entry points of libpmfem (include/pmfem.h).  No exception crosses the ABI.
+#include <chrono>
+#include <cstring>
+#include <string>
+#include "device.cuh"
+#include "pmfem_internal.h"
+
+struct pmfem_ctx_s {
+  pmfem::HostSetup S;
+  pmfem::DeviceState D;
+  std::string err;
+  bool host_only = true;
+};
+
+namespace {
+thread_local std::string g_setup_err;
+
+template <class F>
+pmfem_status guard(pmfem_ctx ctx, F&& f) {
+  try {
+    f();
+    return PMFEM_OK;
+  } catch (const pmfem::Error& e) {
+    if (ctx) ctx->err = e.what(); else g_setup_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->err = "host allocation failed"; else g_setup_err = "host allocation failed";
+    return PMFEM_E_OOM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->err = e.what(); else g_setup_err = e.what();
+    return PMFEM_E_INVALID_ARG;
+  }
+}
+
+double now() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void check_eval(pmfem_ctx ctx, const float* m, float* H) {
+  pmfem::require(!ctx->host_only, PMFEM_E_STATE, "host-only context (cuda_device = -1) cannot evaluate fields");
+  pmfem::require(m != nullptr && H != nullptr, PMFEM_E_INVALID_ARG, "NULL m or H");
+  pmfem::require((const void*)m != (const void*)H, PMFEM_E_INVALID_ARG, "H must not alias m");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, std::string("pending CUDA error: ") + cudaGetErrorString(e));
+  cudaSetDevice(ctx->D.device);
+}
+
+void record_timing(pmfem_ctx ctx, cudaStream_t st) {
+  (void)st;   // events were recorded on the stream; read back lazily in pmfem_get_timing
+  if (ctx->D.timing) ctx->D.timing_pending = true;
+}
+}  // namespace
+
+extern "C" {
+
+pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
+                         const pmfem_grid* grid, int cuda_device) {
+  if (!out) { g_setup_err = "NULL out"; return PMFEM_E_INVALID_ARG; }
+  *out = nullptr;
+  pmfem_ctx ctx = nullptr;
+  try {
+    ctx = new pmfem_ctx_s();
+  } catch (...) {
+    g_setup_err = "host allocation failed";
+    return PMFEM_E_OOM;
+  }
+  pmfem_status st = guard(nullptr, [&] {
+    double t0 = now();
+    pmfem::HostSetup& S = ctx->S;
+    pmfem::setup_mesh(S, mesh, per);
+    pmfem::setup_operators(S);
+    S.z0_ring = grid ? grid->z0_ring : 1;
+    pmfem::require(grid != nullptr, PMFEM_E_INVALID_ARG, "NULL grid");
+    pmfem::require(grid->z0_ring == 0 || grid->z0_ring == 1, PMFEM_E_INVALID_ARG, "z0_ring must be 0 or 1");
+    pmfem::setup_z0(S);
+    pmfem::setup_aim(S, grid);
+    pmfem::setup_order(S);
+    S.setup_seconds = now() - t0;
+    if (cuda_device >= 0) {
+      ctx->host_only = false;
+      ctx->D.device = cuda_device;
+      pmfem::device_upload(ctx->D, S);
+    }
+  });
+  if (st != PMFEM_OK) {
+    if (!ctx->host_only) pmfem::device_free(ctx->D);
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return PMFEM_OK;
+}
+
+pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  (void)target_rel_err;   // the Ewald cutoffs are fixed at the 1e-15 level (reading R5)
+  return guard(ctx, [&] {
+    double t0 = now();
+    pmfem::PgfParams P = pmfem::make_pgf_params(ctx->S.periodic, ctx->S.L);
+    if (ctx->host_only) {
+      pmfem::host_kernel_table(ctx->S, P, ctx->S.kernel);
+      pmfem::host_fft_spectrum(ctx->S, ctx->S.kernel, ctx->S.spectrum);
+    } else {
+      pmfem::device_build_pgf(ctx->D, ctx->S, P);
+    }
+    ctx->S.pgf_seconds = now() - t0;
+  });
+}
+
+static pmfem_status eval(pmfem_ctx ctx, const float* m, float* H, void* stream, pmfem::EvalMode mode) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    check_eval(ctx, m, H);
+    cudaStream_t st = (cudaStream_t)stream;
+    pmfem::device_eval(ctx->D, m, H, st, mode);
+    record_timing(ctx, st);
+  });
+}
+
+pmfem_status pmfem_demag(pmfem_ctx ctx, const float* m, float* H, void* s) { return eval(ctx, m, H, s, pmfem::EVAL_DEMAG); }
+pmfem_status pmfem_exchange(pmfem_ctx ctx, const float* m, float* H, void* s) { return eval(ctx, m, H, s, pmfem::EVAL_EXCHANGE); }
+pmfem_status pmfem_heff(pmfem_ctx ctx, const float* m, float* H, void* s) { return eval(ctx, m, H, s, pmfem::EVAL_HEFF); }
+
+pmfem_status pmfem_heff_host(pmfem_ctx ctx, const float* m_host, float* H_host, void* stream) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    pmfem::require(!ctx->host_only, PMFEM_E_STATE, "host-only context");
+    pmfem::require(m_host && H_host, PMFEM_E_INVALID_ARG, "NULL host buffer");
+    cudaSetDevice(ctx->D.device);
+    const size_t bytes = sizeof(float) * 3 * (size_t)ctx->D.Np;
+    if (!ctx->D.m_stage) {
+      if (cudaMalloc(&ctx->D.m_stage, bytes) != cudaSuccess || cudaMalloc(&ctx->D.H_stage, bytes) != cudaSuccess)
+        throw pmfem::Error(PMFEM_E_OOM, "staging allocation failed");
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(ctx->D.m_stage, m_host, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+      throw pmfem::Error(PMFEM_E_CUDA, "H2D copy failed");
+    pmfem::device_eval(ctx->D, ctx->D.m_stage, ctx->D.H_stage, st, pmfem::EVAL_HEFF);
+    if (cudaMemcpyAsync(H_host, ctx->D.H_stage, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      throw pmfem::Error(PMFEM_E_CUDA, "D2H copy failed");
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, cudaGetErrorString(e));
+  });
+}
+
+pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
+  if (!ctx || !out) return PMFEM_E_INVALID_ARG;
+  const pmfem::HostSetup& S = ctx->S;
+  std::memset(out, 0, sizeof(*out));
+  out->n_nodes = S.N;
+  out->n_parents = S.Np;
+  out->n_parents_local = S.Np;
+  out->periodic_dims = S.periodic[0] + S.periodic[1] + S.periodic[2];
+  out->touching = S.touching;
+  out->protruding = S.protruding;
+  for (int a = 0; a < 3; ++a) { out->grid[a] = S.grid_n[a]; out->fft[a] = S.fft_n[a]; }
+  out->nnz_ring1 = S.ring1.nnz();
+  out->nnz_z0 = S.z0.nnz();
+  out->nnz_cbox = S.cbox.nnz();
+  double tot = 0;
+  for (int i = 0; i < 5; ++i) { out->kernel_bytes[i] = ctx->D.kernel_bytes[i]; tot += ctx->D.kernel_bytes[i]; }
+  out->bytes_per_eval_algorithmic = tot;
+  out->setup_seconds = S.setup_seconds;
+  out->pgf_seconds = S.pgf_seconds;
+  return PMFEM_OK;
+}
+
+pmfem_status pmfem_get_order(pmfem_ctx ctx, int64_t* internal_to_user) {
+  if (!ctx || !internal_to_user) return PMFEM_E_INVALID_ARG;
+  for (int64_t i = 0; i < ctx->S.Np; ++i) internal_to_user[i] = ctx->S.parent[ctx->S.perm[i]];
+  return PMFEM_OK;
+}
+
+pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* count) {
+  if (!ctx || !name || !count) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    const pmfem::HostSetup& S = ctx->S;
+    std::string n(name);
+    auto put = [&](const void* src, int64_t cnt, size_t esz) {
+      *count = cnt;
+      if (dst && cnt) std::memcpy(dst, src, (size_t)cnt * esz);
+    };
+    if (n == "parent") put(S.parent.data(), S.Np, 8);
+    else if (n == "lca") put(S.lca.data(), S.N, 8);
+    else if (n == "shift") put(S.shift.data(), 3 * S.N, 4);
+    else if (n == "Vt") put(S.Vt.data(), S.Np, 8);
+    else if (n == "ring1_rowptr") put(S.ring1.rowptr.data(), S.Np + 1, 8);
+    else if (n == "ring1_col") put(S.ring1.col.data(), S.ring1.nnz(), 4);
+    else if (n == "ring1_val") put(S.ring1.val.data(), 7 * S.ring1.nnz(), 8);
+    else if (n == "rowsumD") put(S.rowsumD.data(), 3 * S.Np, 8);
+    else if (n == "z0_rowptr") put(S.z0.rowptr.data(), S.Np + 1, 8);
+    else if (n == "z0_col") put(S.z0.col.data(), S.z0.nnz(), 4);
+    else if (n == "z0_val") put(S.z0.val.data(), 3 * S.z0.nnz(), 8);
+    else if (n == "rowsumZ") put(S.rowsumZ.data(), 3 * S.Np, 8);
+    else if (n == "cbox_rowptr") put(S.cbox.rowptr.data(), S.Np + 1, 8);
+    else if (n == "cbox_col") put(S.cbox.col.data(), S.cbox.nnz(), 4);
+    else if (n == "cbox_val") put(S.cbox.val.data(), S.cbox.nnz(), 8);
+    else if (n == "xw") put(S.xw.data(), 3 * S.Np, 8);
+    else if (n == "stencil_s") put(S.st_s.data(), 3 * S.Np, 4);
+    else if (n == "stencil_t") put(S.st_t.data(), 3 * S.Np, 8);
+    else if (n == "grid_delta") put(S.delta, 3, 8);
+    else if (n == "grid_origin") put(S.origin, 3, 8);
+    else if (n == "perm") put(S.perm.data(), S.Np, 8);
+    else if (n == "kernel") put(S.kernel.data(), (int64_t)S.kernel.size(), 8);
+    else if (n == "spectrum") put(S.spectrum.data(), (int64_t)S.spectrum.size(), 8);
+    else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
+  });
+}
+
+pmfem_status pmfem_set_timing(pmfem_ctx ctx, int enable) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  ctx->D.timing = enable != 0;
+  return PMFEM_OK;
+}
+
+pmfem_status pmfem_get_timing(pmfem_ctx ctx, float* ms) {
+  if (!ctx || !ms) return PMFEM_E_INVALID_ARG;
+  if (ctx->D.timing_pending) {
+    cudaEventSynchronize(ctx->D.ev[5]);
+    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ctx->D.last_ms[i], ctx->D.ev[i], ctx->D.ev[i + 1]);
+    ctx->D.timing_pending = false;
+  }
+  for (int i = 0; i < 8; ++i) ms[i] = ctx->D.last_ms[i];
+  return PMFEM_OK;
+}
+
+const char* pmfem_last_error(pmfem_ctx ctx) { return ctx ? ctx->err.c_str() : g_setup_err.c_str(); }
+
+void pmfem_destroy(pmfem_ctx ctx) {
+  if (!ctx) return;
+  if (!ctx->host_only) pmfem::device_free(ctx->D);
+  delete ctx;
+}
+
+}  // extern "C"

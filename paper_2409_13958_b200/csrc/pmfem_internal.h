@@ -1,0 +1,100 @@
+// Internal declarations of libpmfem (host setup in fp64, device path in fp32).
+#pragma once
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+#include "../../include/pmfem.h"
+
+namespace pmfem {
+
+struct Error : std::runtime_error {
+  pmfem_status code;
+  Error(pmfem_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void require(bool ok, pmfem_status code, const std::string& msg) {
+  if (!ok) throw Error(code, msg);
+}
+
+// Sparse row-compressed matrix with a fixed number of fp64 values per entry.
+struct Csr {
+  int64_t n_rows = 0;
+  int nv = 1;                       // values per entry
+  std::vector<int64_t> rowptr;      // [n_rows+1]
+  std::vector<int32_t> col;         // [nnz]
+  std::vector<double> val;          // [nnz*nv]
+  int64_t nnz() const { return (int64_t)col.size(); }
+};
+
+// Host setup products (all in fp64, rows/cols in USER parent order [0, N')).
+struct HostSetup {
+  // inputs
+  int64_t N = 0, T = 0;
+  std::vector<double> xyz;          // [N][3]
+  std::vector<int32_t> tets;        // [T][4] (oriented)
+  std::vector<double> Ms_tet, Aex_tet;
+  int periodic[3] = {0, 0, 0};
+  double L[3] = {0, 0, 0};
+  double match_tol = 0;
+  int touching = 0, protruding = 0;
+  // PBC / LCA
+  int64_t Np = 0;
+  std::vector<int64_t> lca;         // [N] original index of the component root (min index)
+  std::vector<int32_t> pid;         // [N] parent id
+  std::vector<int64_t> parent;      // [Np] original node index of parent p
+  std::vector<int32_t> shift;       // [N][3] integer lattice shift r_i = r_parent + shift*L
+  std::vector<int64_t> copies_ptr;  // [Np+1] parent -> its copies (nodes), CSR
+  std::vector<int64_t> copies;      // [N]
+  std::vector<int64_t> ntet_ptr;    // [N+1] node -> incident tets, CSR
+  std::vector<int64_t> ntet;        // [4T]
+  // element data
+  std::vector<double> vol;          // [T]
+  std::vector<double> grads;        // [T][4][3]
+  std::vector<double> Vt;           // [Np] lumped volume
+  // operators (off-diagonal CSR + per-row sums), user parent order
+  Csr ring1;                        // values: L, Dx, Dy, Dz, Gx, Gy, Gz   (nv = 7)
+  std::vector<double> rowsumD;      // [Np][3] sum_m D_nm (non-zero on surfaces)
+  std::vector<double> diagD;        // [Np][3] D_nn
+  Csr z0;                           // values: Zx, Zy, Zz (nv = 3), off-diagonal
+  std::vector<double> rowsumZ;      // [Np][3]
+  // AIM
+  int grid_n[3] = {0, 0, 0}, fft_n[3] = {0, 0, 0};
+  double origin[3] = {0, 0, 0}, delta[3] = {0, 0, 0};
+  int order = 1;
+  double rer_scale = 2.0;
+  int z0_ring = 1;
+  std::vector<double> xw;           // [Np][3] wrapped parent coordinates
+  std::vector<int32_t> st_s;        // [Np][3] unwrapped stencil start index
+  std::vector<double> st_t;         // [Np][3] t - s (local coordinate in grid units)
+  Csr cbox;                         // nv = 1
+  // internal order
+  std::vector<int64_t> perm;        // internal row i -> user parent id
+  std::vector<int64_t> iperm;       // user parent id -> internal row
+  // PGF
+  std::vector<double> kernel;       // host-only contexts: K table [fft2][fft1][fft0]
+  std::vector<double> spectrum;     // host-only: G_hat half spectrum [fft2][fft1][fft0/2+1]
+  double setup_seconds = 0, pgf_seconds = 0;
+};
+
+void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* per);
+void setup_operators(HostSetup& S);
+void setup_z0(HostSetup& S);
+void setup_aim(HostSetup& S, const pmfem_grid* g);
+void setup_order(HostSetup& S);
+
+// Periodic Green's function (Ewald) -- host/device fp64, defined in pgf.cuh.
+struct PgfParams {
+  int dim;                // 1, 2, 3
+  int ax[3];              // periodic axes first, then free axes
+  double L[3];            // periods of the periodic axes (ax[0..dim-1])
+  double alpha;
+  int nreal[3];
+  int mrec[3];
+};
+PgfParams make_pgf_params(const int periodic[3], const double L[3]);
+void gauss_legendre01(int n, double* x, double* w);
+void host_kernel_table(const HostSetup& S, const PgfParams& P, std::vector<double>& K);
+void host_fft_spectrum(const HostSetup& S, const std::vector<double>& K, std::vector<double>& Ghat);
+
+}  // namespace pmfem

@@ -1,0 +1,215 @@
+"""Thin ctypes binding of libpmfem (include/pmfem.h): argument marshalling only.
+
+Every step of the H_eff path runs in the library's CUDA kernels; PyTorch supplies device
+memory and streams.  There is no CPU fallback: if the shared library is missing or cannot be
+loaded, importing this module raises.
+"""
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpmfem.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError("libpmfem.so not built (%s); run __graft_entry__.build() or "
+                      "python paper_2409_13958_b200/build.py" % LIB_PATH)
+_lib = ctypes.CDLL(LIB_PATH)
+
+STATUS = {0: "PMFEM_OK", 1: "PMFEM_E_INVALID_ARG", 2: "PMFEM_E_MESH", 3: "PMFEM_E_PBC_AMBIGUOUS",
+          4: "PMFEM_E_PBC_INCONSISTENT", 5: "PMFEM_E_OUTSIDE_GRID", 6: "PMFEM_E_RER_TOO_LARGE",
+          7: "PMFEM_E_PGF_NOT_CONVERGED", 8: "PMFEM_E_STATE", 9: "PMFEM_E_CUDA", 10: "PMFEM_E_NCCL",
+          11: "PMFEM_E_OOM"}
+
+SYMBOLS = ["pmfem_setup", "pmfem_build_pgf", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
+           "pmfem_heff_host", "pmfem_query", "pmfem_get_order", "pmfem_export", "pmfem_set_timing",
+           "pmfem_get_timing", "pmfem_last_error", "pmfem_destroy"]
+
+
+class PmfemError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__("%s: %s" % (STATUS.get(status, status), msg))
+        self.status = status
+
+
+class _Mesh(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int64), ("xyz", ctypes.POINTER(ctypes.c_double)),
+                ("n_tets", ctypes.c_int64), ("tets", ctypes.POINTER(ctypes.c_int32)),
+                ("region", ctypes.POINTER(ctypes.c_int32)), ("n_regions", ctypes.c_int32),
+                ("Ms", ctypes.POINTER(ctypes.c_double)), ("Aex", ctypes.POINTER(ctypes.c_double))]
+
+
+class _Periodicity(ctypes.Structure):
+    _fields_ = [("periodic", ctypes.c_int32 * 3), ("lattice", ctypes.c_double * 3),
+                ("match_tol", ctypes.c_double)]
+
+
+class _Grid(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32 * 3), ("order", ctypes.c_int32), ("rer_scale", ctypes.c_double),
+                ("z0_ring", ctypes.c_int32)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int64), ("n_parents", ctypes.c_int64), ("n_parents_local", ctypes.c_int64),
+                ("periodic_dims", ctypes.c_int32), ("touching", ctypes.c_int32), ("protruding", ctypes.c_int32),
+                ("grid", ctypes.c_int32 * 3), ("fft", ctypes.c_int32 * 3),
+                ("nnz_ring1", ctypes.c_int64), ("nnz_z0", ctypes.c_int64), ("nnz_cbox", ctypes.c_int64),
+                ("bytes_per_eval_algorithmic", ctypes.c_double), ("setup_seconds", ctypes.c_double),
+                ("pgf_seconds", ctypes.c_double), ("kernel_bytes", ctypes.c_double * 8)]
+
+
+_vp = ctypes.c_void_p
+_lib.pmfem_setup.argtypes = [ctypes.POINTER(_vp), ctypes.POINTER(_Mesh), ctypes.POINTER(_Periodicity),
+                             ctypes.POINTER(_Grid), ctypes.c_int]
+_lib.pmfem_build_pgf.argtypes = [_vp, ctypes.c_double]
+for _n in ("pmfem_demag", "pmfem_exchange", "pmfem_heff", "pmfem_heff_host"):
+    getattr(_lib, _n).argtypes = [_vp, _vp, _vp, _vp]
+_lib.pmfem_query.argtypes = [_vp, ctypes.POINTER(_Info)]
+_lib.pmfem_get_order.argtypes = [_vp, ctypes.POINTER(ctypes.c_int64)]
+_lib.pmfem_export.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(ctypes.c_int64)]
+_lib.pmfem_set_timing.argtypes = [_vp, ctypes.c_int]
+_lib.pmfem_get_timing.argtypes = [_vp, ctypes.POINTER(ctypes.c_float)]
+_lib.pmfem_last_error.argtypes = [_vp]
+_lib.pmfem_last_error.restype = ctypes.c_char_p
+_lib.pmfem_destroy.argtypes = [_vp]
+for _n in SYMBOLS:
+    if _n not in ("pmfem_last_error", "pmfem_destroy"):
+        getattr(_lib, _n).restype = ctypes.c_int
+
+_EXPORT_DTYPES = {"parent": np.int64, "lca": np.int64, "shift": np.int32, "ring1_rowptr": np.int64,
+                  "ring1_col": np.int32, "z0_rowptr": np.int64, "z0_col": np.int32, "cbox_rowptr": np.int64,
+                  "cbox_col": np.int32, "stencil_s": np.int32, "perm": np.int64}
+
+KERNELS = ["K1_local_in", "K2_anterp", "K3_fft_conv", "K4_interp_corr", "K5_grad_sum"]
+
+
+def _ptr(a, ct):
+    return a.ctypes.data_as(ctypes.POINTER(ct))
+
+
+def _dev_ptr(t):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError("expected a contiguous float32 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Context:
+    """Owns a pmfem_ctx.  device=-1 builds a host-only context (setup artifacts, no fields)."""
+
+    def __init__(self, xyz, tets, periodic, lattice, grid_n, Ms=637.0, Aex=1.4e-6, order=1,
+                 rer_scale=2.0, z0_ring=1, device=0, region=None, match_tol=0.0):
+        xyz = np.ascontiguousarray(xyz, dtype=np.float64)
+        tets = np.ascontiguousarray(tets, dtype=np.int32)
+        Ms = np.ascontiguousarray(np.atleast_1d(Ms), dtype=np.float64)
+        Aex = np.ascontiguousarray(np.atleast_1d(Aex), dtype=np.float64)
+        self._keep = [xyz, tets, Ms, Aex]
+        m = _Mesh(xyz.shape[0], _ptr(xyz, ctypes.c_double), tets.shape[0], _ptr(tets, ctypes.c_int32),
+                  None, Ms.size, _ptr(Ms, ctypes.c_double), _ptr(Aex, ctypes.c_double))
+        if region is not None:
+            region = np.ascontiguousarray(region, dtype=np.int32)
+            self._keep.append(region)
+            m.region = _ptr(region, ctypes.c_int32)
+        p = _Periodicity((ctypes.c_int32 * 3)(*[int(bool(v)) for v in periodic]),
+                         (ctypes.c_double * 3)(*[float(v) for v in lattice]), float(match_tol))
+        g = _Grid((ctypes.c_int32 * 3)(*[int(v) for v in grid_n]), int(order), float(rer_scale), int(z0_ring))
+        h = _vp()
+        st = _lib.pmfem_setup(ctypes.byref(h), ctypes.byref(m), ctypes.byref(p), ctypes.byref(g), int(device))
+        if st != 0:
+            raise PmfemError(st, _lib.pmfem_last_error(None).decode())
+        self._h = h
+        self.device = device
+        self._keep = None
+        info = self.query()
+        self.n_parents = info["n_parents"]
+        self.n_nodes = info["n_nodes"]
+
+    def _check(self, st):
+        if st != 0:
+            raise PmfemError(st, _lib.pmfem_last_error(self._h).decode())
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.pmfem_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def build_pgf(self, target_rel_err=1e-12):
+        self._check(_lib.pmfem_build_pgf(self._h, float(target_rel_err)))
+
+    def _stream(self, stream):
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(self.device)
+        return _vp(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+    def _eval(self, fn, m, H, stream):
+        import torch
+        if H is None:
+            H = torch.empty_like(m)
+        fn_st = fn(self._h, _dev_ptr(m), _dev_ptr(H), self._stream(stream))
+        self._check(fn_st)
+        return H
+
+    def demag(self, m, H=None, stream=None):
+        return self._eval(_lib.pmfem_demag, m, H, stream)
+
+    def exchange(self, m, H=None, stream=None):
+        return self._eval(_lib.pmfem_exchange, m, H, stream)
+
+    def heff(self, m, H=None, stream=None):
+        return self._eval(_lib.pmfem_heff, m, H, stream)
+
+    def heff_host(self, m_host, H_host=None, stream=None):
+        """m_host, H_host: float32 [N',3] host arrays (numpy or pinned torch CPU tensors)."""
+        import torch
+        if isinstance(m_host, np.ndarray):
+            m_host = torch.from_numpy(np.ascontiguousarray(m_host, dtype=np.float32))
+        if H_host is None:
+            H_host = torch.empty_like(m_host)
+        self._check(_lib.pmfem_heff_host(self._h, _vp(m_host.data_ptr()), _vp(H_host.data_ptr()),
+                                         self._stream(stream)))
+        return H_host
+
+    def query(self):
+        info = _Info()
+        self._check(_lib.pmfem_query(self._h, ctypes.byref(info)))
+        out = {k: getattr(info, k) for k, _ in _Info._fields_}
+        for k in ("grid", "fft", "kernel_bytes"):
+            out[k] = list(out[k])
+        return out
+
+    def get_order(self):
+        """internal row i -> original (user) node index of its parent."""
+        a = np.zeros(self.n_parents, dtype=np.int64)
+        self._check(_lib.pmfem_get_order(self._h, _ptr(a, ctypes.c_int64)))
+        return a
+
+    def internal_to_parent_rank(self):
+        """internal row i -> parent rank (parents numbered by increasing original index)."""
+        parents = self.export("parent")
+        return np.searchsorted(parents, self.get_order())
+
+    def export(self, name):
+        cnt = ctypes.c_int64(0)
+        self._check(_lib.pmfem_export(self._h, name.encode(), None, ctypes.byref(cnt)))
+        dt = _EXPORT_DTYPES.get(name, np.float64)
+        a = np.zeros(cnt.value, dtype=dt)
+        if cnt.value:
+            self._check(_lib.pmfem_export(self._h, name.encode(), a.ctypes.data_as(_vp), ctypes.byref(cnt)))
+        return a
+
+    def set_timing(self, enable=True):
+        self._check(_lib.pmfem_set_timing(self._h, int(bool(enable))))
+
+    def timing(self):
+        a = (ctypes.c_float * 8)()
+        self._check(_lib.pmfem_get_timing(self._h, a))
+        return dict(zip(KERNELS, list(a)[:5]))
+
+
+def library_symbols():
+    """Exported symbols declared in include/pmfem.h (for the ABI test)."""
+    return {n: hasattr(_lib, n) for n in SYMBOLS}

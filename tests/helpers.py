@@ -1,0 +1,53 @@
+"""Test helpers: build the oracle and the library context on the same seeded inputs."""
+import numpy as np
+
+from oracle.heff import OracleModel
+from synth import make_config, kuhn_voxel_mesh
+
+# small configs (name, kwargs) used by the parity tests; each spans several FFT tiles and has
+# a ragged tail (grid and node counts are not multiples of the CUDA tile sizes)
+SMALL = {
+    "C1r0": dict(cfg=("C1", 2), grid=(16, 16, 16), order=1, s=2.0, ring=0),
+    "C1r1": dict(cfg=("C1", 2), grid=(16, 16, 16), order=1, s=2.0, ring=1),
+    "C2p2": dict(cfg=("C2", 8), grid=(32, 32, 4), order=2, s=2.0, ring=1),
+    "C3p1": dict(cfg=("C3", 12), grid=(64, 8, 8), order=1, s=2.0, ring=0),
+    "C4p3": dict(cfg=("C4", 40), grid=(16, 16, 16), order=3, s=1.5, ring=0),
+    "C5p2": dict(cfg=("C5", 16), grid=(128, 8, 4), order=2, s=2.0, ring=1),
+}
+
+
+def config(key):
+    spec = SMALL[key]
+    name, coarsen = spec["cfg"]
+    cfg = make_config(name, coarsen=coarsen)
+    return cfg, spec
+
+
+def oracle_model(key):
+    cfg, spec = config(key)
+    m = cfg["mesh"]
+    return OracleModel(m.xyz, m.tets, cfg["periodic"], cfg["lattice"], spec["grid"], Ms=cfg["Ms"],
+                       Aex=cfg["Aex"], order=spec["order"], rer_scale=spec["s"], z0_ring=spec["ring"])
+
+
+def lib_context(key, device):
+    from paper_2409_13958_b200 import Context
+    cfg, spec = config(key)
+    m = cfg["mesh"]
+    return Context(m.xyz, m.tets, cfg["periodic"], cfg["lattice"], spec["grid"], Ms=cfg["Ms"],
+                   Aex=cfg["Aex"], order=spec["order"], rer_scale=spec["s"], z0_ring=spec["ring"],
+                   device=device)
+
+
+def dense(ctx, prefix, nv, n):
+    rp = ctx.export(prefix + "_rowptr")
+    col = ctx.export(prefix + "_col")
+    val = ctx.export(prefix + "_val").reshape(-1, nv)
+    A = np.zeros((n, n, nv))
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    np.add.at(A, (rows, col), val)
+    return A
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))

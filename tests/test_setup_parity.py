@@ -1,0 +1,93 @@
+"""Host-logic parity (no GPU): the library's fp64 setup artifacts vs the oracle's.
+
+The library (C++, cone-decomposition quadrature, hashed PBC detection, box-list near search,
+GPU-style FFT layout) and the oracle (NumPy/SciPy, Duffy quadrature, KD-tree search) share no
+code; both follow PAPER.md and the SURVEY.md 8(c) contract.  Bars: exact for integer data,
+1e-12 relative for closed-form assembly, 1e-7 relative for Z0 (two independent quadratures),
+1e-12 for the PGF spectrum.
+"""
+import numpy as np
+import pytest
+
+from helpers import SMALL, oracle_model, lib_context, dense
+
+
+@pytest.fixture(scope="module", params=sorted(SMALL))
+def pair(request):
+    key = request.param
+    return key, oracle_model(key), lib_context(key, device=-1)
+
+
+def test_pbc_and_order(pair):
+    key, om, ctx = pair
+    assert np.array_equal(ctx.export("parent"), om.pm.parent)
+    assert np.array_equal(ctx.export("lca"), om.pm.lca)
+    assert np.array_equal(ctx.export("shift").reshape(-1, 3), om.pm.shift)
+    q = ctx.query()
+    assert q["n_parents"] == om.n_parents
+    t, p = om.pm.classify()
+    assert (q["touching"], q["protruding"]) == (int(t), int(p))
+    perm = ctx.export("perm")
+    assert np.array_equal(np.sort(perm), np.arange(om.n_parents))
+
+
+def test_local_operators(pair):
+    key, om, ctx = pair
+    n = om.n_parents
+    R = dense(ctx, "ring1", 7, n)
+    Vt = om.ops["Vt"]
+    assert np.allclose(ctx.export("Vt"), Vt, rtol=1e-13, atol=0)
+    L = -om.ops["S"].toarray() / Vt[:, None]
+    np.fill_diagonal(L, 0)
+    assert np.abs(R[:, :, 0] - L).max() <= 1e-12 * np.abs(L).max()
+    rsD = ctx.export("rowsumD").reshape(-1, 3)
+    for x, nm in enumerate(("Dx", "Dy", "Dz")):
+        D = om.ops[nm].toarray()
+        rs = D.sum(axis=1)
+        np.fill_diagonal(D, 0)
+        assert np.abs(R[:, :, 1 + x] - D).max() <= 1e-12 * np.abs(D).max()
+        assert np.abs(rsD[:, x] - rs).max() <= 1e-12 * np.abs(D).max()
+    for x, nm in enumerate(("Gx", "Gy", "Gz")):
+        G = om.ops[nm].toarray()
+        np.fill_diagonal(G, 0)
+        assert np.abs(R[:, :, 4 + x] - G).max() <= 1e-12 * np.abs(G).max()
+
+
+def test_z0(pair):
+    key, om, ctx = pair
+    n = om.n_parents
+    Z = dense(ctx, "z0", 3, n)
+    rs = ctx.export("rowsumZ").reshape(-1, 3)
+    for x, nm in enumerate(("Zx", "Zy", "Zz")):
+        Zo = om.z0[nm].toarray()
+        r = Zo.sum(axis=1)
+        np.fill_diagonal(Zo, 0)
+        scale = np.abs(Zo).max()
+        assert np.abs(Z[:, :, x] - Zo).max() <= 1e-7 * scale
+        assert np.abs(rs[:, x] - r).max() <= 1e-7 * scale
+
+
+def test_grid_stencils_cbox(pair):
+    key, om, ctx = pair
+    assert np.allclose(ctx.export("xw").reshape(-1, 3), om.xw, rtol=0, atol=0)
+    assert np.allclose(ctx.export("grid_delta"), om.grid.delta, rtol=1e-15)
+    s = ctx.export("stencil_s").reshape(-1, 3)
+    assert np.array_equal(s, om.S)
+    t = ctx.export("stencil_t").reshape(-1, 3)
+    assert np.allclose(t, ((om.xw - om.grid.origin) / om.grid.delta) - om.S, atol=1e-12)
+    C = dense(ctx, "cbox", 1, om.n_parents)[:, :, 0]
+    Co = om.C.toarray()
+    assert np.array_equal(C != 0, Co != 0)
+    assert np.abs(C - Co).max() <= 1e-11 * np.abs(Co).max()
+
+
+def test_pgf_spectrum(pair):
+    key, om, ctx = pair
+    ctx.build_pgf()
+    K = ctx.export("kernel").reshape(tuple(om.grid.fft[::-1]))       # [P2][P1][P0]
+    Ko = np.transpose(om.K, (2, 1, 0))
+    assert np.abs(K - Ko).max() <= 1e-12 * np.abs(Ko).max()
+    P = om.grid.fft
+    sp = ctx.export("spectrum").reshape(P[2], P[1], P[0] // 2 + 1)
+    Gh = np.transpose(om.Ghat, (2, 1, 0))[:, :, :P[0] // 2 + 1] / np.prod(P)
+    assert np.abs(sp - Gh).max() <= 1e-12 * np.abs(Gh).max()
