@@ -149,20 +149,22 @@ def check_rer(grid, lattice, s, p):
                 raise ValueError("r_ER too large on periodic axis %d" % a)
 
 
-def near_pairs(grid, xyz_w, lattice, s):
+def near_pairs(grid, xyz_w, lattice, s, rows=None):
     """K8: all (n, k, img) with |x_n - x_k - img*L| <= r_ER on every axis (closed),
-    img in {-1,0,1} on periodic axes (Eq. new_er; readings R8, R9)."""
+    img in {-1,0,1} on periodic axes (Eq. new_er; readings R8, R9).
+    With `rows`, only observers n in rows."""
     rER = np.full(3, r_er(grid, s))
     y = xyz_w / rER[None, :]
     tree = cKDTree(y)
     out_n, out_k, out_img = [], [], []
+    obs = np.arange(xyz_w.shape[0]) if rows is None else np.asarray(rows)
     rng = [(-1, 0, 1) if grid.periodic[a] else (0,) for a in range(3)]
     for img in itertools.product(*rng):
         sh = np.array(img, dtype=np.float64) * np.array([lattice[a] if grid.periodic[a] else 0.0
                                                          for a in range(3)])
         # |x_n - (x_k + sh)| <= rER  <=>  query points x_n - sh against tree of x_k
-        hits = tree.query_ball_point((xyz_w - sh[None, :]) / rER[None, :], r=1.0, p=np.inf)
-        for nidx, ks in enumerate(hits):
+        hits = tree.query_ball_point((xyz_w[obs] - sh[None, :]) / rER[None, :], r=1.0, p=np.inf)
+        for nidx, ks in zip(obs, hits):
             for k in ks:
                 d = xyz_w[nidx] - xyz_w[k] - sh
                 if np.all(np.abs(d) <= rER):       # closed interval in unscaled fp64
@@ -170,12 +172,12 @@ def near_pairs(grid, xyz_w, lattice, s):
     return np.array(out_n, dtype=np.int64), np.array(out_k, dtype=np.int64), np.array(out_img, dtype=np.int64).reshape(-1, 3)
 
 
-def precorrection(grid, xyz_w, lattice, S, W, s, p):
+def precorrection(grid, xyz_w, lattice, S, W, s, p, rows=None):
     """O11 / K9: C_box[n,k] = G0*(d) - sum_{a in st(n)} sum_{b in st(k)} w_na w_kb
     G0*((a - b - img*N) o Delta), d = x_n - x_k - img*L (subtract the grid's
-    G_0 contribution and add it back directly)."""
+    G_0 contribution and add it back directly).  With `rows`, only those rows."""
     check_rer(grid, lattice, s, p)
-    nn, kk, img = near_pairs(grid, xyz_w, lattice, s)
+    nn, kk, img = near_pairs(grid, xyz_w, lattice, s, rows)
     Lv = np.array([lattice[a] if grid.periodic[a] else 0.0 for a in range(3)])
     d = xyz_w[nn] - xyz_w[kk] - img * Lv[None, :]
     val = g0_star(d)

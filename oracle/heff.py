@@ -14,13 +14,16 @@ from .pgf import PgfSpec, pgf, pgf_self, pgf_potential
 
 class OracleModel:
     def __init__(self, xyz, tets, periodic, lattice, grid_n, Ms=637.0, Aex=1.4e-6,
-                 order=1, rer_scale=2.0, z0_ring=1, match_tol=0.0, nquad=20, build_aim=True):
+                 order=1, rer_scale=2.0, z0_ring=1, match_tol=0.0, nquad=20, build_aim=True, rows=None):
+        """rows: if given, Z0 and C_box are built only for these parent rows (sampled
+        full-size checks: u is then valid on `rows` only)."""
         self.pm = omesh.PeriodicMesh(xyz, tets, periodic, lattice, match_tol)
         T = self.pm.tets.shape[0]
         self.Ms_tet = np.full(T, float(Ms)) if np.isscalar(Ms) else np.asarray(Ms, float)
         self.Aex_tet = np.full(T, float(Aex)) if np.isscalar(Aex) else np.asarray(Aex, float)
         self.ops = fem.assemble(self.pm, self.Ms_tet, self.Aex_tet)
-        self.z0 = oz0.assemble_z0(self.pm, self.ops, self.Ms_tet, z0_ring, nquad)
+        self.rows = rows
+        self.z0 = oz0.assemble_z0(self.pm, self.ops, self.Ms_tet, z0_ring, nquad, rows)
         self.xw = self.pm.wrapped_parent_xyz()
         self.periodic = self.pm.periodic
         self.lattice = tuple(float(lattice[a]) if periodic[a] else 0.0 for a in range(3))
@@ -33,7 +36,8 @@ class OracleModel:
             self.P = aim.projection_matrix(self.grid, self.S, self.W)
             self.K = aim.kernel_table(self.grid, self.spec)
             self.Ghat = aim.kernel_spectrum(self.K)
-            self.C = aim.precorrection(self.grid, self.xw, self.lattice, self.S, self.W, rer_scale, order)
+            self.C = aim.precorrection(self.grid, self.xw, self.lattice, self.S, self.W, rer_scale, order,
+                                       rows)
 
     @property
     def n_parents(self):

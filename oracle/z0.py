@@ -142,10 +142,10 @@ def tet_moments(P, o, va, n=20, nreg=12, nclose=8, chunk=256):
     return A, Bm
 
 
-def near_structure(pm, z0_ring):
-    """Enumerate, for every parent n, near(n) and the deduplicated tet images U(n).
-    Returns (items, near) where items = list of (n, tet, shift(3), va, nearmask(4)) and
-    near = list of (n, p, ell(3))."""
+def near_structure(pm, z0_ring, rows=None):
+    """Enumerate, for every parent n (or only n in `rows`), near(n) and the deduplicated tet
+    images U(n).  Returns (items, near) where items = list of (n, tet, shift(3), va,
+    nearmask(4)) and near = list of (n, p, ell(3))."""
     copies = [[] for _ in range(pm.n_parents)]
     for c, p in enumerate(pm.pid):
         copies[p].append(c)
@@ -154,7 +154,7 @@ def near_structure(pm, z0_ring):
         for v in tv:
             tets_of[v].append(t)
     items, near_list = [], []
-    for n in range(pm.n_parents):
+    for n in (range(pm.n_parents) if rows is None else rows):
         star = set()
         for c in copies[n]:
             s = tuple(-pm.shift[c])
@@ -188,9 +188,10 @@ def near_structure(pm, z0_ring):
     return items, near_list
 
 
-def assemble_z0(pm, ops, Ms_tet, z0_ring=1, nquad=20):
-    """O7: Z0 as three csr [N',N'] matrices (u_loc = Zx mx + Zy my + Zz mz)."""
-    items, near = near_structure(pm, z0_ring)
+def assemble_z0(pm, ops, Ms_tet, z0_ring=1, nquad=20, rows=None):
+    """O7: Z0 as three csr [N',N'] matrices (u_loc = Zx mx + Zy my + Zz mz).  With `rows`,
+    only those rows are computed (the others are empty) -- for sampled full-size checks."""
+    items, near = near_structure(pm, z0_ring, rows)
     Np = pm.n_parents
     T = pm.tets.shape[0]
     Ms_tet = np.broadcast_to(np.asarray(Ms_tet, dtype=np.float64), (T,))

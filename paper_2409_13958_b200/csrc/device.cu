@@ -9,6 +9,12 @@
 // Every sparse operator is stored off-diagonal with its row sum ("difference form"):
 //   sum_m X_nm v_m = sum_{m != n} X_nm (v_m - v_n) + (sum_m X_nm) v_n,
 // so uniform m gives exactly zero charge and exchange field in fp32 (L, G have zero row sums).
+//
+// Formats: the local operators (L, D, G on the periodic 1-ring and Z0 on the 1-/2-ring) share
+// one column list per row and are stored SELL-32 (slices of 32 rows, column-major inside a
+// slice): K1 and K5 run one thread per row with fully coalesced streaming loads and many
+// independent loads in flight.  C_box (~10^2-10^3 entries per row) is CSR with rows padded to
+// a multiple of 4 and is read by one warp per row with 16-byte vector loads.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -45,67 +51,66 @@ T* dupload(const std::vector<T>& v) {
 int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 
 // ------------------------------------------------------------------ K1 local_in
-// One warp per row.  Reads m (12 B/node, gathered), the ring-1 row (col + 16 B), the Z0 row
-// (col + 16 B); writes q, u_loc (4 B each) and H_ex (12 B, optional).
+// One thread per row (SELL-32).  Reads m (gathered), the shared column list, Z0 (3 planes),
+// (L, D) on the ring-1 prefix and the row sums; writes q, u_loc and (heff) H_ex.
 __global__ void __launch_bounds__(256) k1_local_in(
-    int64_t Np, const float* __restrict__ m, const int64_t* __restrict__ r1_ptr, const int32_t* __restrict__ r1_col,
-    const float4* __restrict__ r1_LD, const float4* __restrict__ rowsumD, const int64_t* __restrict__ z_ptr,
-    const int32_t* __restrict__ z_col, const float4* __restrict__ z_val, const float4* __restrict__ rowsumZ,
-    float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H, int write_hex) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    int64_t Np, const float* __restrict__ m, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
+    const int32_t* __restrict__ s_col, const float* __restrict__ s_z, int64_t zt, const float4* __restrict__ s_LD,
+    const float4* __restrict__ rowsum, float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H,
+    int write_hex) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= Np) return;
+  const int64_t s = n >> 5;
+  const int l = (int)(n & 31);
+  const int64_t o = sl_off[s], o1 = sl1_off[s];
+  const int w = (int)((sl_off[s + 1] - o) >> 5), w1 = (int)((sl1_off[s + 1] - o1) >> 5);
   const float mx = m[3 * n], my = m[3 * n + 1], mz = m[3 * n + 2];
-  float hx = 0, hy = 0, hz = 0, qq = 0, ul = 0;
-  for (int64_t e = r1_ptr[n] + lane; e < r1_ptr[n + 1]; e += 32) {
-    const int32_t c = r1_col[e];
-    const float4 w = r1_LD[e];
+  float hx = 0.f, hy = 0.f, hz = 0.f, qq = 0.f, ul = 0.f;
+  int64_t e = o + l, e1 = o1 + l;
+#pragma unroll 4
+  for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
+    const int32_t c = __ldg(s_col + e);
+    const float4 LD = __ldg(s_LD + e1);
+    const float zx = __ldg(s_z + e), zy = __ldg(s_z + zt + e), zz = __ldg(s_z + 2 * zt + e);
     const float dx = m[3 * c] - mx, dy = m[3 * c + 1] - my, dz = m[3 * c + 2] - mz;
-    hx += w.x * dx; hy += w.x * dy; hz += w.x * dz;
-    qq += w.y * dx + w.z * dy + w.w * dz;
+    hx = fmaf(LD.x, dx, hx); hy = fmaf(LD.x, dy, hy); hz = fmaf(LD.x, dz, hz);
+    qq = fmaf(LD.y, dx, fmaf(LD.z, dy, fmaf(LD.w, dz, qq)));
+    ul = fmaf(zx, dx, fmaf(zy, dy, fmaf(zz, dz, ul)));
   }
-  for (int64_t e = z_ptr[n] + lane; e < z_ptr[n + 1]; e += 32) {
-    const int32_t c = z_col[e];
-    const float4 w = z_val[e];
-    ul += w.x * (m[3 * c] - mx) + w.y * (m[3 * c + 1] - my) + w.z * (m[3 * c + 2] - mz);
+#pragma unroll 4
+  for (int j = w1; j < w; ++j, e += 32) {
+    const int32_t c = __ldg(s_col + e);
+    const float zx = __ldg(s_z + e), zy = __ldg(s_z + zt + e), zz = __ldg(s_z + 2 * zt + e);
+    const float dx = m[3 * c] - mx, dy = m[3 * c + 1] - my, dz = m[3 * c + 2] - mz;
+    ul = fmaf(zx, dx, fmaf(zy, dy, fmaf(zz, dz, ul)));
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    hx += __shfl_xor_sync(0xffffffffu, hx, o);
-    hy += __shfl_xor_sync(0xffffffffu, hy, o);
-    hz += __shfl_xor_sync(0xffffffffu, hz, o);
-    qq += __shfl_xor_sync(0xffffffffu, qq, o);
-    ul += __shfl_xor_sync(0xffffffffu, ul, o);
-  }
-  if (lane == 0) {
-    const float4 rd = rowsumD[n], rz = rowsumZ[n];
-    q[n] = qq + rd.x * mx + rd.y * my + rd.z * mz;
-    uloc[n] = ul + rz.x * mx + rz.y * my + rz.z * mz;
-    if (write_hex) { H[3 * n] = hx; H[3 * n + 1] = hy; H[3 * n + 2] = hz; }
-  }
+  const float4 rd = rowsum[2 * n], rz = rowsum[2 * n + 1];
+  q[n] = qq + rd.x * mx + rd.y * my + rd.z * mz;
+  uloc[n] = ul + rz.x * mx + rz.y * my + rz.z * mz;
+  if (write_hex) { H[3 * n] = hx; H[3 * n + 1] = hy; H[3 * n + 2] = hz; }
 }
 
 // exchange only: H = L m
 __global__ void __launch_bounds__(256) k_exchange(int64_t Np, const float* __restrict__ m,
-                                                  const int64_t* __restrict__ r1_ptr, const int32_t* __restrict__ r1_col,
-                                                  const float4* __restrict__ r1_LD, float* __restrict__ H) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+                                                  const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
+                                                  const int32_t* __restrict__ s_col, const float4* __restrict__ s_LD,
+                                                  float* __restrict__ H) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= Np) return;
+  const int64_t s = n >> 5;
+  const int l = (int)(n & 31);
+  const int64_t o = sl_off[s], o1 = sl1_off[s];
+  const int w1 = (int)((sl1_off[s + 1] - o1) >> 5);
   const float mx = m[3 * n], my = m[3 * n + 1], mz = m[3 * n + 2];
-  float hx = 0, hy = 0, hz = 0;
-  for (int64_t e = r1_ptr[n] + lane; e < r1_ptr[n + 1]; e += 32) {
-    const int32_t c = r1_col[e];
-    const float L = r1_LD[e].x;
-    hx += L * (m[3 * c] - mx); hy += L * (m[3 * c + 1] - my); hz += L * (m[3 * c + 2] - mz);
+  float hx = 0.f, hy = 0.f, hz = 0.f;
+  int64_t e = o + l, e1 = o1 + l;
+#pragma unroll 4
+  for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
+    const int32_t c = __ldg(s_col + e);
+    const float L = __ldg(&s_LD[e1].x);
+    hx = fmaf(L, m[3 * c] - mx, hx); hy = fmaf(L, m[3 * c + 1] - my, hy); hz = fmaf(L, m[3 * c + 2] - mz, hz);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    hx += __shfl_xor_sync(0xffffffffu, hx, o);
-    hy += __shfl_xor_sync(0xffffffffu, hy, o);
-    hz += __shfl_xor_sync(0xffffffffu, hz, o);
-  }
-  if (lane == 0) { H[3 * n] = hx; H[3 * n + 1] = hy; H[3 * n + 2] = hz; }
+  H[3 * n] = hx; H[3 * n + 1] = hy; H[3 * n + 2] = hz;
 }
 
 // Lagrange weights on nodes 0..P at local coordinate t
@@ -154,26 +159,37 @@ __global__ void __launch_bounds__(256) k2_anterp(int64_t Np, const float* __rest
 template <int P>
 __global__ void __launch_bounds__(256) k4_interp_corr(int64_t Np, const float* __restrict__ U, const int4* __restrict__ st_s,
                                                       const float4* __restrict__ st_t, GridDims g,
-                                                      const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_col,
-                                                      const float* __restrict__ c_val, const float* __restrict__ q,
+                                                      const int64_t* __restrict__ c_ptr, const int4* __restrict__ c_col4,
+                                                      const float4* __restrict__ c_val4, const float* __restrict__ q,
                                                       const float* __restrict__ uloc, float* __restrict__ u) {
   const int lane = threadIdx.x & 31;
   const int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (n >= Np) return;
   float acc = 0.f;
-  for (int64_t e = c_ptr[n] + lane; e < c_ptr[n + 1]; e += 32) acc += c_val[e] * q[c_col[e]];
+  const int64_t b = c_ptr[n] >> 2, e_end = c_ptr[n + 1] >> 2;
+#pragma unroll 2
+  for (int64_t e = b + lane; e < e_end; e += 32) {
+    const int4 cc = __ldg(c_col4 + e);
+    const float4 vv = __ldg(c_val4 + e);
+    acc = fmaf(vv.x, q[cc.x], acc);
+    acc = fmaf(vv.y, q[cc.y], acc);
+    acc = fmaf(vv.z, q[cc.z], acc);
+    acc = fmaf(vv.w, q[cc.w], acc);
+  }
   constexpr int NS = (P + 1) * (P + 1) * (P + 1);
-  const int4 s = st_s[n];
-  const float4 t = st_t[n];
-  float wx[P + 1], wy[P + 1], wz[P + 1];
-  lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
-  for (int k = lane; k < NS; k += 32) {
-    const int i = k % (P + 1), j = (k / (P + 1)) % (P + 1), l = k / ((P + 1) * (P + 1));
-    const int ix = wrapi(s.x + i, g.n0, g.per0), iy = wrapi(s.y + j, g.n1, g.per1), iz = wrapi(s.z + l, g.n2, g.per2);
-    float wi = 0, wj = 0, wl = 0;
+  if (lane < NS) {
+    const int4 s = st_s[n];
+    const float4 t = st_t[n];
+    float wx[P + 1], wy[P + 1], wz[P + 1];
+    lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+    for (int k = lane; k < NS; k += 32) {
+      const int i = k % (P + 1), j = (k / (P + 1)) % (P + 1), l = k / ((P + 1) * (P + 1));
+      const int ix = wrapi(s.x + i, g.n0, g.per0), iy = wrapi(s.y + j, g.n1, g.per1), iz = wrapi(s.z + l, g.n2, g.per2);
+      float wi = 0, wj = 0, wl = 0;
 #pragma unroll
-    for (int a = 0; a <= P; ++a) { if (a == i) wi = wx[a]; if (a == j) wj = wy[a]; if (a == l) wl = wz[a]; }
-    acc += wi * wj * wl * U[((int64_t)iz * g.n1 + iy) * g.n0 + ix];
+      for (int a = 0; a <= P; ++a) { if (a == i) wi = wx[a]; if (a == j) wj = wy[a]; if (a == l) wl = wz[a]; }
+      acc = fmaf(wi * wj * wl, U[((int64_t)iz * g.n1 + iy) * g.n0 + ix], acc);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -181,29 +197,29 @@ __global__ void __launch_bounds__(256) k4_interp_corr(int64_t Np, const float* _
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
-__global__ void __launch_bounds__(256) k5_grad_sum(int64_t Np, const float* __restrict__ u, const int64_t* __restrict__ r1_ptr,
-                                                   const int32_t* __restrict__ r1_col, const float4* __restrict__ r1_G,
-                                                   float* __restrict__ H, int accumulate) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+__global__ void __launch_bounds__(256) k5_grad_sum(int64_t Np, const float* __restrict__ u, const int64_t* __restrict__ sl_off,
+                                                   const int64_t* __restrict__ sl1_off, const int32_t* __restrict__ s_col,
+                                                   const float* __restrict__ s_G, int64_t gt, float* __restrict__ H,
+                                                   int accumulate) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= Np) return;
+  const int64_t s = n >> 5;
+  const int l = (int)(n & 31);
+  const int64_t o = sl_off[s], o1 = sl1_off[s];
+  const int w1 = (int)((sl1_off[s + 1] - o1) >> 5);
   const float un = u[n];
-  float gx = 0, gy = 0, gz = 0;
-  for (int64_t e = r1_ptr[n] + lane; e < r1_ptr[n + 1]; e += 32) {
-    const float4 w = r1_G[e];
-    const float du = u[r1_col[e]] - un;
-    gx += w.x * du; gy += w.y * du; gz += w.z * du;
+  float gx = 0.f, gy = 0.f, gz = 0.f;
+  int64_t e = o + l, e1 = o1 + l;
+#pragma unroll 4
+  for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
+    const int32_t c = __ldg(s_col + e);
+    const float du = u[c] - un;
+    gx = fmaf(__ldg(s_G + e1), du, gx);
+    gy = fmaf(__ldg(s_G + gt + e1), du, gy);
+    gz = fmaf(__ldg(s_G + 2 * gt + e1), du, gz);
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    gx += __shfl_xor_sync(0xffffffffu, gx, o);
-    gy += __shfl_xor_sync(0xffffffffu, gy, o);
-    gz += __shfl_xor_sync(0xffffffffu, gz, o);
-  }
-  if (lane == 0) {
-    if (accumulate) { H[3 * n] -= gx; H[3 * n + 1] -= gy; H[3 * n + 2] -= gz; }
-    else { H[3 * n] = -gx; H[3 * n + 1] = -gy; H[3 * n + 2] = -gz; }
-  }
+  if (accumulate) { H[3 * n] -= gx; H[3 * n + 1] -= gy; H[3 * n + 2] -= gz; }
+  else { H[3 * n] = -gx; H[3 * n + 1] = -gy; H[3 * n + 2] = -gz; }
 }
 
 // ------------------------------------------------------------------ PGF table (fp64)
@@ -239,19 +255,6 @@ void twiddles(int P, std::vector<typename Cx<T>::t>& tw) {
   }
 }
 
-// 3D transform driver shared by the fp32 hot path and the fp64 spectrum build
-template <class T>
-struct FftDims {
-  int n[3], P[3], H0;
-};
-
-template <class T>
-size_t x_smem_lines(int P0) {
-  int M = P0 / 2;
-  int nl = std::max(1, 4096 / std::max(M, 1));
-  return (size_t)nl;
-}
-
 constexpr int TILE = 16;
 
 template <class T>
@@ -271,20 +274,35 @@ template <class T>
 void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows, int n0, int P0, int n1, int P1,
               const typename Cx<T>::t* tw, cudaStream_t st) {
   using C = typename Cx<T>::t;
-  int M = P0 / 2;
-  int nl = (int)x_smem_lines<T>(P0);
+  const int M = P0 / 2;
+  // lines per CTA: enough CTAs to cover 2 waves of 148 SMs, at most 4096 complex per CTA
+  int nl = std::max(1, std::min(4096 / std::max(M, 1), nrows / 296));
   size_t smem = (size_t)nl * M * sizeof(C);
   RowMap rm{n1, P1};
   int blocks = (nrows + nl - 1) / nl;
+  int threads = std::min(256, std::max(64, nl * M / 2));
+  threads = (threads + 31) / 32 * 32;
   if (fwd) {
     auto kern = fft_x_forward<T>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<blocks, 256, smem, st>>>(rin, cio, nrows, n0, P0, ilog2(M), rm, tw, nl);
+    kern<<<blocks, threads, smem, st>>>(rin, cio, nrows, n0, P0, ilog2(M), rm, tw, nl);
   } else {
     auto kern = fft_x_inverse<T>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<blocks, 256, smem, st>>>(cio, rout, nrows, n0, P0, ilog2(M), rm, tw, nl);
+    kern<<<blocks, threads, smem, st>>>(cio, rout, nrows, n0, P0, ilog2(M), rm, tw, nl);
   }
+  CK(cudaGetLastError());
+}
+
+void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
+  const int tile = D.fused_tile, P1 = D.P[1], P2 = D.P[2];
+  size_t smem = (size_t)P1 * P2 * tile * sizeof(float2);
+  auto kern = fft_yz_fused<float>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int threads = std::min(512, std::max(128, P1 * P2 * tile / 4));
+  threads = (threads + 31) / 32 * 32;
+  kern<<<(D.H0 + tile - 1) / tile, threads, smem, st>>>(D.C, D.n[1], P1, ilog2(P1), D.n[2], P2, ilog2(P2), D.H0,
+                                                         tile, D.spec, D.tw32[1], D.tw32[2]);
   CK(cudaGetLastError());
 }
 
@@ -297,62 +315,110 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.order = S.order;
   for (int a = 0; a < 3; ++a) { D.periodic[a] = S.periodic[a]; D.n[a] = S.grid_n[a]; D.P[a] = S.fft_n[a]; }
   D.H0 = D.P[0] / 2 + 1;
-  // permute rows and columns to internal order
-  auto perm_csr = [&](const Csr& A, std::vector<int64_t>& ptr, std::vector<int32_t>& col, std::vector<int64_t>& src) {
-    ptr.assign(Np + 1, 0);
-    for (int64_t i = 0; i < Np; ++i) {
-      int64_t r = S.perm[i];
-      ptr[i + 1] = ptr[i] + (A.rowptr[r + 1] - A.rowptr[r]);
+
+  // ---- shared local operator in SELL-32, internal order
+  const int64_t ns = (Np + 31) / 32;
+  D.nslices = ns;
+  std::vector<int64_t> sl_off(ns + 1, 0), sl1_off(ns + 1, 0);
+  // per internal row: ring-1 cols (user ids) + Z0-only cols, with values
+  std::vector<int> len1(Np), lenz(Np);
+  std::vector<std::vector<int32_t>> rcols(Np);
+  std::vector<std::vector<float>> rz(Np), rld(Np), rg(Np);
+#pragma omp parallel for schedule(dynamic, 1024)
+  for (int64_t i = 0; i < Np; ++i) {
+    const int64_t r = S.perm[i];
+    std::vector<std::pair<int32_t, int64_t>> r1, rzl;
+    for (int64_t e = S.ring1.rowptr[r]; e < S.ring1.rowptr[r + 1]; ++e) r1.push_back({(int32_t)S.iperm[S.ring1.col[e]], e});
+    for (int64_t e = S.z0.rowptr[r]; e < S.z0.rowptr[r + 1]; ++e) rzl.push_back({(int32_t)S.iperm[S.z0.col[e]], e});
+    std::sort(r1.begin(), r1.end());
+    std::sort(rzl.begin(), rzl.end());
+    std::vector<int32_t>& cols = rcols[i];
+    std::vector<float>& z = rz[i];
+    for (auto& pr : r1) {
+      cols.push_back(pr.first);
+      const double* v = &S.ring1.val[7 * pr.second];
+      for (int x = 0; x < 4; ++x) rld[i].push_back((float)v[x]);
+      for (int x = 0; x < 3; ++x) rg[i].push_back((float)v[4 + x]);
+      // Z0 value for this column (0 if Z0 has no entry there)
+      auto it = std::lower_bound(rzl.begin(), rzl.end(), std::make_pair(pr.first, (int64_t)-1));
+      for (int x = 0; x < 3; ++x)
+        z.push_back((it != rzl.end() && it->first == pr.first) ? (float)S.z0.val[3 * it->second + x] : 0.f);
     }
-    col.resize(ptr[Np]);
-    src.resize(ptr[Np]);
+    for (auto& pr : rzl) {
+      auto it = std::lower_bound(r1.begin(), r1.end(), std::make_pair(pr.first, (int64_t)-1));
+      if (it != r1.end() && it->first == pr.first) continue;
+      cols.push_back(pr.first);
+      for (int x = 0; x < 3; ++x) z.push_back((float)S.z0.val[3 * pr.second + x]);
+    }
+    len1[i] = (int)r1.size();
+    lenz[i] = (int)cols.size();
+  }
+  for (int64_t s = 0; s < ns; ++s) {
+    int w = 0, w1 = 0;
+    for (int64_t i = 32 * s; i < std::min(Np, 32 * s + 32); ++i) { w = std::max(w, lenz[i]); w1 = std::max(w1, len1[i]); }
+    sl_off[s + 1] = sl_off[s] + 32 * (int64_t)w;
+    sl1_off[s + 1] = sl1_off[s] + 32 * (int64_t)w1;
+  }
+  const int64_t zt = sl_off[ns], gt = sl1_off[ns];
+  D.zt = zt;
+  D.gt = gt;
+  std::vector<int32_t> s_col(zt);
+  std::vector<float> s_z(3 * zt, 0.f), s_G(3 * gt, 0.f);
+  std::vector<float4> s_LD(gt, make_float4(0, 0, 0, 0));
+#pragma omp parallel for
+  for (int64_t s = 0; s < ns; ++s) {
+    const int w = (int)((sl_off[s + 1] - sl_off[s]) / 32), w1 = (int)((sl1_off[s + 1] - sl1_off[s]) / 32);
+    for (int l = 0; l < 32; ++l) {
+      const int64_t i = 32 * s + l;
+      for (int j = 0; j < w; ++j) {
+        const int64_t e = sl_off[s] + 32 * j + l;
+        if (i < Np && j < lenz[i]) {
+          s_col[e] = rcols[i][j];
+          for (int x = 0; x < 3; ++x) s_z[x * zt + e] = rz[i][3 * j + x];
+        } else {
+          s_col[e] = (int32_t)std::min<int64_t>(i, Np - 1);   // padding: the row itself, weight 0
+        }
+      }
+      for (int j = 0; j < w1; ++j) {
+        const int64_t e1 = sl1_off[s] + 32 * j + l;
+        if (i < Np && j < len1[i]) {
+          s_LD[e1] = make_float4(rld[i][4 * j], rld[i][4 * j + 1], rld[i][4 * j + 2], rld[i][4 * j + 3]);
+          for (int x = 0; x < 3; ++x) s_G[x * gt + e1] = rg[i][3 * j + x];
+        }
+      }
+    }
+  }
+  D.sl_off = dupload(sl_off); D.sl1_off = dupload(sl1_off); D.s_col = dupload(s_col);
+  D.s_z = dupload(s_z); D.s_LD = dupload(s_LD); D.s_G = dupload(s_G);
+
+  // ---- C_box: CSR with rows padded to a multiple of 4
+  {
+    std::vector<int64_t> ptr(Np + 1, 0);
     for (int64_t i = 0; i < Np; ++i) {
       int64_t r = S.perm[i];
-      int64_t o = ptr[i];
-      // sort the row by internal column for locality
+      int64_t len = S.cbox.rowptr[r + 1] - S.cbox.rowptr[r];
+      ptr[i + 1] = ptr[i] + (len + 3) / 4 * 4;
+    }
+    std::vector<int32_t> col(ptr[Np]);
+    std::vector<float> val(ptr[Np], 0.f);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t i = 0; i < Np; ++i) {
+      int64_t r = S.perm[i];
       std::vector<std::pair<int32_t, int64_t>> tmp;
-      for (int64_t e = A.rowptr[r]; e < A.rowptr[r + 1]; ++e) tmp.push_back({(int32_t)S.iperm[A.col[e]], e});
+      for (int64_t e = S.cbox.rowptr[r]; e < S.cbox.rowptr[r + 1]; ++e) tmp.push_back({(int32_t)S.iperm[S.cbox.col[e]], e});
       std::sort(tmp.begin(), tmp.end());
-      for (auto& pr : tmp) { col[o] = pr.first; src[o] = pr.second; ++o; }
+      int64_t o = ptr[i];
+      for (auto& pr : tmp) { col[o] = pr.first; val[o] = (float)S.cbox.val[pr.second]; ++o; }
+      for (; o < ptr[i + 1]; ++o) col[o] = (int32_t)i;
     }
-  };
-  {
-    std::vector<int64_t> ptr, src;
-    std::vector<int32_t> col;
-    perm_csr(S.ring1, ptr, col, src);
-    std::vector<float4> LD(col.size()), G(col.size());
-    for (size_t e = 0; e < col.size(); ++e) {
-      const double* v = &S.ring1.val[7 * src[e]];
-      LD[e] = make_float4((float)v[0], (float)v[1], (float)v[2], (float)v[3]);
-      G[e] = make_float4((float)v[4], (float)v[5], (float)v[6], 0.f);
-    }
-    D.r1_ptr = dupload(ptr); D.r1_col = dupload(col); D.r1_LD = dupload(LD); D.r1_G = dupload(G);
+    D.c_ptr = dupload(ptr); D.c_col = dupload(col); D.c_val = dupload(val);
   }
-  {
-    std::vector<int64_t> ptr, src;
-    std::vector<int32_t> col;
-    perm_csr(S.z0, ptr, col, src);
-    std::vector<float4> Z(col.size());
-    for (size_t e = 0; e < col.size(); ++e) {
-      const double* v = &S.z0.val[3 * src[e]];
-      Z[e] = make_float4((float)v[0], (float)v[1], (float)v[2], 0.f);
-    }
-    D.z_ptr = dupload(ptr); D.z_col = dupload(col); D.z_val = dupload(Z);
-  }
-  {
-    std::vector<int64_t> ptr, src;
-    std::vector<int32_t> col;
-    perm_csr(S.cbox, ptr, col, src);
-    std::vector<float> V(col.size());
-    for (size_t e = 0; e < col.size(); ++e) V[e] = (float)S.cbox.val[src[e]];
-    D.c_ptr = dupload(ptr); D.c_col = dupload(col); D.c_val = dupload(V);
-  }
-  std::vector<float4> rD(Np), rZ(Np), stt(Np);
+  std::vector<float4> rsum(2 * Np), stt(Np);
   std::vector<int4> sts(Np);
   for (int64_t i = 0; i < Np; ++i) {
     int64_t r = S.perm[i];
-    rD[i] = make_float4((float)S.rowsumD[3 * r], (float)S.rowsumD[3 * r + 1], (float)S.rowsumD[3 * r + 2], 0.f);
-    rZ[i] = make_float4((float)S.rowsumZ[3 * r], (float)S.rowsumZ[3 * r + 1], (float)S.rowsumZ[3 * r + 2], 0.f);
+    rsum[2 * i] = make_float4((float)S.rowsumD[3 * r], (float)S.rowsumD[3 * r + 1], (float)S.rowsumD[3 * r + 2], 0.f);
+    rsum[2 * i + 1] = make_float4((float)S.rowsumZ[3 * r], (float)S.rowsumZ[3 * r + 1], (float)S.rowsumZ[3 * r + 2], 0.f);
     int s[3];
     for (int a = 0; a < 3; ++a) {
       int v = S.st_s[3 * r + a];
@@ -362,7 +428,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     sts[i] = make_int4(s[0], s[1], s[2], 0);
     stt[i] = make_float4((float)S.st_t[3 * r], (float)S.st_t[3 * r + 1], (float)S.st_t[3 * r + 2], 0.f);
   }
-  D.rowsumD = dupload(rD); D.rowsumZ = dupload(rZ); D.st_s = dupload(sts); D.st_t = dupload(stt);
+  D.rowsum = dupload(rsum); D.st_s = dupload(sts); D.st_t = dupload(stt);
   for (int a = 0; a < 3; ++a) {
     std::vector<float2> t32; std::vector<double2> t64;
     twiddles<float>(D.P[a], t32); twiddles<double>(D.P[a], t64);
@@ -373,24 +439,38 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.C = dalloc<float2>((size_t)D.H0 * D.P[1] * D.P[2]);
   D.spec = dalloc<float>((size_t)D.H0 * D.P[1] * D.P[2]);
   for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&D.ev[i]));
-  // algorithmic bytes per launch (DESIGN.md byte model; fp32 values, int32 columns, int64 row ptrs)
-  const double nnz1 = (double)S.ring1.nnz(), nnzz = (double)S.z0.nnz(), nnzc = (double)S.cbox.nnz();
-  const double G = (double)D.n[0] * D.n[1] * D.n[2];
-  const int ns = (S.order + 1) * (S.order + 1) * (S.order + 1);
-  D.kernel_bytes[0] = Np * (12.0 + 16 + 16 + 8 + 8 + 4 + 4 + 12) + nnz1 * (4 + 16) + nnzz * (4 + 16);
-  D.kernel_bytes[1] = Np * (4.0 + 16 + 16) + G * 4.0 * 2;                 // read q + stencil, grid RMW
+  // FFT plan: fused YZ when a yz plane of `tile` columns fits in shared memory
   {
-    double Hc = (double)D.H0;
-    double bx = G * 4 + (double)D.n[1] * D.n[2] * Hc * 8;                   // X fwd: read real, write cplx
-    double by = 2.0 * (double)D.n[2] * Hc * D.P[1] * 8;                     // Y fwd read+write (pruned in)
-    double bz = 2.0 * Hc * D.P[1] * D.P[2] * 8 + Hc * D.P[1] * D.P[2] * 4;  // Z fused + spectrum
-    double by2 = 2.0 * (double)D.n[2] * Hc * D.P[1] * 8;
-    double bx2 = (double)D.n[1] * D.n[2] * Hc * 8 + G * 4;
-    (void)by2;
-    D.kernel_bytes[2] = bx + by + bz + by + bx2;
+    const size_t plane_bytes = (size_t)D.P[1] * D.P[2] * sizeof(float2);
+    D.fused_tile = 0;
+    if (plane_bytes <= 200 * 1024) {
+      int tile = 1;
+      while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && (D.H0 + 2 * tile - 1) / (2 * tile) >= 148) tile *= 2;
+      D.fused_tile = tile;
+    }
   }
-  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4) + nnzc * (4 + 4 + 4) + Np * ns * 4.0;
-  D.kernel_bytes[4] = Np * (4.0 + 8 + 12 + 12) + nnz1 * (4 + 16 + 4);
+  D.launches_per_eval = 3 + (D.fused_tile ? 3 : 5) + 1;   // K1, K2, FFT passes, K4, K5 (memset excluded)
+  // compulsory bytes per launch: every array read or written once (gathered m, q, u once)
+  const double G = (double)D.n[0] * D.n[1] * D.n[2];
+  D.kernel_bytes[0] = Np * (12.0 + 32 + 16 + 4 + 4 + 12) + (double)zt * (4 + 12) + (double)gt * 16;
+  D.kernel_bytes[1] = Np * (4.0 + 16 + 16) + G * 4.0 * 2;
+  {
+    const double Hc = (double)D.H0;
+    const double spec_b = Hc * D.P[1] * D.P[2] * 4;
+    if (D.fused_tile) {
+      D.kernel_bytes[2] = (G * 4 + (double)D.n[1] * D.n[2] * Hc * 8)        // X
+                          + 2.0 * (double)D.n[1] * D.n[2] * Hc * 8 + spec_b   // YZ: data block in + out
+                          + ((double)D.n[1] * D.n[2] * Hc * 8 + G * 4);       // X'
+    } else {
+      D.kernel_bytes[2] = (G * 4 + (double)D.n[1] * D.n[2] * Hc * 8) + 2.0 * (double)D.n[2] * Hc * D.P[1] * 8 +
+                          2.0 * Hc * D.P[1] * D.P[2] * 8 + spec_b + 2.0 * (double)D.n[2] * Hc * D.P[1] * 8 +
+                          ((double)D.n[1] * D.n[2] * Hc * 8 + G * 4);
+    }
+  }
+  int64_t cnnz = 0;
+  for (int64_t i = 0; i < Np; ++i) cnnz += S.cbox.rowptr[S.perm[i] + 1] - S.cbox.rowptr[S.perm[i]];
+  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 8 + G * 4.0;
+  D.kernel_bytes[4] = Np * (4.0 + 8 + 12 + 12) + (double)gt * (4 + 12);
 }
 
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
@@ -425,9 +505,9 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
 void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
-  void* ptrs[] = {D.r1_ptr, D.r1_col, D.r1_LD, D.r1_G, D.rowsumD, D.z_ptr, D.z_col, D.z_val, D.rowsumZ,
-                  D.c_ptr, D.c_col, D.c_val, D.st_s, D.st_t, D.spec, D.q, D.uloc, D.u, D.Q, D.C,
-                  D.m_stage, D.H_stage, D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2]};
+  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_col, D.s_z, D.s_LD, D.s_G, D.rowsum, D.c_ptr, D.c_col, D.c_val,
+                  D.st_s, D.st_t, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
+                  D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int i = 0; i < 8; ++i)
@@ -436,11 +516,11 @@ void device_free(DeviceState& D) {
 
 void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, EvalMode mode) {
   const int64_t Np = D.Np;
-  const int WPB = 8;                       // warps per block (256 threads)
-  const unsigned rows_blocks = (unsigned)((Np + WPB - 1) / WPB);
-  const unsigned node_blocks = (unsigned)((Np + 255) / 256);
+  const unsigned thr_blocks = (unsigned)((Np + 255) / 256);      // thread per row
+  const unsigned warp_blocks = (unsigned)((Np + 7) / 8);         // warp per row, 8 warps per block
+  const int64_t zt_h = D.zt, gt_h = D.gt;                        // SoA plane strides
   if (mode == EVAL_EXCHANGE) {
-    k_exchange<<<rows_blocks, 256, 0, st>>>(Np, m, D.r1_ptr, D.r1_col, D.r1_LD, H);
+    k_exchange<<<thr_blocks, 256, 0, st>>>(Np, m, D.sl_off, D.sl1_off, D.s_col, D.s_LD, H);
     CK(cudaGetLastError());
     return;
   }
@@ -448,36 +528,42 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   auto mark = [&](int i) { if (D.timing) CK(cudaEventRecord(D.ev[i], st)); };
   GridDims g{D.n[0], D.n[1], D.n[2], D.periodic[0], D.periodic[1], D.periodic[2]};
   mark(0);
-  k1_local_in<<<rows_blocks, 256, 0, st>>>(Np, m, D.r1_ptr, D.r1_col, D.r1_LD, D.rowsumD, D.z_ptr, D.z_col, D.z_val,
-                                           D.rowsumZ, D.q, D.uloc, H, mode == EVAL_HEFF ? 1 : 0);
+  k1_local_in<<<thr_blocks, 256, 0, st>>>(Np, m, D.sl_off, D.sl1_off, D.s_col, D.s_z, zt_h, D.s_LD, D.rowsum, D.q,
+                                          D.uloc, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(1);
   CK(cudaMemsetAsync(D.Q, 0, sizeof(float) * (size_t)D.n[0] * D.n[1] * D.n[2], st));
   switch (D.order) {
-    case 1: k2_anterp<1><<<node_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
-    case 2: k2_anterp<2><<<node_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
-    default: k2_anterp<3><<<node_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
+    case 1: k2_anterp<1><<<thr_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
+    case 2: k2_anterp<2><<<thr_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
+    default: k2_anterp<3><<<thr_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
   }
   CK(cudaGetLastError());
   mark(2);
   {
     const int n0 = D.n[0], n1 = D.n[1], n2 = D.n[2], P0 = D.P[0], P1 = D.P[1], P2 = D.P[2], H0 = D.H0;
     launch_x<float>(true, D.Q, D.C, nullptr, n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
-    launch_strided<float>(D.C, P1, H0, H0, n2, (long long)P1 * H0, n1, P1, 0, nullptr, 0, 0, D.tw32[1], st);
-    launch_strided<float>(D.C, P2, (long long)P1 * H0, H0, P1, H0, n2, n2, 2, D.spec, (long long)P1 * H0, H0,
-                          D.tw32[2], st);
-    launch_strided<float>(D.C, P1, H0, H0, n2, (long long)P1 * H0, P1, n1, 1, nullptr, 0, 0, D.tw32[1], st);
+    if (D.fused_tile) {
+      launch_yz_fused(D, st);
+    } else {
+      launch_strided<float>(D.C, P1, H0, H0, n2, (long long)P1 * H0, n1, P1, 0, nullptr, 0, 0, D.tw32[1], st);
+      launch_strided<float>(D.C, P2, (long long)P1 * H0, H0, P1, H0, n2, n2, 2, D.spec, (long long)P1 * H0, H0,
+                            D.tw32[2], st);
+      launch_strided<float>(D.C, P1, H0, H0, n2, (long long)P1 * H0, P1, n1, 1, nullptr, 0, 0, D.tw32[1], st);
+    }
     launch_x<float>(false, nullptr, D.C, D.Q, n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
   }
   mark(3);
+  const int4* c4 = reinterpret_cast<const int4*>(D.c_col);
+  const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   switch (D.order) {
-    case 1: k4_interp_corr<1><<<rows_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_col, D.c_val, D.q, D.uloc, D.u); break;
-    case 2: k4_interp_corr<2><<<rows_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_col, D.c_val, D.q, D.uloc, D.u); break;
-    default: k4_interp_corr<3><<<rows_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_col, D.c_val, D.q, D.uloc, D.u); break;
+    case 1: k4_interp_corr<1><<<warp_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
+    case 2: k4_interp_corr<2><<<warp_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
+    default: k4_interp_corr<3><<<warp_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
   }
   CK(cudaGetLastError());
   mark(4);
-  k5_grad_sum<<<rows_blocks, 256, 0, st>>>(Np, D.u, D.r1_ptr, D.r1_col, D.r1_G, H, mode == EVAL_HEFF ? 1 : 0);
+  k5_grad_sum<<<thr_blocks, 256, 0, st>>>(Np, D.u, D.sl_off, D.sl1_off, D.s_col, D.s_G, gt_h, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(5);
 }

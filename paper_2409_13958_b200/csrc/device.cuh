@@ -14,16 +14,18 @@ struct DeviceState {
   int order = 1;
   int periodic[3] = {0, 0, 0};
   int n[3] = {0, 0, 0}, P[3] = {0, 0, 0}, H0 = 0;
-  // ring-1 operators (off-diagonal, difference form)
-  int64_t* r1_ptr = nullptr;  int32_t* r1_col = nullptr;
-  float4* r1_LD = nullptr;    // (L, Dx, Dy, Dz)
-  float4* r1_G = nullptr;     // (Gx, Gy, Gz, 0)
-  float4* rowsumD = nullptr;  // (sum_m D_nm, 0)
-  // Z0 (off-diagonal) + row sums
-  int64_t* z_ptr = nullptr;   int32_t* z_col = nullptr;
-  float4* z_val = nullptr;    // (Zx, Zy, Zz, 0)
-  float4* rowsumZ = nullptr;
-  // C_box
+  // Local operators in SELL-32 (32 rows per slice, column-major inside a slice).  One shared
+  // column list per row: the ring-1 columns first, then the Z0-only columns (2-ring at ring 1).
+  int64_t nslices = 0;
+  int64_t zt = 0, gt = 0;      // total SELL entries of the shared / ring-1 arrays (SoA plane strides)
+  int64_t* sl_off = nullptr;   // [nslices+1] entry offsets of the shared col / Z arrays
+  int64_t* sl1_off = nullptr;  // [nslices+1] entry offsets of the ring-1 value arrays
+  int32_t* s_col = nullptr;    // shared columns (padding: the row itself)
+  float* s_z = nullptr;        // Z0 values, 3 planes (x, y, z) of length sl_off[nslices]
+  float4* s_LD = nullptr;      // (L, Dx, Dy, Dz) for the first sl1 width entries
+  float* s_G = nullptr;        // G values, 3 planes of length sl1_off[nslices]
+  float4* rowsum = nullptr;    // [N'][2] (sum_m D_nm, 0), (sum_m Z_nm, 0)
+  // C_box, CSR with rows padded to a multiple of 4 entries (col = row, val = 0)
   int64_t* c_ptr = nullptr;   int32_t* c_col = nullptr;
   float* c_val = nullptr;
   // stencils
@@ -32,7 +34,8 @@ struct DeviceState {
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32
   float* spec = nullptr;
   bool pgf_ready = false;
-  // FFT twiddles per axis (fp32 and fp64)
+  // FFT plan + twiddles per axis (fp32 and fp64)
+  int fused_tile = 0;          // > 0: fused YZ plan with this column tile
   float2* tw32[3] = {nullptr, nullptr, nullptr};
   double2* tw64[3] = {nullptr, nullptr, nullptr};
   // scratch
@@ -49,6 +52,7 @@ struct DeviceState {
   cudaEvent_t ev[8] = {};
   float last_ms[8] = {0};
   double kernel_bytes[8] = {0};
+  int launches_per_eval = 0;
 };
 
 void device_upload(DeviceState& D, const HostSetup& S);

@@ -2,14 +2,14 @@
 //   U = F^-1( G_hat . F Q ) on the padded grid (periodic axes circular, no padding, P:340;
 //   non-periodic axes zero-padded to 2N).
 // Layout: real grid [n2][n1][n0] (x fastest); complex half spectrum [P2][P1][H0], H0 = P0/2+1.
-// Plan (5 sweeps of the data, pruned on padded axes):
-//   X  forward real->complex along x  (rows i1 < n1, i2 < n2 only; padding never read)
-//   Y  forward C2C along y            (planes i2 < n2; input rows >= n1 are zero)
-//   Z  forward C2C along z, * G_hat, inverse C2C along z, keep i2 < n2   (fused, one sweep)
-//   Y' inverse C2C along y, keep i1 < n1
-//   X' inverse complex->real along x, keep i0 < n0
-// Each CTA stages a tile of lines in shared memory, runs an in-place radix-2 DIT FFT there
-// (bit-reversed load, log2 P butterfly stages) and writes back with coalesced accesses.
+// Plans (pruned on padded axes: zero halves are never read, unneeded outputs never written):
+//   fused (yz plane of TILE columns fits in shared memory -- C1, C2, C3, C5):
+//     X  : real->complex along x for the n1*n2 data rows
+//     YZ : per column tile: FFT_y (n2 data planes) -> FFT_z -> * G_hat -> IFFT_z (keep n2)
+//          -> IFFT_y (keep n1), all in shared memory (one read + one write of the spectrum)
+//     X' : complex->real along x, keep n0
+//   split (C4, 256^2 planes): X, Y, Z(* G_hat, fused fwd/inv), Y', X'.
+// In-place radix-2 DIT in shared memory (bit-reversed load, log2 P butterfly stages).
 // Templated on the real type: float for the hot path, double for the PGF spectrum build.
 #pragma once
 #include <cuda_runtime.h>
@@ -25,30 +25,27 @@ template <class C> __device__ __forceinline__ C cmul(C a, C b) {
 }
 template <class C> __device__ __forceinline__ C cconj(C a) { a.y = -a.y; return a; }
 
-__device__ __forceinline__ int bitrev(int v, int logn) { return __brev(v) >> (32 - logn); }
+__device__ __forceinline__ int bitrev(int v, int logn) { return logn ? (int)(__brev((unsigned)v) >> (32 - logn)) : 0; }
 
-// In-place radix-2 DIT on `nl` lines in smem: element e of line l at buf[l*ls + e*es].
-// Input must be in bit-reversed order.  tw[k] = exp(-2 pi i k / Pt) for k < Pt/2 with
-// Pt = P * tw_stride (so the P-point twiddle j is tw[j * tw_stride]).  inv -> conj twiddles.
-template <class C>
-__device__ void smem_fft(C* buf, int P, int logP, int nl, int ls, int es, const C* __restrict__ tw,
-                         int tw_stride, bool inv) {
+// In-place radix-2 DIT on nl lines in smem; element e of line l is at base(l) + e*es.
+// Input in bit-reversed order, output natural.  tw[k] = exp(-2 pi i k / (P*tw_stride)).
+// line_fast: consecutive threads take consecutive lines (tile layouts, es > 1).
+template <class C, class Base>
+__device__ void smem_fft(C* buf, int P, int logP, int nl, Base base, int es, const C* __restrict__ tw,
+                         int tw_stride, bool inv, bool line_fast) {
   const int nb = P >> 1;
   for (int s = 0; s < logP; ++s) {
     const int half = 1 << s;
     const int tstep = (nb >> s) * tw_stride;
     for (int idx = threadIdx.x; idx < nl * nb; idx += blockDim.x) {
-      // tile layout (es > 1, lines contiguous): line fastest; row layout (es == 1): butterfly
-      // fastest -- either way consecutive threads touch consecutive banks
       int l, b;
-      if (es == 1) { b = idx % nb; l = idx / nb; } else { l = idx % nl; b = idx / nl; }
-      int j = b & (half - 1);
-      int i0 = ((b >> s) << (s + 1)) + j;
-      int i1 = i0 + half;
+      if (line_fast) { l = idx % nl; b = idx / nl; } else { b = idx % nb; l = idx / nb; }
+      const int j = b & (half - 1);
+      const int i0 = ((b >> s) << (s + 1)) + j;
       C w = tw[j * tstep];
       if (inv) w.y = -w.y;
-      C* p0 = buf + l * ls + i0 * es;
-      C* p1 = buf + l * ls + i1 * es;
+      C* p0 = buf + base(l) + i0 * es;
+      C* p1 = p0 + half * es;
       C a = *p0, bb = *p1;
       C t = cmul(w, bb);
       p0->x = a.x + t.x; p0->y = a.y + t.y;
@@ -58,15 +55,31 @@ __device__ void smem_fft(C* buf, int P, int logP, int nl, int ls, int es, const 
   }
 }
 
-// ---------------------------------------------------------------- X pass (contiguous lines)
-// forward: real rows (length n0 valid, P0 padded) -> H0 complex.  One CTA handles `nl` rows.
-// Row r in [0, nrows): real source offset r * in_row_stride, complex dest offset r * H0 (rows
-// are mapped (i1,i2) -> complex row index i2*P1 + i1 by the caller via row_map()).
-struct RowMap {
-  int n1, P1;        // real rows are r = i2*n1 + i1 ; complex rows are i2*P1 + i1
+// bit-reversal permutation of nl lines in place
+template <class C, class Base>
+__device__ void smem_bitrev(C* buf, int P, int logP, int nl, Base base, int es) {
+  for (int idx = threadIdx.x; idx < nl * P; idx += blockDim.x) {
+    const int l = idx % nl, e = idx / nl;
+    const int r = bitrev(e, logP);
+    if (r > e) {
+      C* p = buf + base(l);
+      C a = p[e * es]; p[e * es] = p[r * es]; p[r * es] = a;
+    }
+  }
+  __syncthreads();
+}
+
+struct RowMap {   // real rows r = i2*n1 + i1  ->  complex rows i2*P1 + i1
+  int n1, P1;
   __device__ __forceinline__ long long crow(int r) const { int i2 = r / n1, i1 = r - i2 * n1; return (long long)i2 * P1 + i1; }
 };
 
+struct RowBase {
+  int M;
+  __device__ __forceinline__ int operator()(int l) const { return l * M; }
+};
+
+// ---------------------------------------------------------------- X pass (contiguous lines)
 template <class T>
 __global__ void fft_x_forward(const T* __restrict__ in, typename Cx<T>::t* __restrict__ out, int nrows, int n0,
                               int P0, int logM, RowMap rm, const typename Cx<T>::t* __restrict__ tw, int nl) {
@@ -76,9 +89,8 @@ __global__ void fft_x_forward(const T* __restrict__ in, typename Cx<T>::t* __res
   const int M = P0 >> 1, H0 = M + 1;
   const int r0 = blockIdx.x * nl;
   const int nlines = min(nl, nrows - r0);
-  // load z_j = x_2j + i x_2j+1 in bit-reversed position
   for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    int l = idx / M, j = idx - l * M;
+    const int l = idx / M, j = idx - l * M;
     const T* row = in + (long long)(r0 + l) * n0;
     C z;
     z.x = (2 * j < n0) ? row[2 * j] : T(0);
@@ -86,15 +98,14 @@ __global__ void fft_x_forward(const T* __restrict__ in, typename Cx<T>::t* __res
     buf[l * M + bitrev(j, logM)] = z;
   }
   __syncthreads();
-  smem_fft<C>(buf, M, logM, nlines, M, 1, tw, 2, false);
+  smem_fft<C>(buf, M, logM, nlines, RowBase{M}, 1, tw, 2, false, false);
   // X_k = A_k + W^k B_k, A = (Z_k + conj Z_{M-k})/2, B = (Z_k - conj Z_{M-k})/(2i)
   for (int idx = threadIdx.x; idx < nlines * H0; idx += blockDim.x) {
-    int l = idx / H0, k = idx - l * H0;
+    const int l = idx / H0, k = idx - l * H0;
     C zk = buf[l * M + (k % M)];
     C zm = cconj(buf[l * M + ((M - k) % M)]);
     C A, B;
     A.x = T(0.5) * (zk.x + zm.x); A.y = T(0.5) * (zk.y + zm.y);
-    // (zk - zm)/(2i) = ( (zk-zm).y/2 , -(zk-zm).x/2 )
     B.x = T(0.5) * (zk.y - zm.y); B.y = -T(0.5) * (zk.x - zm.x);
     C w;
     if (k < M) w = tw[k]; else { w.x = T(-1); w.y = T(0); }
@@ -116,21 +127,20 @@ __global__ void fft_x_inverse(const typename Cx<T>::t* __restrict__ in, T* __res
   const int nlines = min(nl, nrows - r0);
   // Z_k = (X_k + conj X_{M-k}) + i W^{-k} (X_k - conj X_{M-k}),  k < M
   for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    int l = idx / M, k = idx - l * M;
+    const int l = idx / M, k = idx - l * M;
     const C* row = in + rm.crow(r0 + l) * H0;
     C xk = row[k];
     C xm = cconj(row[M - k]);
     C E; E.x = xk.x + xm.x; E.y = xk.y + xm.y;
     C D; D.x = xk.x - xm.x; D.y = xk.y - xm.y;
-    C w = cconj(tw[k]);
-    C O = cmul(w, D);
+    C O = cmul(cconj(tw[k]), D);
     C Z; Z.x = E.x - O.y; Z.y = E.y + O.x;     // E + i O
     buf[l * M + bitrev(k, logM)] = Z;
   }
   __syncthreads();
-  smem_fft<C>(buf, M, logM, nlines, M, 1, tw, 2, true);
+  smem_fft<C>(buf, M, logM, nlines, RowBase{M}, 1, tw, 2, true, false);
   for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    int l = idx / M, j = idx - l * M;
+    const int l = idx / M, j = idx - l * M;
     C z = buf[l * M + j];
     T* row = out + (long long)(r0 + l) * n0;
     if (2 * j < n0) row[2 * j] = z.x;
@@ -138,14 +148,13 @@ __global__ void fft_x_inverse(const typename Cx<T>::t* __restrict__ in, T* __res
   }
 }
 
-// ---------------------------------------------------------------- strided C2C passes
-// Lines along an axis with element stride `es` (in complex elements); a CTA takes TILE
-// consecutive columns (contiguous in memory) of one "plane" so every global access is a
-// TILE-wide contiguous segment.  Line element e of column c is at base + e*es + c.
-//   nin  : input elements 0..nin-1 are read, the rest are zero (pruning)
-//   nout : outputs 0..nout-1 are written
-//   mode : 0 forward, 1 inverse, 2 forward * spec * inverse (fused, spec real [P][ncol] at
-//          spec_base + e*spec_es + c)
+// ---------------------------------------------------------------- strided C2C pass (split plan)
+// Lines along an axis with element stride es; a CTA takes TILE consecutive columns of one
+// plane.  mode 0 forward, 1 inverse, 2 forward * spec * inverse.
+struct TileBase {
+  __device__ __forceinline__ int operator()(int l) const { return l; }
+};
+
 template <class T, int TILE>
 __global__ void fft_strided(typename Cx<T>::t* __restrict__ data, int P, int logP, long long es, int ncol,
                             long long plane_stride, int nin, int nout, int mode,
@@ -158,36 +167,87 @@ __global__ void fft_strided(typename Cx<T>::t* __restrict__ data, int P, int log
   const int nc = min(TILE, ncol - c0);
   C* base = data + (long long)blockIdx.y * plane_stride + c0;
   for (int idx = threadIdx.x; idx < P * TILE; idx += blockDim.x) {
-    int e = idx / TILE, c = idx - e * TILE;
+    const int e = idx / TILE, c = idx - e * TILE;
     C v; v.x = T(0); v.y = T(0);
     if (e < nin && c < nc) v = base[e * es + c];
     buf[bitrev(e, logP) * TILE + c] = v;
   }
   __syncthreads();
-  smem_fft<C>(buf, P, logP, TILE, 1, TILE, tw, 1, mode == 1);
+  smem_fft<C>(buf, P, logP, TILE, TileBase{}, TILE, tw, 1, mode == 1, true);
   if (mode == 2) {
     const T* sp = spec + (long long)blockIdx.y * spec_plane_stride + c0;
-    // multiply (natural order) and re-load bit-reversed for the inverse
     for (int idx = threadIdx.x; idx < P * TILE; idx += blockDim.x) {
-      int e = idx / TILE, c = idx - e * TILE;
-      T g = (c < nc) ? sp[e * spec_es + c] : T(0);
+      const int e = idx / TILE, c = idx - e * TILE;
+      const T g = (c < nc) ? sp[e * spec_es + c] : T(0);
       C v = buf[e * TILE + c];
       v.x *= g; v.y *= g;
       buf[e * TILE + c] = v;
     }
     __syncthreads();
-    // bit-reverse permutation in place (swap pairs)
-    for (int idx = threadIdx.x; idx < P * TILE; idx += blockDim.x) {
-      int e = idx / TILE, c = idx - e * TILE;
-      int r = bitrev(e, logP);
-      if (r > e) { C a = buf[e * TILE + c]; buf[e * TILE + c] = buf[r * TILE + c]; buf[r * TILE + c] = a; }
-    }
-    __syncthreads();
-    smem_fft<C>(buf, P, logP, TILE, 1, TILE, tw, 1, true);
+    smem_bitrev<C>(buf, P, logP, TILE, TileBase{}, TILE);
+    smem_fft<C>(buf, P, logP, TILE, TileBase{}, TILE, tw, 1, true, true);
   }
   for (int idx = threadIdx.x; idx < nout * TILE; idx += blockDim.x) {
-    int e = idx / TILE, c = idx - e * TILE;
+    const int e = idx / TILE, c = idx - e * TILE;
     if (c < nc) base[e * es + c] = buf[e * TILE + c];
+  }
+}
+
+// ---------------------------------------------------------------- fused YZ pass (fused plan)
+struct PlaneBase {   // line l = (plane index l / tile, column l % tile); logP2 = 0: natural order
+  int tile, plane, logP2;
+  __device__ __forceinline__ int operator()(int l) const {
+    const int p = l / tile;
+    return (logP2 ? bitrev(p, logP2) : p) * plane + (l - p * tile);
+  }
+};
+
+// smem [P2][P1][tile] (tile columns contiguous).  Planes are stored at bit-reversed z
+// positions so the y transforms of the n2 data planes leave the z lines in DIT input order.
+template <class T>
+__global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P1, int logP1, int n2, int P2,
+                             int logP2, int H0, int tile, const T* __restrict__ spec,
+                             const typename Cx<T>::t* __restrict__ tw1, const typename Cx<T>::t* __restrict__ tw2) {
+  using C = typename Cx<T>::t;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* buf = reinterpret_cast<C*>(smem_raw);
+  const int c0 = blockIdx.x * tile;
+  const int nc = min(tile, H0 - c0);
+  const int plane = P1 * tile;
+  // zero the whole tile (padded planes / rows must read as zero), then load the data block
+  for (int idx = threadIdx.x; idx < P2 * plane; idx += blockDim.x) { C z; z.x = T(0); z.y = T(0); buf[idx] = z; }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
+    const int c = idx % tile, r = idx / tile, i1 = r % n1, i2 = r / n1;
+    if (c < nc)
+      buf[bitrev(i2, logP2) * plane + bitrev(i1, logP1) * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
+  }
+  __syncthreads();
+  // forward y on the n2 data planes: line (i2, c) base = bitrev(i2)*plane + c, stride tile
+  const PlaneBase ybase{tile, plane, logP2};
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, true);
+  // forward z on every (k1, c): base = k1*tile + c, stride plane
+  const TileBase zbase{};
+  smem_fft<C>(buf, P2, logP2, plane, zbase, plane, tw2, 1, false, true);
+  // multiply by the real spectrum G_hat[k2][k1][k0] (natural order now)
+  for (int idx = threadIdx.x; idx < P2 * plane; idx += blockDim.x) {
+    const int c = idx % tile, r = idx / tile, k1 = r % P1, k2 = r / P1;
+    const T g = (c < nc) ? spec[((long long)k2 * P1 + k1) * H0 + c0 + c] : T(0);
+    C v = buf[idx];
+    v.x *= g; v.y *= g;
+    buf[idx] = v;
+  }
+  __syncthreads();
+  // inverse z (bit-reverse first); only planes i2 < n2 are needed afterwards
+  smem_bitrev<C>(buf, P2, logP2, plane, zbase, plane);
+  smem_fft<C>(buf, P2, logP2, plane, zbase, plane, tw2, 1, true, true);
+  // inverse y on planes i2 < n2 (natural z order now)
+  const PlaneBase ybase2{tile, plane, 0};
+  smem_bitrev<C>(buf, P1, logP1, n2 * tile, ybase2, tile);
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, true);
+  for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
+    const int c = idx % tile, r = idx / tile, i1 = r % n1, i2 = r / n1;
+    if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * plane + i1 * tile + c];
   }
 }
 
