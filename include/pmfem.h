@@ -99,6 +99,21 @@ typedef struct {
 pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
                          const pmfem_grid* grid, int cuda_device);
 
+/* Multi-GPU context: every rank passes the FULL mesh; the library runs the
+ * same deterministic setup, partitions the internal (box-sorted, z-slowest) rows into `world`
+ * contiguous, cost-balanced slab ranges and builds halo lists for m (K1 columns), q (C_box
+ * columns) and u (ring-1 columns).  m and H passed to the field calls then cover this rank's
+ * rows only ([n_parents_local][3], order from pmfem_get_order).  Per evaluation: grouped
+ * ncclSend/ncclRecv halo exchanges with every peer that shares a boundary, one ncclAllReduce
+ * of the anterpolated grid Q, and a replicated FFT convolution.  nccl_unique_id: 128 bytes
+ * from pmfem_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
+ * cuda_device = -1 builds the host-only plan (exportable: dist_bounds, send_/recv_{m,q,u}_{ptr,idx}).
+ * world = 1 is identical to pmfem_setup. */
+pmfem_status pmfem_setup_dist(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
+                              const pmfem_grid* grid, int cuda_device, const void* nccl_unique_id,
+                              int rank, int world);
+pmfem_status pmfem_nccl_unique_id(void* out128);
+
 /* Tabulate the periodic Green's function K on the padded grid with Ewald sums in fp64
  * (Eq. 2 with k0 = 0; "exponentially rapidly convergent sums"; normalisation
  * R3), K(0) = G_p^reg(0), and store G_hat = real(FFT(K)) / (#FFT points), G_hat[0] = 0, as fp32

@@ -7,4 +7,4 @@
 
 The package is a thin binding; all arithmetic of the hot path runs in csrc/ (CUDA, sm_100a).
 """
-from .pmfem import Context, PmfemError, LIB_PATH, KERNELS, library_symbols  # noqa: F401
+from .pmfem import Context, PmfemError, LIB_PATH, KERNELS, library_symbols, nccl_unique_id  # noqa: F401

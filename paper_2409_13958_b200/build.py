@@ -7,8 +7,18 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libpmfem.so")
 SOURCES = ["pmfem_api.cu", "device.cu", "setup_mesh.cpp", "setup_operators.cpp", "setup_z0.cpp",
-           "setup_aim.cpp", "pgf_host.cpp"]
+           "setup_aim.cpp", "setup_dist.cpp", "pgf_host.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def nccl_dirs():
+    """NCCL headers + library: the copy torch loads (same soname), so one libnccl is in use."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        return os.path.join(base, "include"), os.path.join(base, "lib")
+    except Exception:
+        return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
 def nvcc():
@@ -39,7 +49,7 @@ def build(force=False, verbose=False):
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc(), "-c", os.path.join(CSRC, src), "-o", obj, "-O3", "-std=c++17", "-lineinfo",
-               "-Xcompiler", "-fPIC,-fopenmp,-O3", "-I", os.path.join(HERE, "..", "include"),
+               "-Xcompiler", "-fPIC,-fopenmp,-O3", "-I", os.path.join(HERE, "..", "include"), "-I", nccl_dirs()[0],
                "--expt-relaxed-constexpr"] + ARCH
         if src.endswith(".cpp"):
             cmd += ["-x", "cu"] if False else []
@@ -55,7 +65,9 @@ def build(force=False, verbose=False):
             sys.stderr.write(out)
     if failed:
         raise RuntimeError("libpmfem build failed")
-    link = [nvcc(), "-shared", "-o", LIB] + objs + ARCH + ["-Xcompiler", "-fopenmp", "-lgomp"]
+    inc, libdir = nccl_dirs()
+    link = [nvcc(), "-shared", "-o", LIB] + objs + ARCH + ["-Xcompiler", "-fopenmp", "-lgomp", "-L", libdir,
+                                                           "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode())

@@ -23,6 +23,7 @@
 #include "device.cuh"
 #include "fft.cuh"
 #include "pgf.cuh"
+#include <nccl.h>
 
 namespace pmfem {
 
@@ -50,16 +51,38 @@ T* dupload(const std::vector<T>& v) {
 }
 int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 
+// Rows [row0, row1) of the internal order are processed; per-row outputs H are stored at
+// n - hoff (hoff = row0 for the rank-local H of a distributed context, 0 otherwise).
+struct RowRange {
+  int64_t row0, row1, hoff;
+};
+
+// halo pack / unpack: buf[i*w + c] <-> v[idx[i]*w + c]
+__global__ void k_pack(const float* __restrict__ v, const int32_t* __restrict__ idx, int64_t n, int w,
+                       float* __restrict__ buf) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * w) return;
+  const int64_t i = t / w;
+  buf[t] = v[(int64_t)idx[i] * w + (t - i * w)];
+}
+__global__ void k_unpack(const float* __restrict__ buf, const int32_t* __restrict__ idx, int64_t n, int w,
+                         float* __restrict__ v) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * w) return;
+  const int64_t i = t / w;
+  v[(int64_t)idx[i] * w + (t - i * w)] = buf[t];
+}
+
 // ------------------------------------------------------------------ K1 local_in
 // One thread per row (SELL-32).  Reads m (gathered), the shared column list, Z0 (3 planes),
 // (L, D) on the ring-1 prefix and the row sums; writes q, u_loc and (heff) H_ex.
 __global__ void __launch_bounds__(256) k1_local_in(
-    int64_t Np, const float* __restrict__ m, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
+    RowRange rr, const float* __restrict__ m, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
     const int32_t* __restrict__ s_col, const float* __restrict__ s_z, int64_t zt, const float4* __restrict__ s_LD,
     const float4* __restrict__ rowsum, float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H,
     int write_hex) {
-  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= Np) return;
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= rr.row1) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
   const int64_t o = sl_off[s], o1 = sl1_off[s];
@@ -87,16 +110,16 @@ __global__ void __launch_bounds__(256) k1_local_in(
   const float4 rd = rowsum[2 * n], rz = rowsum[2 * n + 1];
   q[n] = qq + rd.x * mx + rd.y * my + rd.z * mz;
   uloc[n] = ul + rz.x * mx + rz.y * my + rz.z * mz;
-  if (write_hex) { H[3 * n] = hx; H[3 * n + 1] = hy; H[3 * n + 2] = hz; }
+  if (write_hex) { H[3 * (n - rr.hoff)] = hx; H[3 * (n - rr.hoff) + 1] = hy; H[3 * (n - rr.hoff) + 2] = hz; }
 }
 
 // exchange only: H = L m
-__global__ void __launch_bounds__(256) k_exchange(int64_t Np, const float* __restrict__ m,
+__global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float* __restrict__ m,
                                                   const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
                                                   const int32_t* __restrict__ s_col, const float4* __restrict__ s_LD,
                                                   float* __restrict__ H) {
-  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= Np) return;
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= rr.row1) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
   const int64_t o = sl_off[s], o1 = sl1_off[s];
@@ -110,7 +133,7 @@ __global__ void __launch_bounds__(256) k_exchange(int64_t Np, const float* __res
     const float L = __ldg(&s_LD[e1].x);
     hx = fmaf(L, m[3 * c] - mx, hx); hy = fmaf(L, m[3 * c + 1] - my, hy); hz = fmaf(L, m[3 * c + 2] - mz, hz);
   }
-  H[3 * n] = hx; H[3 * n + 1] = hy; H[3 * n + 2] = hz;
+  H[3 * (n - rr.hoff)] = hx; H[3 * (n - rr.hoff) + 1] = hy; H[3 * (n - rr.hoff) + 2] = hz;
 }
 
 // Lagrange weights on nodes 0..P at local coordinate t
@@ -132,10 +155,10 @@ __device__ __forceinline__ int wrapi(int i, int n, int per) { return per ? (i >=
 
 // ------------------------------------------------------------------ K2 anterpolation
 template <int P>
-__global__ void __launch_bounds__(256) k2_anterp(int64_t Np, const float* __restrict__ q, const int4* __restrict__ st_s,
+__global__ void __launch_bounds__(256) k2_anterp(RowRange rr, const float* __restrict__ q, const int4* __restrict__ st_s,
                                                  const float4* __restrict__ st_t, GridDims g, float* __restrict__ Q) {
-  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= Np) return;
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= rr.row1) return;
   const int4 s = st_s[n];
   const float4 t = st_t[n];
   const float qn = q[n];
@@ -157,14 +180,14 @@ __global__ void __launch_bounds__(256) k2_anterp(int64_t Np, const float* __rest
 
 // ------------------------------------------------------------------ K4 interpolation + precorrection
 template <int P>
-__global__ void __launch_bounds__(256) k4_interp_corr(int64_t Np, const float* __restrict__ U, const int4* __restrict__ st_s,
+__global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
                                                       const float4* __restrict__ st_t, GridDims g,
                                                       const int64_t* __restrict__ c_ptr, const int4* __restrict__ c_col4,
                                                       const float4* __restrict__ c_val4, const float* __restrict__ q,
                                                       const float* __restrict__ uloc, float* __restrict__ u) {
   const int lane = threadIdx.x & 31;
-  const int64_t n = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (n >= Np) return;
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (n >= rr.row1) return;
   float acc = 0.f;
   const int64_t b = c_ptr[n] >> 2, e_end = c_ptr[n + 1] >> 2;
 #pragma unroll 2
@@ -197,12 +220,12 @@ __global__ void __launch_bounds__(256) k4_interp_corr(int64_t Np, const float* _
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
-__global__ void __launch_bounds__(256) k5_grad_sum(int64_t Np, const float* __restrict__ u, const int64_t* __restrict__ sl_off,
+__global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __restrict__ u, const int64_t* __restrict__ sl_off,
                                                    const int64_t* __restrict__ sl1_off, const int32_t* __restrict__ s_col,
                                                    const float* __restrict__ s_G, int64_t gt, float* __restrict__ H,
                                                    int accumulate) {
-  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= Np) return;
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= rr.row1) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
   const int64_t o = sl_off[s], o1 = sl1_off[s];
@@ -218,8 +241,8 @@ __global__ void __launch_bounds__(256) k5_grad_sum(int64_t Np, const float* __re
     gy = fmaf(__ldg(s_G + gt + e1), du, gy);
     gz = fmaf(__ldg(s_G + 2 * gt + e1), du, gz);
   }
-  if (accumulate) { H[3 * n] -= gx; H[3 * n + 1] -= gy; H[3 * n + 2] -= gz; }
-  else { H[3 * n] = -gx; H[3 * n + 1] = -gy; H[3 * n + 2] = -gz; }
+  if (accumulate) { H[3 * (n - rr.hoff)] -= gx; H[3 * (n - rr.hoff) + 1] -= gy; H[3 * (n - rr.hoff) + 2] -= gz; }
+  else { H[3 * (n - rr.hoff)] = -gx; H[3 * (n - rr.hoff) + 1] = -gy; H[3 * (n - rr.hoff) + 2] = -gz; }
 }
 
 // ------------------------------------------------------------------ PGF table (fp64)
@@ -315,6 +338,10 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.order = S.order;
   for (int a = 0; a < 3; ++a) { D.periodic[a] = S.periodic[a]; D.n[a] = S.grid_n[a]; D.P[a] = S.fft_n[a]; }
   D.H0 = D.P[0] / 2 + 1;
+  D.rank = S.dist.rank;
+  D.world = S.dist.world;
+  D.lo = S.dist.lo();
+  D.hi = S.dist.hi();
 
   // ---- shared local operator in SELL-32, internal order
   const int64_t ns = (Np + 31) / 32;
@@ -507,38 +534,110 @@ void device_free(DeviceState& D) {
   cudaSetDevice(D.device);
   void* ptrs[] = {D.sl_off, D.sl1_off, D.s_col, D.s_z, D.s_LD, D.s_G, D.rowsum, D.c_ptr, D.c_col, D.c_val,
                   D.st_s, D.st_t, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
-                  D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2]};
+                  D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
+                  D.mfull, D.send_buf, D.recv_buf, D.send_idx[0], D.send_idx[1], D.send_idx[2],
+                  D.recv_idx[0], D.recv_idx[1], D.recv_idx[2]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int i = 0; i < 8; ++i)
     if (D.ev[i]) cudaEventDestroy(D.ev[i]);
+  if (D.comm) ncclCommDestroy((ncclComm_t)D.comm);
 }
 
+#define NCK(x)                                                                                  \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) throw Error(PMFEM_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id) {
+  CK(cudaSetDevice(D.device));
+  const DistPlan& P = S.dist;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, sizeof(id));
+  ncclComm_t comm;
+  NCK(ncclCommInitRank(&comm, P.world, id, P.rank));
+  D.comm = comm;
+  int64_t sbuf = 0, rbuf = 0;
+  const int width[3] = {3, 1, 1};
+  D.comm_bytes_per_eval = 4.0 * (double)D.n[0] * D.n[1] * D.n[2] * 2.0 * (P.world - 1) / P.world;  // ring all-reduce
+  for (int k = 0; k < 3; ++k) {
+    D.send_ptr[k] = P.send_ptr[k];
+    D.recv_ptr[k] = P.recv_ptr[k];
+    D.send_idx[k] = dupload(P.send_idx[k]);
+    D.recv_idx[k] = dupload(P.recv_idx[k]);
+    sbuf = std::max<int64_t>(sbuf, (int64_t)P.send_idx[k].size() * width[k]);
+    rbuf = std::max<int64_t>(rbuf, (int64_t)P.recv_idx[k].size() * width[k]);
+    D.comm_bytes_per_eval += 4.0 * width[k] * (double)(P.send_idx[k].size() + P.recv_idx[k].size());
+  }
+  D.send_buf = dalloc<float>(sbuf);
+  D.recv_buf = dalloc<float>(rbuf);
+  D.mfull = dalloc<float>(3 * (size_t)D.Np);
+  CK(cudaMemset(D.mfull, 0, 12 * (size_t)D.Np));
+}
+
+namespace {
+// halo exchange of vector v (width w floats per row) for plan kind k: pack my rows that peers
+// need, grouped NCCL send/recv with every peer, unpack the received rows in place
+void halo(DeviceState& D, int k, float* v, int w, cudaStream_t st) {
+  if (D.world <= 1) return;
+  const int64_t ns = D.send_ptr[k][D.world], nr = D.recv_ptr[k][D.world];
+  if (ns) {
+    k_pack<<<(unsigned)((ns * w + 255) / 256), 256, 0, st>>>(v, D.send_idx[k], ns, w, D.send_buf);
+    CK(cudaGetLastError());
+  }
+  ncclComm_t comm = (ncclComm_t)D.comm;
+  NCK(ncclGroupStart());
+  for (int p = 0; p < D.world; ++p) {
+    const int64_t sc = D.send_ptr[k][p + 1] - D.send_ptr[k][p];
+    const int64_t rc = D.recv_ptr[k][p + 1] - D.recv_ptr[k][p];
+    if (sc) NCK(ncclSend(D.send_buf + D.send_ptr[k][p] * w, (size_t)(sc * w), ncclFloat, p, comm, st));
+    if (rc) NCK(ncclRecv(D.recv_buf + D.recv_ptr[k][p] * w, (size_t)(rc * w), ncclFloat, p, comm, st));
+  }
+  NCK(ncclGroupEnd());
+  if (nr) {
+    k_unpack<<<(unsigned)((nr * w + 255) / 256), 256, 0, st>>>(D.recv_buf, D.recv_idx[k], nr, w, v);
+    CK(cudaGetLastError());
+  }
+}
+}  // namespace
+
+// m, H: [hi-lo][3] rank-local rows (the full [N'][3] on a single GPU)
 void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, EvalMode mode) {
-  const int64_t Np = D.Np;
-  const unsigned thr_blocks = (unsigned)((Np + 255) / 256);      // thread per row
-  const unsigned warp_blocks = (unsigned)((Np + 7) / 8);         // warp per row, 8 warps per block
+  const RowRange rr{D.lo, D.hi, D.lo};
+  const int64_t nrows = D.hi - D.lo;
+  if (nrows <= 0) return;
+  const unsigned thr_blocks = (unsigned)((nrows + 255) / 256);   // thread per row
+  const unsigned warp_blocks = (unsigned)((nrows + 7) / 8);      // warp per row, 8 warps per block
   const int64_t zt_h = D.zt, gt_h = D.gt;                        // SoA plane strides
+  auto mark = [&](int i) { if (D.timing) CK(cudaEventRecord(D.ev[i], st)); };
+  mark(0);
+  const float* mg = m - 3 * D.lo;                                 // global-row view of m
+  if (D.world > 1) {
+    CK(cudaMemcpyAsync(D.mfull + 3 * D.lo, m, 12 * (size_t)nrows, cudaMemcpyDeviceToDevice, st));
+    halo(D, 0, D.mfull, 3, st);
+    mg = D.mfull;
+  }
   if (mode == EVAL_EXCHANGE) {
-    k_exchange<<<thr_blocks, 256, 0, st>>>(Np, m, D.sl_off, D.sl1_off, D.s_col, D.s_LD, H);
+    k_exchange<<<thr_blocks, 256, 0, st>>>(rr, mg, D.sl_off, D.sl1_off, D.s_col, D.s_LD, H);
     CK(cudaGetLastError());
     return;
   }
   if (!D.pgf_ready) throw Error(PMFEM_E_STATE, "pmfem_build_pgf has not been called");
-  auto mark = [&](int i) { if (D.timing) CK(cudaEventRecord(D.ev[i], st)); };
   GridDims g{D.n[0], D.n[1], D.n[2], D.periodic[0], D.periodic[1], D.periodic[2]};
-  mark(0);
-  k1_local_in<<<thr_blocks, 256, 0, st>>>(Np, m, D.sl_off, D.sl1_off, D.s_col, D.s_z, zt_h, D.s_LD, D.rowsum, D.q,
+  k1_local_in<<<thr_blocks, 256, 0, st>>>(rr, mg, D.sl_off, D.sl1_off, D.s_col, D.s_z, zt_h, D.s_LD, D.rowsum, D.q,
                                           D.uloc, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(1);
-  CK(cudaMemsetAsync(D.Q, 0, sizeof(float) * (size_t)D.n[0] * D.n[1] * D.n[2], st));
+  const size_t G = (size_t)D.n[0] * D.n[1] * D.n[2];
+  CK(cudaMemsetAsync(D.Q, 0, sizeof(float) * G, st));
   switch (D.order) {
-    case 1: k2_anterp<1><<<thr_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
-    case 2: k2_anterp<2><<<thr_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
-    default: k2_anterp<3><<<thr_blocks, 256, 0, st>>>(Np, D.q, D.st_s, D.st_t, g, D.Q); break;
+    case 1: k2_anterp<1><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
+    case 2: k2_anterp<2><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
+    default: k2_anterp<3><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
   }
   CK(cudaGetLastError());
+  if (D.world > 1) NCK(ncclAllReduce(D.Q, D.Q, G, ncclFloat, ncclSum, (ncclComm_t)D.comm, st));
   mark(2);
   {
     const int n0 = D.n[0], n1 = D.n[1], n2 = D.n[2], P0 = D.P[0], P1 = D.P[1], P2 = D.P[2], H0 = D.H0;
@@ -553,17 +652,19 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     }
     launch_x<float>(false, nullptr, D.C, D.Q, n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
   }
+  halo(D, 1, D.q, 1, st);
   mark(3);
   const int4* c4 = reinterpret_cast<const int4*>(D.c_col);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   switch (D.order) {
-    case 1: k4_interp_corr<1><<<warp_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
-    case 2: k4_interp_corr<2><<<warp_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
-    default: k4_interp_corr<3><<<warp_blocks, 256, 0, st>>>(Np, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
+    case 1: k4_interp_corr<1><<<warp_blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
+    case 2: k4_interp_corr<2><<<warp_blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
+    default: k4_interp_corr<3><<<warp_blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
   }
   CK(cudaGetLastError());
+  halo(D, 2, D.u, 1, st);
   mark(4);
-  k5_grad_sum<<<thr_blocks, 256, 0, st>>>(Np, D.u, D.sl_off, D.sl1_off, D.s_col, D.s_G, gt_h, H, mode == EVAL_HEFF ? 1 : 0);
+  k5_grad_sum<<<thr_blocks, 256, 0, st>>>(rr, D.u, D.sl_off, D.sl1_off, D.s_col, D.s_G, gt_h, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(5);
 }

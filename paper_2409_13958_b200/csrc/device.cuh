@@ -53,7 +53,22 @@ struct DeviceState {
   float last_ms[8] = {0};
   double kernel_bytes[8] = {0};
   int launches_per_eval = 0;
+  // multi-GPU (world > 1): this rank owns internal rows [lo, hi); gathered vectors are kept
+  // full length (global column indices) and filled at owned + halo rows; the anterpolated
+  // grid is all-reduced and the FFT convolution is replicated on every rank.
+  int rank = 0, world = 1;
+  int64_t lo = 0, hi = 0;
+  void* comm = nullptr;                         // ncclComm_t
+  float* mfull = nullptr;                       // [N'][3] full-length m (world > 1)
+  std::vector<int64_t> send_ptr[3], recv_ptr[3];
+  int32_t* send_idx[3] = {nullptr, nullptr, nullptr};
+  int32_t* recv_idx[3] = {nullptr, nullptr, nullptr};
+  float* send_buf = nullptr;
+  float* recv_buf = nullptr;
+  double comm_bytes_per_eval = 0;
 };
+
+void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id);
 
 void device_upload(DeviceState& D, const HostSetup& S);
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& P);

@@ -2,6 +2,7 @@
 #include <chrono>
 #include <cstring>
 #include <string>
+#include <nccl.h>
 #include "device.cuh"
 #include "pmfem_internal.h"
 
@@ -53,8 +54,8 @@ void record_timing(pmfem_ctx ctx, cudaStream_t st) {
 
 extern "C" {
 
-pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
-                         const pmfem_grid* grid, int cuda_device) {
+static pmfem_status setup_impl(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
+                               const pmfem_grid* grid, int cuda_device, const void* nccl_id, int rank, int world) {
   if (!out) { g_setup_err = "NULL out"; return PMFEM_E_INVALID_ARG; }
   *out = nullptr;
   pmfem_ctx ctx = nullptr;
@@ -75,11 +76,16 @@ pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_per
     pmfem::setup_z0(S);
     pmfem::setup_aim(S, grid);
     pmfem::setup_order(S);
+    pmfem::setup_dist(S, rank, world);
     S.setup_seconds = now() - t0;
     if (cuda_device >= 0) {
       ctx->host_only = false;
       ctx->D.device = cuda_device;
       pmfem::device_upload(ctx->D, S);
+      if (world > 1) {
+        pmfem::require(nccl_id != nullptr, PMFEM_E_INVALID_ARG, "NULL NCCL unique id");
+        pmfem::device_init_comm(ctx->D, S, nccl_id);
+      }
     }
   });
   if (st != PMFEM_OK) {
@@ -88,6 +94,27 @@ pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_per
     return st;
   }
   *out = ctx;
+  return PMFEM_OK;
+}
+
+pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
+                         const pmfem_grid* grid, int cuda_device) {
+  return setup_impl(out, mesh, per, grid, cuda_device, nullptr, 0, 1);
+}
+
+pmfem_status pmfem_setup_dist(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
+                              const pmfem_grid* grid, int cuda_device, const void* nccl_unique_id, int rank,
+                              int world) {
+  if (world < 1 || rank < 0 || rank >= world) { g_setup_err = "bad rank/world"; return PMFEM_E_INVALID_ARG; }
+  return setup_impl(out, mesh, per, grid, cuda_device, nccl_unique_id, rank, world);
+}
+
+pmfem_status pmfem_nccl_unique_id(void* out128) {
+  if (!out128) return PMFEM_E_INVALID_ARG;
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) { g_setup_err = ncclGetErrorString(r); return PMFEM_E_NCCL; }
+  std::memcpy(out128, &id, sizeof(id));
   return PMFEM_OK;
 }
 
@@ -127,7 +154,7 @@ pmfem_status pmfem_heff_host(pmfem_ctx ctx, const float* m_host, float* H_host, 
     pmfem::require(!ctx->host_only, PMFEM_E_STATE, "host-only context");
     pmfem::require(m_host && H_host, PMFEM_E_INVALID_ARG, "NULL host buffer");
     cudaSetDevice(ctx->D.device);
-    const size_t bytes = sizeof(float) * 3 * (size_t)ctx->D.Np;
+    const size_t bytes = sizeof(float) * 3 * (size_t)(ctx->D.hi - ctx->D.lo);   // rank-local rows
     if (!ctx->D.m_stage) {
       if (cudaMalloc(&ctx->D.m_stage, bytes) != cudaSuccess || cudaMalloc(&ctx->D.H_stage, bytes) != cudaSuccess)
         throw pmfem::Error(PMFEM_E_OOM, "staging allocation failed");
@@ -149,7 +176,7 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
   std::memset(out, 0, sizeof(*out));
   out->n_nodes = S.N;
   out->n_parents = S.Np;
-  out->n_parents_local = S.Np;
+  out->n_parents_local = S.dist.hi() - S.dist.lo();
   out->periodic_dims = S.periodic[0] + S.periodic[1] + S.periodic[2];
   out->touching = S.touching;
   out->protruding = S.protruding;
@@ -167,7 +194,8 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
 
 pmfem_status pmfem_get_order(pmfem_ctx ctx, int64_t* internal_to_user) {
   if (!ctx || !internal_to_user) return PMFEM_E_INVALID_ARG;
-  for (int64_t i = 0; i < ctx->S.Np; ++i) internal_to_user[i] = ctx->S.parent[ctx->S.perm[i]];
+  const pmfem::HostSetup& S = ctx->S;
+  for (int64_t i = S.dist.lo(); i < S.dist.hi(); ++i) internal_to_user[i - S.dist.lo()] = S.parent[S.perm[i]];
   return PMFEM_OK;
 }
 
@@ -201,6 +229,20 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     else if (n == "grid_delta") put(S.delta, 3, 8);
     else if (n == "grid_origin") put(S.origin, 3, 8);
     else if (n == "perm") put(S.perm.data(), S.Np, 8);
+    else if (n == "dist_bounds") put(S.dist.bounds.data(), (int64_t)S.dist.bounds.size(), 8);
+    else if (n.rfind("send_", 0) == 0 || n.rfind("recv_", 0) == 0) {
+      const std::string kinds = "mqu";
+      const bool snd = n[0] == 's';
+      const size_t kpos = kinds.find(n[5]);
+      if (kpos == std::string::npos || n.size() < 8) throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
+      const int k = (int)kpos;
+      const std::string tail = n.substr(7);
+      if (tail == "ptr") put(snd ? S.dist.send_ptr[k].data() : S.dist.recv_ptr[k].data(), S.dist.world + 1, 8);
+      else if (tail == "idx") {
+        const auto& v = snd ? S.dist.send_idx[k] : S.dist.recv_idx[k];
+        put(v.data(), (int64_t)v.size(), 4);
+      } else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
+    }
     else if (n == "kernel") put(S.kernel.data(), (int64_t)S.kernel.size(), 8);
     else if (n == "spectrum") put(S.spectrum.data(), (int64_t)S.spectrum.size(), 8);
     else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");

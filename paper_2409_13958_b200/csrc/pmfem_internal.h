@@ -27,6 +27,17 @@ struct Csr {
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 
+// Multi-GPU plan: contiguous internal-row ranges per rank and halo exchange index lists
+// (internal row indices) for the gathered vectors M (m), Q (q), U (u).
+struct DistPlan {
+  int rank = 0, world = 1;
+  std::vector<int64_t> bounds{0, 0};           // [world+1] internal row boundaries
+  std::vector<int64_t> send_ptr[3], recv_ptr[3];  // [world+1] per peer
+  std::vector<int32_t> send_idx[3], recv_idx[3];  // my rows to send / peer rows to receive
+  int64_t lo() const { return bounds[rank]; }
+  int64_t hi() const { return bounds[rank + 1]; }
+};
+
 // Host setup products (all in fp64, rows/cols in USER parent order [0, N')).
 struct HostSetup {
   // inputs
@@ -75,6 +86,7 @@ struct HostSetup {
   std::vector<double> kernel;       // host-only contexts: K table [fft2][fft1][fft0]
   std::vector<double> spectrum;     // host-only: G_hat half spectrum [fft2][fft1][fft0/2+1]
   double setup_seconds = 0, pgf_seconds = 0;
+  DistPlan dist;
 };
 
 void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* per);
@@ -82,6 +94,7 @@ void setup_operators(HostSetup& S);
 void setup_z0(HostSetup& S);
 void setup_aim(HostSetup& S, const pmfem_grid* g);
 void setup_order(HostSetup& S);
+void setup_dist(HostSetup& S, int rank, int world);
 
 // Periodic Green's function (Ewald) -- host/device fp64, defined in pgf.cuh.
 struct PgfParams {

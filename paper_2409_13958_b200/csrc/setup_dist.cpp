@@ -1,0 +1,85 @@
+// Host setup, multi-GPU plan: contiguous row partition of the internal
+// (box-sorted, z-slowest) order = slab-aligned mesh partition, and the halo exchange lists
+// for the three gathered vectors of the evaluation:
+//   M: m at the shared local-operator columns (K1: ring-1 + Z0)
+//   Q: q at the C_box columns (K4)
+//   U: u at the ring-1 columns (K5)
+// Every rank runs the same deterministic setup on the full mesh, so each rank computes every
+// peer's needs locally: no coordination is required to build the plan.
+#include <algorithm>
+#include <numeric>
+#include <omp.h>
+#include "pmfem_internal.h"
+
+namespace pmfem {
+
+void setup_dist(HostSetup& S, int rank, int world) {
+  require(world >= 1 && rank >= 0 && rank < world, PMFEM_E_INVALID_ARG, "bad rank / world");
+  DistPlan& D = S.dist;
+  D.rank = rank;
+  D.world = world;
+  const int64_t Np = S.Np;
+  // per-row cost in bytes of the streamed operators (balanced partition)
+  std::vector<double> cost(Np);
+  for (int64_t i = 0; i < Np; ++i) {
+    const int64_t r = S.perm[i];
+    cost[i] = 64.0 + 20.0 * (S.ring1.rowptr[r + 1] - S.ring1.rowptr[r]) + 16.0 * (S.z0.rowptr[r + 1] - S.z0.rowptr[r]) +
+              8.0 * (S.cbox.rowptr[r + 1] - S.cbox.rowptr[r]);
+  }
+  std::vector<double> pre(Np + 1, 0.0);
+  for (int64_t i = 0; i < Np; ++i) pre[i + 1] = pre[i] + cost[i];
+  D.bounds.assign(world + 1, 0);
+  D.bounds[world] = Np;
+  for (int w = 1; w < world; ++w) {
+    const double target = pre[Np] * w / world;
+    int64_t i = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+    i = (i + 16) / 32 * 32;                              // SELL slices never straddle ranks
+    D.bounds[w] = std::min<int64_t>(std::max<int64_t>(i, D.bounds[w - 1]), Np);
+  }
+  auto owner = [&](int64_t i) {
+    return (int)(std::upper_bound(D.bounds.begin(), D.bounds.end(), i) - D.bounds.begin()) - 1;
+  };
+  // needed external rows of rank p for kind k
+  const Csr* ops[3][2] = {{&S.ring1, &S.z0}, {&S.cbox, nullptr}, {&S.ring1, nullptr}};
+  std::vector<std::vector<int32_t>> need[3];
+  for (int k = 0; k < 3; ++k) need[k].resize(world);
+#pragma omp parallel for collapse(2) schedule(dynamic)
+  for (int k = 0; k < 3; ++k)
+    for (int p = 0; p < world; ++p) {
+      std::vector<int32_t> v;
+      for (int64_t i = D.bounds[p]; i < D.bounds[p + 1]; ++i) {
+        const int64_t r = S.perm[i];
+        for (int o = 0; o < 2; ++o) {
+          const Csr* A = ops[k][o];
+          if (!A) continue;
+          for (int64_t e = A->rowptr[r]; e < A->rowptr[r + 1]; ++e) {
+            const int64_t c = S.iperm[A->col[e]];
+            if (c < D.bounds[p] || c >= D.bounds[p + 1]) v.push_back((int32_t)c);
+          }
+        }
+      }
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      need[k][p] = std::move(v);
+    }
+  for (int k = 0; k < 3; ++k) {
+    D.send_ptr[k].assign(world + 1, 0);
+    D.recv_ptr[k].assign(world + 1, 0);
+    D.send_idx[k].clear();
+    D.recv_idx[k].clear();
+    for (int p = 0; p < world; ++p) {
+      // what peer p needs from me
+      if (p != rank)
+        for (int32_t c : need[k][p])
+          if (owner(c) == rank) D.send_idx[k].push_back(c);
+      D.send_ptr[k][p + 1] = (int64_t)D.send_idx[k].size();
+      // what I need from peer p
+      if (p != rank)
+        for (int32_t c : need[k][rank])
+          if (owner(c) == p) D.recv_idx[k].push_back(c);
+      D.recv_ptr[k][p + 1] = (int64_t)D.recv_idx[k].size();
+    }
+  }
+}
+
+}  // namespace pmfem

@@ -22,7 +22,7 @@ STATUS = {0: "PMFEM_OK", 1: "PMFEM_E_INVALID_ARG", 2: "PMFEM_E_MESH", 3: "PMFEM_
           7: "PMFEM_E_PGF_NOT_CONVERGED", 8: "PMFEM_E_STATE", 9: "PMFEM_E_CUDA", 10: "PMFEM_E_NCCL",
           11: "PMFEM_E_OOM"}
 
-SYMBOLS = ["pmfem_setup", "pmfem_build_pgf", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
+SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
            "pmfem_heff_host", "pmfem_query", "pmfem_get_order", "pmfem_export", "pmfem_set_timing",
            "pmfem_get_timing", "pmfem_last_error", "pmfem_destroy"]
 
@@ -62,6 +62,9 @@ class _Info(ctypes.Structure):
 _vp = ctypes.c_void_p
 _lib.pmfem_setup.argtypes = [ctypes.POINTER(_vp), ctypes.POINTER(_Mesh), ctypes.POINTER(_Periodicity),
                              ctypes.POINTER(_Grid), ctypes.c_int]
+_lib.pmfem_setup_dist.argtypes = [ctypes.POINTER(_vp), ctypes.POINTER(_Mesh), ctypes.POINTER(_Periodicity),
+                                  ctypes.POINTER(_Grid), ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+_lib.pmfem_nccl_unique_id.argtypes = [ctypes.c_void_p]
 _lib.pmfem_build_pgf.argtypes = [_vp, ctypes.c_double]
 for _n in ("pmfem_demag", "pmfem_exchange", "pmfem_heff", "pmfem_heff_host"):
     getattr(_lib, _n).argtypes = [_vp, _vp, _vp, _vp]
@@ -79,7 +82,12 @@ for _n in SYMBOLS:
 
 _EXPORT_DTYPES = {"parent": np.int64, "lca": np.int64, "shift": np.int32, "ring1_rowptr": np.int64,
                   "ring1_col": np.int32, "z0_rowptr": np.int64, "z0_col": np.int32, "cbox_rowptr": np.int64,
-                  "cbox_col": np.int32, "stencil_s": np.int32, "perm": np.int64}
+                  "cbox_col": np.int32, "stencil_s": np.int32, "perm": np.int64, "dist_bounds": np.int64}
+for _k in "mqu":
+    _EXPORT_DTYPES["send_%s_ptr" % _k] = np.int64
+    _EXPORT_DTYPES["recv_%s_ptr" % _k] = np.int64
+    _EXPORT_DTYPES["send_%s_idx" % _k] = np.int32
+    _EXPORT_DTYPES["recv_%s_idx" % _k] = np.int32
 
 KERNELS = ["K1_local_in", "K2_anterp", "K3_fft_conv", "K4_interp_corr", "K5_grad_sum"]
 
@@ -99,7 +107,8 @@ class Context:
     """Owns a pmfem_ctx.  device=-1 builds a host-only context (setup artifacts, no fields)."""
 
     def __init__(self, xyz, tets, periodic, lattice, grid_n, Ms=637.0, Aex=1.4e-6, order=1,
-                 rer_scale=2.0, z0_ring=1, device=0, region=None, match_tol=0.0):
+                 rer_scale=2.0, z0_ring=1, device=0, region=None, match_tol=0.0, rank=0, world=1,
+                 nccl_id=None):
         xyz = np.ascontiguousarray(xyz, dtype=np.float64)
         tets = np.ascontiguousarray(tets, dtype=np.int32)
         Ms = np.ascontiguousarray(np.atleast_1d(Ms), dtype=np.float64)
@@ -115,7 +124,15 @@ class Context:
                          (ctypes.c_double * 3)(*[float(v) for v in lattice]), float(match_tol))
         g = _Grid((ctypes.c_int32 * 3)(*[int(v) for v in grid_n]), int(order), float(rer_scale), int(z0_ring))
         h = _vp()
-        st = _lib.pmfem_setup(ctypes.byref(h), ctypes.byref(m), ctypes.byref(p), ctypes.byref(g), int(device))
+        if world == 1:
+            st = _lib.pmfem_setup(ctypes.byref(h), ctypes.byref(m), ctypes.byref(p), ctypes.byref(g), int(device))
+        else:
+            idbuf = None
+            if nccl_id is not None:
+                idbuf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            st = _lib.pmfem_setup_dist(ctypes.byref(h), ctypes.byref(m), ctypes.byref(p), ctypes.byref(g),
+                                       int(device), idbuf, int(rank), int(world))
+        self.rank, self.world = rank, world
         if st != 0:
             raise PmfemError(st, _lib.pmfem_last_error(None).decode())
         self._h = h
@@ -123,6 +140,7 @@ class Context:
         self._keep = None
         info = self.query()
         self.n_parents = info["n_parents"]
+        self.n_parents_local = info["n_parents_local"]
         self.n_nodes = info["n_nodes"]
 
     def _check(self, st):
@@ -182,13 +200,13 @@ class Context:
         return out
 
     def get_order(self):
-        """internal row i -> original (user) node index of its parent."""
-        a = np.zeros(self.n_parents, dtype=np.int64)
+        """rank-local internal row i -> original (user) node index of its parent."""
+        a = np.zeros(self.n_parents_local, dtype=np.int64)
         self._check(_lib.pmfem_get_order(self._h, _ptr(a, ctypes.c_int64)))
         return a
 
     def internal_to_parent_rank(self):
-        """internal row i -> parent rank (parents numbered by increasing original index)."""
+        """rank-local internal row i -> parent rank (parents numbered by increasing original index)."""
         parents = self.export("parent")
         return np.searchsorted(parents, self.get_order())
 
@@ -208,6 +226,15 @@ class Context:
         a = (ctypes.c_float * 8)()
         self._check(_lib.pmfem_get_timing(self._h, a))
         return dict(zip(KERNELS, list(a)[:5]))
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it with torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    st = _lib.pmfem_nccl_unique_id(buf)
+    if st != 0:
+        raise PmfemError(st, _lib.pmfem_last_error(None).decode())
+    return bytes(buf.raw)
 
 
 def library_symbols():
