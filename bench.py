@@ -183,17 +183,24 @@ def main():
     aim = aim_params(a)
     cfg = make_config(a.config, coarsen=a.coarsen)
     mesh = cfg["mesh"]
+    nccl_id = None
+    if world > 1:
+        from paper_2409_13958_b200 import nccl_unique_id
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
     t0 = time.time()
     ctx = Context(mesh.xyz, mesh.tets, cfg["periodic"], cfg["lattice"], cfg["grid"], Ms=cfg["Ms"], Aex=cfg["Aex"],
-                  device=dev, **aim)
+                  device=dev, rank=rank, world=world, nccl_id=nccl_id, **aim)
     t_setup = time.time() - t0
     t0 = time.time()
     ctx.build_pgf()
     t_pgf = time.time() - t0
     info = ctx.query()
     Np = info["n_parents"]
+    Nloc = info["n_parents_local"]
     g = torch.Generator(device="cuda").manual_seed(1000 + rank)
-    m = torch.randn(Np, 3, device="cuda", generator=g)
+    m = torch.randn(Nloc, 3, device="cuda", generator=g)
     m = (m / m.norm(dim=1, keepdim=True)).contiguous()
     H = torch.empty_like(m)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MiB > L2 (126 MB)
@@ -234,7 +241,8 @@ def main():
         t = torch.tensor([tot_ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
-    value = world * a.steps / (tot_ms / 1e3)
+    # one distributed evaluation covers the whole mesh: evals/s of the job = steps / max time
+    value = a.steps / (tot_ms / 1e3)
 
     # end to end through the public API with host buffers (pinned), copies inside the timed region
     m_h = m.cpu().pin_memory()
@@ -255,7 +263,7 @@ def main():
         t = torch.tensor([e2e_tot], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_tot = float(t.item())
-    e2e_value = world * a.steps / (e2e_tot / 1e3)
+    e2e_value = a.steps / (e2e_tot / 1e3)
 
     peaks, peak_src = load_peaks()
     kb = info["kernel_bytes"]
@@ -270,21 +278,23 @@ def main():
                 "share_of_step": kernels[dom]["ms"] / float(np.mean(step_ms))}
     alg_total = sum(kb[:5])
     line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": tot_ms / a.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "%s: %s" % (a.config, cfg["desc"]), "n_nodes": info["n_nodes"],
                        "n_parents": Np, "grid": info["grid"], "fft": info["fft"], **aim,
                        "nnz_ring1": info["nnz_ring1"], "nnz_z0": info["nnz_z0"], "nnz_cbox": info["nnz_cbox"],
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": "single GPU" if world == 1 else
-                       "replicas (one full problem per GPU; slab-distributed FFT not implemented)"},
+                       "slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + all-reduce of the "
+                       "anterpolated grid, replicated FFT" % world, "n_parents_local": Nloc},
             "nodes_per_s": value * Np, "setup_s": t_setup, "build_pgf_s": t_pgf,
             "bytes_per_eval_algorithmic": alg_total,
             "eval_GBps_algorithmic": alg_total / (tot_ms / a.steps * 1e-3) / 1e9,
             "kernels": kernels, "roofline": roofline,
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(m_h.numel() * 4),
                     "d2h_bytes_per_step": int(H_h.numel() * 4)},
-            "gpu_launches": 9 * a.steps, "clocks": clocks}
+            "gpu_launches": info["launches_per_eval"] * a.steps, "clocks": clocks,
+            "comm_bytes_per_eval_rank": info["comm_bytes_per_eval"]}
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         cb = cpu_baseline(a.config, aim, a.cpu_seconds)
         v = cb["n_parents"] / cb["s_per_eval"] / Np

@@ -88,6 +88,9 @@ typedef struct {
   double  setup_seconds, pgf_seconds;             /* host wall time of setup / build_pgf      */
   double  kernel_bytes[8];                        /* algorithmic bytes per launch of K1..K5 (index
                                                      0 K1, 1 K2, 2 K3 (all FFT passes), 3 K4, 4 K5) */
+  int32_t launches_per_eval;                      /* library kernels launched by one pmfem_heff   */
+  int32_t fft_fused;                              /* 1: fused YZ FFT plan, 0: split plan          */
+  double  comm_bytes_per_eval;                    /* bytes this rank sends+receives per evaluation */
 } pmfem_info;
 
 /* Build a context: validate, orient, detect T-PBC pairs and fold them to LCAs,

@@ -569,6 +569,7 @@ void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id) {
     sbuf = std::max<int64_t>(sbuf, (int64_t)P.send_idx[k].size() * width[k]);
     rbuf = std::max<int64_t>(rbuf, (int64_t)P.recv_idx[k].size() * width[k]);
     D.comm_bytes_per_eval += 4.0 * width[k] * (double)(P.send_idx[k].size() + P.recv_idx[k].size());
+    D.launches_per_eval += (P.send_idx[k].empty() ? 0 : 1) + (P.recv_idx[k].empty() ? 0 : 1);   // pack/unpack
   }
   D.send_buf = dalloc<float>(sbuf);
   D.recv_buf = dalloc<float>(rbuf);

@@ -187,6 +187,9 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
   double tot = 0;
   for (int i = 0; i < 5; ++i) { out->kernel_bytes[i] = ctx->D.kernel_bytes[i]; tot += ctx->D.kernel_bytes[i]; }
   out->bytes_per_eval_algorithmic = tot;
+  out->launches_per_eval = ctx->D.launches_per_eval;
+  out->fft_fused = ctx->D.fused_tile > 0;
+  out->comm_bytes_per_eval = ctx->D.comm_bytes_per_eval;
   out->setup_seconds = S.setup_seconds;
   out->pgf_seconds = S.pgf_seconds;
   return PMFEM_OK;

@@ -56,7 +56,9 @@ class _Info(ctypes.Structure):
                 ("grid", ctypes.c_int32 * 3), ("fft", ctypes.c_int32 * 3),
                 ("nnz_ring1", ctypes.c_int64), ("nnz_z0", ctypes.c_int64), ("nnz_cbox", ctypes.c_int64),
                 ("bytes_per_eval_algorithmic", ctypes.c_double), ("setup_seconds", ctypes.c_double),
-                ("pgf_seconds", ctypes.c_double), ("kernel_bytes", ctypes.c_double * 8)]
+                ("pgf_seconds", ctypes.c_double), ("kernel_bytes", ctypes.c_double * 8),
+                ("launches_per_eval", ctypes.c_int32), ("fft_fused", ctypes.c_int32),
+                ("comm_bytes_per_eval", ctypes.c_double)]
 
 
 _vp = ctypes.c_void_p
