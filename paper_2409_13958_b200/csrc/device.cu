@@ -50,6 +50,7 @@ T* dupload(const std::vector<T>& v) {
   return p;
 }
 int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+float __int_as_float_host(int32_t c) { float f; std::memcpy(&f, &c, 4); return f; }
 
 // Rows [row0, row1) of the internal order are processed; per-row outputs H are stored at
 // n - hoff (hoff = row0 for the rank-local H of a distributed context, 0 otherwise).
@@ -74,49 +75,56 @@ __global__ void k_unpack(const float* __restrict__ buf, const int32_t* __restric
 }
 
 // ------------------------------------------------------------------ K1 local_in
-// One thread per row (SELL-32).  Reads m (gathered), the shared column list, Z0 (3 planes),
-// (L, D) on the ring-1 prefix and the row sums; writes q, u_loc and (heff) H_ex.
+// One thread per row (SELL-32).  Per shared entry one 16-byte load (Zx, Zy, Zz, col) and one
+// 16-byte gather of m (float4 copy); on the ring-1 prefix one more 16-byte load (L, Dx, Dy, Dz).
+__device__ __forceinline__ int colof(float4 v) { return __float_as_int(v.w); }
+
+__global__ void k_to_m4(RowRange rr, const float* __restrict__ m, float4* __restrict__ m4) {
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= rr.row1) return;
+  const int64_t h = n - rr.hoff;
+  m4[n] = make_float4(m[3 * h], m[3 * h + 1], m[3 * h + 2], 0.f);
+}
+
 __global__ void __launch_bounds__(256) k1_local_in(
-    RowRange rr, const float* __restrict__ m, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
-    const int32_t* __restrict__ s_col, const float* __restrict__ s_z, int64_t zt, const float4* __restrict__ s_LD,
-    const float4* __restrict__ rowsum, float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H,
-    int write_hex) {
+    RowRange rr, const float4* __restrict__ m4, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
+    const float4* __restrict__ s_zc, const float4* __restrict__ s_LD, const float4* __restrict__ rowsum,
+    float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H, int write_hex) {
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= rr.row1) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
   const int64_t o = sl_off[s], o1 = sl1_off[s];
   const int w = (int)((sl_off[s + 1] - o) >> 5), w1 = (int)((sl1_off[s + 1] - o1) >> 5);
-  const float mx = m[3 * n], my = m[3 * n + 1], mz = m[3 * n + 2];
+  const float4 mn = m4[n];
   float hx = 0.f, hy = 0.f, hz = 0.f, qq = 0.f, ul = 0.f;
   int64_t e = o + l, e1 = o1 + l;
 #pragma unroll 4
   for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
-    const int32_t c = __ldg(s_col + e);
+    const float4 zc = __ldg(s_zc + e);
     const float4 LD = __ldg(s_LD + e1);
-    const float zx = __ldg(s_z + e), zy = __ldg(s_z + zt + e), zz = __ldg(s_z + 2 * zt + e);
-    const float dx = m[3 * c] - mx, dy = m[3 * c + 1] - my, dz = m[3 * c + 2] - mz;
+    const float4 mc = m4[colof(zc)];
+    const float dx = mc.x - mn.x, dy = mc.y - mn.y, dz = mc.z - mn.z;
     hx = fmaf(LD.x, dx, hx); hy = fmaf(LD.x, dy, hy); hz = fmaf(LD.x, dz, hz);
     qq = fmaf(LD.y, dx, fmaf(LD.z, dy, fmaf(LD.w, dz, qq)));
-    ul = fmaf(zx, dx, fmaf(zy, dy, fmaf(zz, dz, ul)));
+    ul = fmaf(zc.x, dx, fmaf(zc.y, dy, fmaf(zc.z, dz, ul)));
   }
 #pragma unroll 4
   for (int j = w1; j < w; ++j, e += 32) {
-    const int32_t c = __ldg(s_col + e);
-    const float zx = __ldg(s_z + e), zy = __ldg(s_z + zt + e), zz = __ldg(s_z + 2 * zt + e);
-    const float dx = m[3 * c] - mx, dy = m[3 * c + 1] - my, dz = m[3 * c + 2] - mz;
-    ul = fmaf(zx, dx, fmaf(zy, dy, fmaf(zz, dz, ul)));
+    const float4 zc = __ldg(s_zc + e);
+    const float4 mc = m4[colof(zc)];
+    ul = fmaf(zc.x, mc.x - mn.x, fmaf(zc.y, mc.y - mn.y, fmaf(zc.z, mc.z - mn.z, ul)));
   }
   const float4 rd = rowsum[2 * n], rz = rowsum[2 * n + 1];
-  q[n] = qq + rd.x * mx + rd.y * my + rd.z * mz;
-  uloc[n] = ul + rz.x * mx + rz.y * my + rz.z * mz;
+  q[n] = qq + rd.x * mn.x + rd.y * mn.y + rd.z * mn.z;
+  uloc[n] = ul + rz.x * mn.x + rz.y * mn.y + rz.z * mn.z;
   if (write_hex) { H[3 * (n - rr.hoff)] = hx; H[3 * (n - rr.hoff) + 1] = hy; H[3 * (n - rr.hoff) + 2] = hz; }
 }
 
 // exchange only: H = L m
-__global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float* __restrict__ m,
+__global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float4* __restrict__ m4,
                                                   const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
-                                                  const int32_t* __restrict__ s_col, const float4* __restrict__ s_LD,
+                                                  const float4* __restrict__ s_zc, const float4* __restrict__ s_LD,
                                                   float* __restrict__ H) {
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= rr.row1) return;
@@ -124,14 +132,14 @@ __global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float* __re
   const int l = (int)(n & 31);
   const int64_t o = sl_off[s], o1 = sl1_off[s];
   const int w1 = (int)((sl1_off[s + 1] - o1) >> 5);
-  const float mx = m[3 * n], my = m[3 * n + 1], mz = m[3 * n + 2];
+  const float4 mn = m4[n];
   float hx = 0.f, hy = 0.f, hz = 0.f;
   int64_t e = o + l, e1 = o1 + l;
 #pragma unroll 4
   for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
-    const int32_t c = __ldg(s_col + e);
+    const float4 mc = m4[colof(__ldg(s_zc + e))];
     const float L = __ldg(&s_LD[e1].x);
-    hx = fmaf(L, m[3 * c] - mx, hx); hy = fmaf(L, m[3 * c + 1] - my, hy); hz = fmaf(L, m[3 * c + 2] - mz, hz);
+    hx = fmaf(L, mc.x - mn.x, hx); hy = fmaf(L, mc.y - mn.y, hy); hz = fmaf(L, mc.z - mn.z, hz);
   }
   H[3 * (n - rr.hoff)] = hx; H[3 * (n - rr.hoff) + 1] = hy; H[3 * (n - rr.hoff) + 2] = hz;
 }
@@ -154,28 +162,51 @@ struct GridDims { int n0, n1, n2; int per0, per1, per2; };
 __device__ __forceinline__ int wrapi(int i, int n, int per) { return per ? (i >= n ? i - n : i) : i; }
 
 // ------------------------------------------------------------------ K2 anterpolation
+// Gather form of the anterpolation (deterministic, no atomics, no memset): one thread per grid
+// point g sums w_n(g) q_n over the nodes whose stencil covers g.  Nodes are sorted by anchor
+// box (internal order), so the candidates are the node ranges of the (P+1)^3 anchor boxes
+// g - delta, read through box_ptr.  Rows outside [lo, hi) belong to other ranks (their
+// contributions arrive through the all-reduce of Q).
 template <int P>
-__global__ void __launch_bounds__(256) k2_anterp(RowRange rr, const float* __restrict__ q, const int4* __restrict__ st_s,
-                                                 const float4* __restrict__ st_t, GridDims g, float* __restrict__ Q) {
-  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= rr.row1) return;
-  const int4 s = st_s[n];
-  const float4 t = st_t[n];
-  const float qn = q[n];
-  float wx[P + 1], wy[P + 1], wz[P + 1];
-  lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+__device__ __forceinline__ float lagr1(float t, int d) {
+  float v = 1.f;
 #pragma unroll
-  for (int k = 0; k <= P; ++k) {
-    const int iz = wrapi(s.z + k, g.n2, g.per2);
+  for (int i = 0; i <= P; ++i)
+    if (i != d) v *= (t - (float)i) / (float)(d - i);
+  return v;
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k2_gather(GridDims g, const int32_t* __restrict__ box_ptr,
+                                                 const float4* __restrict__ st_t, const float* __restrict__ q,
+                                                 int64_t lo, int64_t hi, float* __restrict__ Q) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t G = (int64_t)g.n0 * g.n1 * g.n2;
+  if (gid >= G) return;
+  const int gx = (int)(gid % g.n0), gy = (int)((gid / g.n0) % g.n1), gz = (int)(gid / ((int64_t)g.n0 * g.n1));
+  float acc = 0.f;
 #pragma unroll
-    for (int j = 0; j <= P; ++j) {
-      const int iy = wrapi(s.y + j, g.n1, g.per1);
-      const float wzy = qn * wz[k] * wy[j];
-      float* row = Q + ((int64_t)iz * g.n1 + iy) * g.n0;
+  for (int dz = 0; dz <= P; ++dz) {
+    int sz = gz - dz;
+    if (g.per2) { if (sz < 0) sz += g.n2; } else if (sz < 0 || sz > g.n2 - 1 - P) continue;
 #pragma unroll
-      for (int i = 0; i <= P; ++i) atomicAdd(row + wrapi(s.x + i, g.n0, g.per0), wzy * wx[i]);
+    for (int dy = 0; dy <= P; ++dy) {
+      int sy = gy - dy;
+      if (g.per1) { if (sy < 0) sy += g.n1; } else if (sy < 0 || sy > g.n1 - 1 - P) continue;
+#pragma unroll
+      for (int dx = 0; dx <= P; ++dx) {
+        int sx = gx - dx;
+        if (g.per0) { if (sx < 0) sx += g.n0; } else if (sx < 0 || sx > g.n0 - 1 - P) continue;
+        const int64_t b = ((int64_t)sz * g.n1 + sy) * g.n0 + sx;
+        const int64_t i0 = max((int64_t)__ldg(box_ptr + b), lo), i1 = min((int64_t)__ldg(box_ptr + b + 1), hi);
+        for (int64_t i = i0; i < i1; ++i) {
+          const float4 t = __ldg(st_t + i);
+          acc = fmaf(lagr1<P>(t.x, dx) * lagr1<P>(t.y, dy) * lagr1<P>(t.z, dz), __ldg(q + i), acc);
+        }
+      }
     }
   }
+  Q[gid] = acc;
 }
 
 // ------------------------------------------------------------------ K4 interpolation + precorrection
@@ -220,26 +251,22 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
-__global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __restrict__ u, const int64_t* __restrict__ sl_off,
-                                                   const int64_t* __restrict__ sl1_off, const int32_t* __restrict__ s_col,
-                                                   const float* __restrict__ s_G, int64_t gt, float* __restrict__ H,
-                                                   int accumulate) {
+__global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __restrict__ u, const int64_t* __restrict__ sl1_off,
+                                                   const float4* __restrict__ s_Gc, float* __restrict__ H, int accumulate) {
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= rr.row1) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
-  const int64_t o = sl_off[s], o1 = sl1_off[s];
+  const int64_t o1 = sl1_off[s];
   const int w1 = (int)((sl1_off[s + 1] - o1) >> 5);
   const float un = u[n];
   float gx = 0.f, gy = 0.f, gz = 0.f;
-  int64_t e = o + l, e1 = o1 + l;
+  int64_t e1 = o1 + l;
 #pragma unroll 4
-  for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
-    const int32_t c = __ldg(s_col + e);
-    const float du = u[c] - un;
-    gx = fmaf(__ldg(s_G + e1), du, gx);
-    gy = fmaf(__ldg(s_G + gt + e1), du, gy);
-    gz = fmaf(__ldg(s_G + 2 * gt + e1), du, gz);
+  for (int j = 0; j < w1; ++j, e1 += 32) {
+    const float4 gc = __ldg(s_Gc + e1);
+    const float du = u[colof(gc)] - un;
+    gx = fmaf(gc.x, du, gx); gy = fmaf(gc.y, du, gy); gz = fmaf(gc.z, du, gz);
   }
   if (accumulate) { H[3 * (n - rr.hoff)] -= gx; H[3 * (n - rr.hoff) + 1] -= gy; H[3 * (n - rr.hoff) + 2] -= gz; }
   else { H[3 * (n - rr.hoff)] = -gx; H[3 * (n - rr.hoff) + 1] = -gy; H[3 * (n - rr.hoff) + 2] = -gz; }
@@ -389,34 +416,34 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   const int64_t zt = sl_off[ns], gt = sl1_off[ns];
   D.zt = zt;
   D.gt = gt;
-  std::vector<int32_t> s_col(zt);
-  std::vector<float> s_z(3 * zt, 0.f), s_G(3 * gt, 0.f);
-  std::vector<float4> s_LD(gt, make_float4(0, 0, 0, 0));
+  std::vector<float4> s_zc(zt), s_Gc(gt), s_LD(gt, make_float4(0, 0, 0, 0));
+  auto pack = [](float x, float y, float z, int32_t c) { return make_float4(x, y, z, __int_as_float_host(c)); };
 #pragma omp parallel for
   for (int64_t s = 0; s < ns; ++s) {
     const int w = (int)((sl_off[s + 1] - sl_off[s]) / 32), w1 = (int)((sl1_off[s + 1] - sl1_off[s]) / 32);
     for (int l = 0; l < 32; ++l) {
       const int64_t i = 32 * s + l;
+      const int32_t self = (int32_t)std::min<int64_t>(i, Np - 1);   // padding: the row itself, weight 0
       for (int j = 0; j < w; ++j) {
         const int64_t e = sl_off[s] + 32 * j + l;
-        if (i < Np && j < lenz[i]) {
-          s_col[e] = rcols[i][j];
-          for (int x = 0; x < 3; ++x) s_z[x * zt + e] = rz[i][3 * j + x];
-        } else {
-          s_col[e] = (int32_t)std::min<int64_t>(i, Np - 1);   // padding: the row itself, weight 0
-        }
+        if (i < Np && j < lenz[i]) s_zc[e] = pack(rz[i][3 * j], rz[i][3 * j + 1], rz[i][3 * j + 2], rcols[i][j]);
+        else s_zc[e] = pack(0.f, 0.f, 0.f, self);
       }
       for (int j = 0; j < w1; ++j) {
         const int64_t e1 = sl1_off[s] + 32 * j + l;
         if (i < Np && j < len1[i]) {
           s_LD[e1] = make_float4(rld[i][4 * j], rld[i][4 * j + 1], rld[i][4 * j + 2], rld[i][4 * j + 3]);
-          for (int x = 0; x < 3; ++x) s_G[x * gt + e1] = rg[i][3 * j + x];
+          s_Gc[e1] = pack(rg[i][3 * j], rg[i][3 * j + 1], rg[i][3 * j + 2], rcols[i][j]);
+        } else {
+          s_Gc[e1] = pack(0.f, 0.f, 0.f, self);
         }
       }
     }
   }
-  D.sl_off = dupload(sl_off); D.sl1_off = dupload(sl1_off); D.s_col = dupload(s_col);
-  D.s_z = dupload(s_z); D.s_LD = dupload(s_LD); D.s_G = dupload(s_G);
+  D.sl_off = dupload(sl_off); D.sl1_off = dupload(sl1_off);
+  D.s_zc = dupload(s_zc); D.s_LD = dupload(s_LD); D.s_Gc = dupload(s_Gc);
+  D.m4 = dalloc<float4>(Np);
+  CK(cudaMemset(D.m4, 0, sizeof(float4) * (size_t)Np));
 
   // ---- C_box: CSR with rows padded to a multiple of 4
   {
@@ -456,6 +483,22 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     stt[i] = make_float4((float)S.st_t[3 * r], (float)S.st_t[3 * r + 1], (float)S.st_t[3 * r + 2], 0.f);
   }
   D.rowsum = dupload(rsum); D.st_s = dupload(sts); D.st_t = dupload(stt);
+  {
+    // anchor-box row pointers (internal rows are sorted by the anchor key, x fastest)
+    const int64_t Gb = (int64_t)D.n[0] * D.n[1] * D.n[2];
+    std::vector<int32_t> bp(Gb + 1, 0);
+    for (int64_t i = 0; i < Np; ++i) {
+      const int64_t key = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
+      bp[key + 1]++;
+    }
+    for (int64_t b = 0; b < Gb; ++b) bp[b + 1] += bp[b];
+    for (int64_t i = 1; i < Np; ++i) {
+      const int64_t k0 = ((int64_t)sts[i - 1].z * D.n[1] + sts[i - 1].y) * D.n[0] + sts[i - 1].x;
+      const int64_t k1 = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
+      if (k1 < k0) throw Error(PMFEM_E_STATE, "internal rows are not sorted by anchor box");
+    }
+    D.box_ptr = dupload(bp);
+  }
   for (int a = 0; a < 3; ++a) {
     std::vector<float2> t32; std::vector<double2> t64;
     twiddles<float>(D.P[a], t32); twiddles<double>(D.P[a], t64);
@@ -476,11 +519,15 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       D.fused_tile = tile;
     }
   }
-  D.launches_per_eval = 3 + (D.fused_tile ? 3 : 5) + 1;   // K1, K2, FFT passes, K4, K5 (memset excluded)
-  // compulsory bytes per launch: every array read or written once (gathered m, q, u once)
+  D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5
+  // compulsory bytes per launch: every array read or written once (gathered m, q, u once),
+  // actual entries only (SELL padding is overhead, not algorithmic traffic)
   const double G = (double)D.n[0] * D.n[1] * D.n[2];
-  D.kernel_bytes[0] = Np * (12.0 + 32 + 16 + 4 + 4 + 12) + (double)zt * (4 + 12) + (double)gt * 16;
-  D.kernel_bytes[1] = Np * (4.0 + 16 + 16) + G * 4.0 * 2;
+  double nsh = 0, n1e = 0;
+  for (int64_t i = 0; i < Np; ++i) { nsh += lenz[i]; n1e += len1[i]; }
+  // K1 window = m -> float4 copy (12 + 16) + K1 (m4 16, row sums 32, slice offsets ~0, q, u_loc, H_ex)
+  D.kernel_bytes[0] = Np * (12.0 + 16 + 16 + 32 + 4 + 4 + 12) + nsh * 16 + n1e * 16;
+  D.kernel_bytes[1] = Np * (4.0 + 16) + G * 4.0 * 2;          // q + local t, box_ptr, Q write
   {
     const double Hc = (double)D.H0;
     const double spec_b = Hc * D.P[1] * D.P[2] * 4;
@@ -497,7 +544,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   int64_t cnnz = 0;
   for (int64_t i = 0; i < Np; ++i) cnnz += S.cbox.rowptr[S.perm[i] + 1] - S.cbox.rowptr[S.perm[i]];
   D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 8 + G * 4.0;
-  D.kernel_bytes[4] = Np * (4.0 + 8 + 12 + 12) + (double)gt * (4 + 12);
+  D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
 
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
@@ -532,10 +579,10 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
 void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
-  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_col, D.s_z, D.s_LD, D.s_G, D.rowsum, D.c_ptr, D.c_col, D.c_val,
-                  D.st_s, D.st_t, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
+  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_col, D.c_val,
+                  D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
-                  D.mfull, D.send_buf, D.recv_buf, D.send_idx[0], D.send_idx[1], D.send_idx[2],
+                  D.send_buf, D.recv_buf, D.send_idx[0], D.send_idx[1], D.send_idx[2],
                   D.recv_idx[0], D.recv_idx[1], D.recv_idx[2]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -559,7 +606,7 @@ void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id) {
   NCK(ncclCommInitRank(&comm, P.world, id, P.rank));
   D.comm = comm;
   int64_t sbuf = 0, rbuf = 0;
-  const int width[3] = {3, 1, 1};
+  const int width[3] = {4, 1, 1};   // m travels as the float4 copy
   D.comm_bytes_per_eval = 4.0 * (double)D.n[0] * D.n[1] * D.n[2] * 2.0 * (P.world - 1) / P.world;  // ring all-reduce
   for (int k = 0; k < 3; ++k) {
     D.send_ptr[k] = P.send_ptr[k];
@@ -573,8 +620,6 @@ void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id) {
   }
   D.send_buf = dalloc<float>(sbuf);
   D.recv_buf = dalloc<float>(rbuf);
-  D.mfull = dalloc<float>(3 * (size_t)D.Np);
-  CK(cudaMemset(D.mfull, 0, 12 * (size_t)D.Np));
 }
 
 namespace {
@@ -610,32 +655,28 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   if (nrows <= 0) return;
   const unsigned thr_blocks = (unsigned)((nrows + 255) / 256);   // thread per row
   const unsigned warp_blocks = (unsigned)((nrows + 7) / 8);      // warp per row, 8 warps per block
-  const int64_t zt_h = D.zt, gt_h = D.gt;                        // SoA plane strides
   auto mark = [&](int i) { if (D.timing) CK(cudaEventRecord(D.ev[i], st)); };
   mark(0);
-  const float* mg = m - 3 * D.lo;                                 // global-row view of m
-  if (D.world > 1) {
-    CK(cudaMemcpyAsync(D.mfull + 3 * D.lo, m, 12 * (size_t)nrows, cudaMemcpyDeviceToDevice, st));
-    halo(D, 0, D.mfull, 3, st);
-    mg = D.mfull;
-  }
+  k_to_m4<<<thr_blocks, 256, 0, st>>>(rr, m, D.m4);
+  CK(cudaGetLastError());
+  halo(D, 0, reinterpret_cast<float*>(D.m4), 4, st);
   if (mode == EVAL_EXCHANGE) {
-    k_exchange<<<thr_blocks, 256, 0, st>>>(rr, mg, D.sl_off, D.sl1_off, D.s_col, D.s_LD, H);
+    k_exchange<<<thr_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, H);
     CK(cudaGetLastError());
     return;
   }
   if (!D.pgf_ready) throw Error(PMFEM_E_STATE, "pmfem_build_pgf has not been called");
   GridDims g{D.n[0], D.n[1], D.n[2], D.periodic[0], D.periodic[1], D.periodic[2]};
-  k1_local_in<<<thr_blocks, 256, 0, st>>>(rr, mg, D.sl_off, D.sl1_off, D.s_col, D.s_z, zt_h, D.s_LD, D.rowsum, D.q,
-                                          D.uloc, H, mode == EVAL_HEFF ? 1 : 0);
+  k1_local_in<<<thr_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.rowsum, D.q, D.uloc, H,
+                                          mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(1);
   const size_t G = (size_t)D.n[0] * D.n[1] * D.n[2];
-  CK(cudaMemsetAsync(D.Q, 0, sizeof(float) * G, st));
+  const unsigned grid_blocks = (unsigned)((G + 255) / 256);
   switch (D.order) {
-    case 1: k2_anterp<1><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
-    case 2: k2_anterp<2><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
-    default: k2_anterp<3><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
+    case 1: k2_gather<1><<<grid_blocks, 256, 0, st>>>(g, D.box_ptr, D.st_t, D.q, D.lo, D.hi, D.Q); break;
+    case 2: k2_gather<2><<<grid_blocks, 256, 0, st>>>(g, D.box_ptr, D.st_t, D.q, D.lo, D.hi, D.Q); break;
+    default: k2_gather<3><<<grid_blocks, 256, 0, st>>>(g, D.box_ptr, D.st_t, D.q, D.lo, D.hi, D.Q); break;
   }
   CK(cudaGetLastError());
   if (D.world > 1) NCK(ncclAllReduce(D.Q, D.Q, G, ncclFloat, ncclSum, (ncclComm_t)D.comm, st));
@@ -665,7 +706,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   CK(cudaGetLastError());
   halo(D, 2, D.u, 1, st);
   mark(4);
-  k5_grad_sum<<<thr_blocks, 256, 0, st>>>(rr, D.u, D.sl_off, D.sl1_off, D.s_col, D.s_G, gt_h, H, mode == EVAL_HEFF ? 1 : 0);
+  k5_grad_sum<<<thr_blocks, 256, 0, st>>>(rr, D.u, D.sl1_off, D.s_Gc, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(5);
 }

@@ -20,16 +20,17 @@ struct DeviceState {
   int64_t zt = 0, gt = 0;      // total SELL entries of the shared / ring-1 arrays (SoA plane strides)
   int64_t* sl_off = nullptr;   // [nslices+1] entry offsets of the shared col / Z arrays
   int64_t* sl1_off = nullptr;  // [nslices+1] entry offsets of the ring-1 value arrays
-  int32_t* s_col = nullptr;    // shared columns (padding: the row itself)
-  float* s_z = nullptr;        // Z0 values, 3 planes (x, y, z) of length sl_off[nslices]
+  float4* s_zc = nullptr;      // (Zx, Zy, Zz, column bits) per shared entry (padding: the row itself, 0)
   float4* s_LD = nullptr;      // (L, Dx, Dy, Dz) for the first sl1 width entries
-  float* s_G = nullptr;        // G values, 3 planes of length sl1_off[nslices]
+  float4* s_Gc = nullptr;      // (Gx, Gy, Gz, column bits) for the first sl1 width entries
+  float4* m4 = nullptr;        // [N'] internal float4 copy of m (one 16-byte gather per entry)
   float4* rowsum = nullptr;    // [N'][2] (sum_m D_nm, 0), (sum_m Z_nm, 0)
   // C_box, CSR with rows padded to a multiple of 4 entries (col = row, val = 0)
   int64_t* c_ptr = nullptr;   int32_t* c_col = nullptr;
   float* c_val = nullptr;
   // stencils
   int4* st_s = nullptr;       // wrapped (periodic) / clamped anchors
+  int32_t* box_ptr = nullptr; // [G+1] first internal row of each anchor box (rows are box-sorted)
   float4* st_t = nullptr;     // local coordinates t - s
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32
   float* spec = nullptr;
@@ -59,7 +60,6 @@ struct DeviceState {
   int rank = 0, world = 1;
   int64_t lo = 0, hi = 0;
   void* comm = nullptr;                         // ncclComm_t
-  float* mfull = nullptr;                       // [N'][3] full-length m (world > 1)
   std::vector<int64_t> send_ptr[3], recv_ptr[3];
   int32_t* send_idx[3] = {nullptr, nullptr, nullptr};
   int32_t* recv_idx[3] = {nullptr, nullptr, nullptr};

@@ -59,7 +59,9 @@ __device__ void smem_fft(C* buf, int P, int logP, int nl, Base base, int es, con
 template <class C, class Base>
 __device__ void smem_bitrev(C* buf, int P, int logP, int nl, Base base, int es) {
   for (int idx = threadIdx.x; idx < nl * P; idx += blockDim.x) {
-    const int l = idx % nl, e = idx / nl;
+    // es == 1: element fastest (consecutive banks); else line fastest (lines are contiguous)
+    const int l = (es == 1) ? idx / P : idx % nl;
+    const int e = (es == 1) ? idx - l * P : idx / nl;
     const int r = bitrev(e, logP);
     if (r > e) {
       C* p = buf + base(l);
@@ -225,7 +227,9 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   __syncthreads();
   // forward y on the n2 data planes: line (i2, c) base = bitrev(i2)*plane + c, stride tile
   const PlaneBase ybase{tile, plane, logP2};
-  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, true);
+  // line-fast only when lines are adjacent in smem (tile > 1); with tile == 1 the y lines are
+  // contiguous rows and butterfly-fast ordering avoids plane-stride bank conflicts
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, tile > 1);
   // forward z on every (k1, c): base = k1*tile + c, stride plane
   const TileBase zbase{};
   smem_fft<C>(buf, P2, logP2, plane, zbase, plane, tw2, 1, false, true);
@@ -244,7 +248,7 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   // inverse y on planes i2 < n2 (natural z order now)
   const PlaneBase ybase2{tile, plane, 0};
   smem_bitrev<C>(buf, P1, logP1, n2 * tile, ybase2, tile);
-  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, true);
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, tile > 1);
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
     const int c = idx % tile, r = idx / tile, i1 = r % n1, i2 = r / n1;
     if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * plane + i1 * tile + c];

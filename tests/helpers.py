@@ -12,7 +12,7 @@ SMALL = {
     "C2p2": dict(cfg=("C2", 8), grid=(32, 32, 4), order=2, s=2.0, ring=1),
     "C3p1": dict(cfg=("C3", 12), grid=(64, 8, 8), order=1, s=2.0, ring=0),
     "C4p3": dict(cfg=("C4", 40), grid=(16, 16, 16), order=3, s=1.5, ring=0),
-    "C5p2": dict(cfg=("C5", 16), grid=(128, 8, 4), order=2, s=2.0, ring=1),
+    "C5p2": dict(cfg=("C5", 16), grid=(128, 8, 4), order=2, s=2.0, ring=0),
 }
 
 
