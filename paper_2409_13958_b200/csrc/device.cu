@@ -193,15 +193,31 @@ __global__ void __launch_bounds__(256) k2_gather(GridDims g, const int32_t* __re
     for (int dy = 0; dy <= P; ++dy) {
       int sy = gy - dy;
       if (g.per1) { if (sy < 0) sy += g.n1; } else if (sy < 0 || sy > g.n1 - 1 - P) continue;
-#pragma unroll
-      for (int dx = 0; dx <= P; ++dx) {
-        int sx = gx - dx;
-        if (g.per0) { if (sx < 0) sx += g.n0; } else if (sx < 0 || sx > g.n0 - 1 - P) continue;
-        const int64_t b = ((int64_t)sz * g.n1 + sy) * g.n0 + sx;
-        const int64_t i0 = max((int64_t)__ldg(box_ptr + b), lo), i1 = min((int64_t)__ldg(box_ptr + b + 1), hi);
+      // the anchor boxes gx-P..gx of one (sz, sy) line are consecutive in the box-sorted row
+      // order (x fastest): one contiguous node range (two when a periodic x wraps)
+      const int64_t line = ((int64_t)sz * g.n1 + sy) * g.n0;
+      int xr[2][2], nr = 0;
+      if (g.per0) {
+        if (gx - P >= 0) { xr[0][0] = gx - P; xr[0][1] = gx; nr = 1; }
+        else { xr[0][0] = 0; xr[0][1] = gx; xr[1][0] = g.n0 + gx - P; xr[1][1] = g.n0 - 1; nr = 2; }
+      } else {
+        const int a = max(gx - P, 0), b = min(gx, g.n0 - 1 - P);
+        if (a <= b) { xr[0][0] = a; xr[0][1] = b; nr = 1; }
+      }
+      const float wyz = 1.f;
+      for (int r = 0; r < nr; ++r) {
+        const int64_t i0 = max((int64_t)__ldg(box_ptr + line + xr[r][0]), lo);
+        const int64_t i1 = min((int64_t)__ldg(box_ptr + line + xr[r][1] + 1), hi);
         for (int64_t i = i0; i < i1; ++i) {
           const float4 t = __ldg(st_t + i);
-          acc = fmaf(lagr1<P>(t.x, dx) * lagr1<P>(t.y, dy) * lagr1<P>(t.z, dz), __ldg(q + i), acc);
+          int dx = gx - __float_as_int(t.w);        // wrapped anchor x is stored in t.w
+          if (dx < 0) dx += g.n0;
+          float wx[P + 1];
+          lagr<P>(t.x, wx);
+          float w = wx[0];
+#pragma unroll
+          for (int k = 1; k <= P; ++k) w = (dx == k) ? wx[k] : w;
+          acc = fmaf(w * wyz * lagr1<P>(t.y, dy) * lagr1<P>(t.z, dz), __ldg(q + i), acc);
         }
       }
     }
@@ -273,20 +289,29 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
 }
 
 // ------------------------------------------------------------------ PGF table (fp64)
+// One thread per point of the octant j_a in [0, P_a/2]; the value is written to every mirror
+// position j_a and P_a - j_a (K is even on each axis: lattice reflection symmetry + periodicity
+// on periodic axes, K(2N - j) = G(-(2N - j) Delta) on padded axes), so K is exactly symmetric
+// and its spectrum exactly real.
 __global__ void k_pgf_table(PgfDev pd, int P0, int P1, int P2, int n0, int n1, int n2, int per0, int per1, int per2,
                             double d0, double d1, double d2, double* __restrict__ K) {
+  const int Q0 = P0 / 2 + 1, Q1 = P1 / 2 + 1, Q2 = P2 / 2 + 1;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t tot = (int64_t)P0 * P1 * P2;
-  if (idx >= tot) return;
-  const int j0 = (int)(idx % P0), j1 = (int)((idx / P0) % P1), j2 = (int)(idx / ((int64_t)P0 * P1));
-  // K6: periodic j -> j Delta ; non-periodic j < n -> j Delta, j > n -> (j - 2n) Delta, j = n -> 0
-  if ((!per0 && j0 == n0) || (!per1 && j1 == n1) || (!per2 && j2 == n2)) { K[idx] = 0.0; return; }
-  double r[3];
-  r[0] = (per0 ? j0 : (j0 < n0 ? j0 : j0 - P0)) * d0;
-  r[1] = (per1 ? j1 : (j1 < n1 ? j1 : j1 - P1)) * d1;
-  r[2] = (per2 ? j2 : (j2 < n2 ? j2 : j2 - P2)) * d2;
-  const bool self = (j0 == 0 && j1 == 0 && j2 == 0);
-  K[idx] = pgf_eval(pd, r, self);
+  if (idx >= (int64_t)Q0 * Q1 * Q2) return;
+  const int j0 = (int)(idx % Q0), j1 = (int)((idx / Q0) % Q1), j2 = (int)(idx / ((int64_t)Q0 * Q1));
+  double v;
+  // K6: j -> j Delta (j <= P/2 here); on a padded axis j = n -> value 0 (never used)
+  if ((!per0 && j0 == n0) || (!per1 && j1 == n1) || (!per2 && j2 == n2)) {
+    v = 0.0;
+  } else {
+    const double r[3] = {j0 * d0, j1 * d1, j2 * d2};
+    v = pgf_eval(pd, r, j0 == 0 && j1 == 0 && j2 == 0);
+  }
+  const int a0[2] = {j0, P0 - j0}, a1[2] = {j1, P1 - j1}, a2[2] = {j2, P2 - j2};
+  for (int z = 0; z < ((j2 > 0 && P2 - j2 != j2) ? 2 : 1); ++z)
+    for (int y = 0; y < ((j1 > 0 && P1 - j1 != j1) ? 2 : 1); ++y)
+      for (int x = 0; x < ((j0 > 0 && P0 - j0 != j0) ? 2 : 1); ++x)
+        K[((int64_t)a2[z] * P1 + a1[y]) * P0 + a0[x]] = v;
 }
 
 __global__ void k_spec_finish(const double2* __restrict__ C, float* __restrict__ spec, int64_t tot, double scale) {
@@ -445,8 +470,10 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.m4 = dalloc<float4>(Np);
   CK(cudaMemset(D.m4, 0, sizeof(float4) * (size_t)Np));
 
-  // ---- C_box: CSR with rows padded to a multiple of 4
-  {
+  // ---- C_box: CSR with rows padded to a multiple of 4 (built on the GPU when cbox_device)
+  if (S.cbox_device) {
+    device_build_cbox(D, S);
+  } else {
     std::vector<int64_t> ptr(Np + 1, 0);
     for (int64_t i = 0; i < Np; ++i) {
       int64_t r = S.perm[i];
@@ -466,6 +493,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       for (; o < ptr[i + 1]; ++o) col[o] = (int32_t)i;
     }
     D.c_ptr = dupload(ptr); D.c_col = dupload(col); D.c_val = dupload(val);
+    D.cbox_nnz = S.cbox.nnz();
   }
   std::vector<float4> rsum(2 * Np), stt(Np);
   std::vector<int4> sts(Np);
@@ -480,7 +508,9 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       s[a] = v;
     }
     sts[i] = make_int4(s[0], s[1], s[2], 0);
-    stt[i] = make_float4((float)S.st_t[3 * r], (float)S.st_t[3 * r + 1], (float)S.st_t[3 * r + 2], 0.f);
+    // .w carries the wrapped anchor x (bit pattern) for the gather anterpolation
+    stt[i] = make_float4((float)S.st_t[3 * r], (float)S.st_t[3 * r + 1], (float)S.st_t[3 * r + 2],
+                         __int_as_float_host(s[0]));
   }
   D.rowsum = dupload(rsum); D.st_s = dupload(sts); D.st_t = dupload(stt);
   {
@@ -541,8 +571,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
                           ((double)D.n[1] * D.n[2] * Hc * 8 + G * 4);
     }
   }
-  int64_t cnnz = 0;
-  for (int64_t i = 0; i < Np; ++i) cnnz += S.cbox.rowptr[S.perm[i] + 1] - S.cbox.rowptr[S.perm[i]];
+  const int64_t cnnz = D.cbox_nnz;
   D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 8 + G * 4.0;
   D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
@@ -558,7 +587,8 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
   const int P0 = D.P[0], P1 = D.P[1], P2 = D.P[2];
   const int64_t tot = (int64_t)P0 * P1 * P2;
   double* K = dalloc<double>(tot);
-  k_pgf_table<<<(unsigned)((tot + 127) / 128), 128>>>(pd, P0, P1, P2, D.n[0], D.n[1], D.n[2], D.periodic[0],
+  const int64_t oct = (int64_t)(P0 / 2 + 1) * (P1 / 2 + 1) * (P2 / 2 + 1);
+  k_pgf_table<<<(unsigned)((oct + 63) / 64), 64>>>(pd, P0, P1, P2, D.n[0], D.n[1], D.n[2], D.periodic[0],
                                                       D.periodic[1], D.periodic[2], S.delta[0], S.delta[1], S.delta[2], K);
   CK(cudaGetLastError());
   // fp64 forward transform of the full padded table (no pruning)

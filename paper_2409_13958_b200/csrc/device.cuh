@@ -28,6 +28,7 @@ struct DeviceState {
   // C_box, CSR with rows padded to a multiple of 4 entries (col = row, val = 0)
   int64_t* c_ptr = nullptr;   int32_t* c_col = nullptr;
   float* c_val = nullptr;
+  int64_t cbox_nnz = 0;       // unpadded entries
   // stencils
   int4* st_s = nullptr;       // wrapped (periodic) / clamped anchors
   int32_t* box_ptr = nullptr; // [G+1] first internal row of each anchor box (rows are box-sorted)
@@ -69,6 +70,7 @@ struct DeviceState {
 };
 
 void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id);
+int64_t device_build_cbox(DeviceState& D, const HostSetup& S);
 
 void device_upload(DeviceState& D, const HostSetup& S);
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& P);

@@ -73,7 +73,9 @@ static pmfem_status setup_impl(pmfem_ctx* out, const pmfem_mesh* mesh, const pmf
     S.z0_ring = grid ? grid->z0_ring : 1;
     pmfem::require(grid != nullptr, PMFEM_E_INVALID_ARG, "NULL grid");
     pmfem::require(grid->z0_ring == 0 || grid->z0_ring == 1, PMFEM_E_INVALID_ARG, "z0_ring must be 0 or 1");
+    S.z0_device = cuda_device;            // device contexts integrate Z0 on the GPU
     pmfem::setup_z0(S);
+    S.cbox_device = cuda_device >= 0;     // device contexts build C_box on the GPU
     pmfem::setup_aim(S, grid);
     pmfem::setup_order(S);
     pmfem::setup_dist(S, rank, world);
@@ -183,7 +185,7 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
   for (int a = 0; a < 3; ++a) { out->grid[a] = S.grid_n[a]; out->fft[a] = S.fft_n[a]; }
   out->nnz_ring1 = S.ring1.nnz();
   out->nnz_z0 = S.z0.nnz();
-  out->nnz_cbox = S.cbox.nnz();
+  out->nnz_cbox = S.cbox_device ? ctx->D.cbox_nnz : S.cbox.nnz();
   double tot = 0;
   for (int i = 0; i < 5; ++i) { out->kernel_bytes[i] = ctx->D.kernel_bytes[i]; tot += ctx->D.kernel_bytes[i]; }
   out->bytes_per_eval_algorithmic = tot;
@@ -233,6 +235,21 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     else if (n == "grid_origin") put(S.origin, 3, 8);
     else if (n == "perm") put(S.perm.data(), S.Np, 8);
     else if (n == "dist_bounds") put(S.dist.bounds.data(), (int64_t)S.dist.bounds.size(), 8);
+    else if (n.rfind("cbox_device_", 0) == 0) {
+      // the device-built C_box (internal order, rows padded to 4), copied back for tests
+      pmfem::require(!ctx->host_only && S.cbox_device, PMFEM_E_STATE, "C_box was not built on the device");
+      const pmfem::DeviceState& D = ctx->D;
+      std::vector<int64_t> ptr(S.Np + 1);
+      cudaMemcpy(ptr.data(), D.c_ptr, sizeof(int64_t) * (S.Np + 1), cudaMemcpyDeviceToHost);
+      const std::string tail = n.substr(12);
+      if (tail == "rowptr") put(ptr.data(), S.Np + 1, 8);
+      else if (tail == "col" || tail == "val") {
+        *count = ptr[S.Np];
+        if (dst && ptr[S.Np])
+          cudaMemcpy(dst, tail == "col" ? (const void*)D.c_col : (const void*)D.c_val, 4 * (size_t)ptr[S.Np],
+                     cudaMemcpyDeviceToHost);
+      } else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
+    }
     else if (n.rfind("send_", 0) == 0 || n.rfind("recv_", 0) == 0) {
       const std::string kinds = "mqu";
       const bool snd = n[0] == 's';

@@ -27,6 +27,16 @@ struct Csr {
   int64_t nnz() const { return (int64_t)col.size(); }
 };
 
+// One (row, element image) Z0 integration task for the GPU (z0_gpu.cu).
+struct Z0Item {
+  int64_t row;        // observer parent n
+  int32_t tet;        // element id
+  int16_t code;       // packed lattice shift of the element image
+  int8_t va;          // local vertex that coincides with the observer, or -1
+  uint8_t flags;      // bit j: local vertex j is a near source of row n
+  int16_t pos[4];     // row-relative column slot of each local vertex
+};
+
 // Multi-GPU plan: contiguous internal-row ranges per rank and halo exchange index lists
 // (internal row indices) for the gathered vectors M (m), Q (q), U (u).
 struct DistPlan {
@@ -75,10 +85,12 @@ struct HostSetup {
   int order = 1;
   double rer_scale = 2.0;
   int z0_ring = 1;
+  int z0_device = -1;               // >= 0: Z0 element integrals run on this CUDA device
   std::vector<double> xw;           // [Np][3] wrapped parent coordinates
   std::vector<int32_t> st_s;        // [Np][3] unwrapped stencil start index
   std::vector<double> st_t;         // [Np][3] t - s (local coordinate in grid units)
-  Csr cbox;                         // nv = 1
+  Csr cbox;                         // nv = 1 (empty when built on the device, cbox_device)
+  bool cbox_device = false;         // device contexts build C_box on the GPU (cbox_gpu.cu)
   // internal order
   std::vector<int64_t> perm;        // internal row i -> user parent id
   std::vector<int64_t> iperm;       // user parent id -> internal row
@@ -95,6 +107,10 @@ void setup_z0(HostSetup& S);
 void setup_aim(HostSetup& S, const pmfem_grid* g);
 void setup_order(HostSetup& S);
 void setup_dist(HostSetup& S, int rank, int world);
+struct TriRules;
+void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& items,
+                         const std::vector<std::vector<int32_t>>& rcol, std::vector<std::vector<double>>& rval,
+                         const TriRules& rules, int64_t r0, int64_t r1);
 
 // Periodic Green's function (Ewald) -- host/device fp64, defined in pgf.cuh.
 struct PgfParams {

@@ -89,6 +89,10 @@ void setup_aim(HostSetup& S, const pmfem_grid* g) {
       S.st_t[3 * n + a] = t - (double)s;
     }
 
+  if (S.cbox_device) {            // device contexts: C_box is built on the GPU (cbox_gpu.cu)
+    S.cbox = Csr();
+    return;
+  }
   // near pairs (K8) by a box list on the wrapped coordinates, box size r_ER
   int64_t nb[3];
   double blo[3];

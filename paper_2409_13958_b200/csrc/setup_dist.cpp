@@ -7,6 +7,8 @@
 // Every rank runs the same deterministic setup on the full mesh, so each rank computes every
 // peer's needs locally: no coordination is required to build the plan.
 #include <algorithm>
+#include <cmath>
+#include <cstdlib>
 #include <numeric>
 #include <omp.h>
 #include "pmfem_internal.h"
@@ -43,9 +45,62 @@ void setup_dist(HostSetup& S, int rank, int world) {
   const Csr* ops[3][2] = {{&S.ring1, &S.z0}, {&S.cbox, nullptr}, {&S.ring1, nullptr}};
   std::vector<std::vector<int32_t>> need[3];
   for (int k = 0; k < 3; ++k) need[k].resize(world);
+  // C_box built on the device: q halo = every foreign node in the r_ER boxes (edge >= r_ER)
+  // adjacent to a box holding an owned node -- a superset of the C_box columns
+  // (PMFEM_GEOMETRIC_QHALO=1 forces this path on host-only contexts so the CPU tests cover it)
+  const bool geometric_q = S.cbox.rowptr.empty() || std::getenv("PMFEM_GEOMETRIC_QHALO") != nullptr;
+  std::vector<int64_t> bkey;
+  int64_t nb[3] = {1, 1, 1};
+  if (geometric_q && world > 1) {
+    const double rer = S.rer_scale * std::max(S.delta[0], std::max(S.delta[1], S.delta[2]));
+    double blo[3], bs[3];
+    for (int a = 0; a < 3; ++a) {
+      double lo = 1e300, hi = -1e300;
+      for (int64_t n = 0; n < Np; ++n) { lo = std::min(lo, S.xw[3 * n + a]); hi = std::max(hi, S.xw[3 * n + a]); }
+      if (S.periodic[a]) { blo[a] = 0; nb[a] = std::max<int64_t>(1, (int64_t)std::floor(S.L[a] / rer)); bs[a] = S.L[a] / nb[a]; }
+      else { blo[a] = lo; nb[a] = (int64_t)std::floor((hi - lo) / rer) + 1; bs[a] = rer; }
+    }
+    bkey.resize(Np);
+    for (int64_t i = 0; i < Np; ++i) {
+      const int64_t r = S.perm[i];
+      int64_t b[3];
+      for (int a = 0; a < 3; ++a)
+        b[a] = std::min<int64_t>(std::max<int64_t>((int64_t)std::floor((S.xw[3 * r + a] - blo[a]) / bs[a]), 0), nb[a] - 1);
+      bkey[i] = (b[0] * nb[1] + b[1]) * nb[2] + b[2];
+    }
+    const int64_t nbox = nb[0] * nb[1] * nb[2];
+    std::vector<std::vector<int32_t>> box_nodes(nbox);
+    for (int64_t i = 0; i < Np; ++i) box_nodes[bkey[i]].push_back((int32_t)i);
+    for (int p = 0; p < world; ++p) {
+      std::vector<char> mark(nbox, 0);
+      for (int64_t i = D.bounds[p]; i < D.bounds[p + 1]; ++i) {
+        const int64_t b = bkey[i];
+        const int64_t b0 = b / (nb[1] * nb[2]), b1 = (b / nb[2]) % nb[1], b2 = b % nb[2];
+        for (int dx = -1; dx <= 1; ++dx)
+          for (int dy = -1; dy <= 1; ++dy)
+            for (int dz = -1; dz <= 1; ++dz) {
+              int64_t c[3] = {b0 + dx, b1 + dy, b2 + dz};
+              bool ok = true;
+              for (int a = 0; a < 3; ++a) {
+                if (S.periodic[a]) c[a] = ((c[a] % nb[a]) + nb[a]) % nb[a];
+                else ok &= (c[a] >= 0 && c[a] < nb[a]);
+              }
+              if (ok) mark[(c[0] * nb[1] + c[1]) * nb[2] + c[2]] = 1;
+            }
+      }
+      std::vector<int32_t> v;
+      for (int64_t b = 0; b < nbox; ++b)
+        if (mark[b])
+          for (int32_t i : box_nodes[b])
+            if (i < D.bounds[p] || i >= D.bounds[p + 1]) v.push_back(i);
+      std::sort(v.begin(), v.end());
+      need[1][p] = std::move(v);
+    }
+  }
 #pragma omp parallel for collapse(2) schedule(dynamic)
   for (int k = 0; k < 3; ++k)
     for (int p = 0; p < world; ++p) {
+      if (k == 1 && geometric_q) continue;
       std::vector<int32_t> v;
       for (int64_t i = D.bounds[p]; i < D.bounds[p + 1]; ++i) {
         const int64_t r = S.perm[i];

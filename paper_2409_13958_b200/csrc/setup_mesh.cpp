@@ -42,10 +42,18 @@ struct CellHash {
   template <class F>
   void query(const double p[3], const std::vector<double>& xyz, double tol, F&& f) const {
     int64_t c[3];
-    for (int a = 0; a < 3; ++a) c[a] = (int64_t)std::floor((p[a] - lo[a]) / cell);
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy)
-        for (int dz = -1; dz <= 1; ++dz) {
+    int lo_o[3], hi_o[3];
+    for (int a = 0; a < 3; ++a) {
+      const double u = (p[a] - lo[a]) / cell;
+      c[a] = (int64_t)std::floor(u);
+      // only the neighbouring cells the tol-ball reaches (tol << cell: almost always one cell)
+      const double f = (u - (double)c[a]) * cell;
+      lo_o[a] = (f <= tol) ? -1 : 0;
+      hi_o[a] = (cell - f <= tol) ? 1 : 0;
+    }
+    for (int dx = lo_o[0]; dx <= hi_o[0]; ++dx)
+      for (int dy = lo_o[1]; dy <= hi_o[1]; ++dy)
+        for (int dz = lo_o[2]; dz <= hi_o[2]; ++dz) {
           int64_t cc[3] = {c[0] + dx, c[1] + dy, c[2] + dz};
           bool ok = true;
           for (int a = 0; a < 3; ++a) ok &= (cc[a] >= 0 && cc[a] < dim[a]);

@@ -1,0 +1,152 @@
+// Exact element integrals of the Z0 near-field correction, host + device, fp64.
+//
+// For an observer o and a tetrahedron T with linear basis phi_i:
+//   A_m    = int_T phi_m(r) / |o - r| dV
+//   B_km   = int_T phi_k(r) phi_m(r) (o - r) / |o - r|^3 dV
+// via the signed cone decomposition from o,
+//   int_T g dV = sum_F h_F int_F dA(y) int_0^1 t^2 g(o + t (y - o)) dt,
+// h_F = signed distance from o to the plane of face F (positive on the inner side).  With
+// phi(o + t(y-o)) = a + t b (a = phi(o), b = phi(y) - phi(o)) the radial integrals are exact:
+//   A : t^2 * phi_m / (t |y-o|)               -> (a_m/6 + phi_m(y)/3) / |y-o|
+//   B : t^2 * phi_k phi_m (-t(y-o))/(t^3|y-o|^3) -> -(a_k a_m + (a_k b_m + a_m b_k)/2 + b_k b_m/3) (y-o)/|y-o|^3
+// leaving smooth face integrals, evaluated with collapsed Gauss rules (n = 4, 6, 8 chosen by
+// the size/distance ratio) on adaptively subdivided triangles (iterative, explicit stack).
+#pragma once
+#include <cmath>
+
+#ifdef __CUDACC__
+#define ZC_HD __host__ __device__
+#else
+#define ZC_HD
+#endif
+
+namespace pmfem {
+
+struct TriRules {              // collapsed n x n Gauss on the reference triangle, n = 4, 6, 8
+  double l0[116], l1[116], l2[116], w[116];
+  int off[3], cnt[3];
+};
+
+// host: fill the three rules (Gauss-Legendre nodes on [0,1] by Newton iteration)
+void build_tri_rules(TriRules& R);
+
+ZC_HD inline double zc_dot(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+
+struct ConeIntegrator {
+  double P[4][3], g[4][3], c[4];     // phi_i(r) = c_i + g_i . r
+  double o[3], a[4];
+  double A[4], B[4][4][3];
+  const TriRules* R;
+
+  ZC_HD double phi(int i, const double* r) const { return c[i] + zc_dot(g[i], r); }
+
+  ZC_HD void quad(const double* V0, const double* V1, const double* V2, double h, double size, double dest) {
+    double e01[3], e02[3];
+    for (int x = 0; x < 3; ++x) { e01[x] = V1[x] - V0[x]; e02[x] = V2[x] - V0[x]; }
+    const double cr[3] = {e01[1] * e02[2] - e01[2] * e02[1], e01[2] * e02[0] - e01[0] * e02[2],
+                          e01[0] * e02[1] - e01[1] * e02[0]};
+    const double area2 = sqrt(zc_dot(cr, cr));
+    const double ratio = size / dest;
+    const int r = ratio <= 0.3 ? 0 : (ratio <= 0.6 ? 1 : 2);
+    for (int q = R->off[r]; q < R->off[r] + R->cnt[r]; ++q) {
+      double y[3];
+      for (int x = 0; x < 3; ++x) y[x] = R->l0[q] * V0[x] + R->l1[q] * V1[x] + R->l2[q] * V2[x];
+      const double Rv[3] = {y[0] - o[0], y[1] - o[1], y[2] - o[2]};
+      const double inv = 1.0 / sqrt(zc_dot(Rv, Rv));
+      const double inv3 = inv * inv * inv;
+      const double w = R->w[q] * area2 * h;
+      double py[4], b[4];
+      for (int i = 0; i < 4; ++i) { py[i] = phi(i, y); b[i] = py[i] - a[i]; }
+      for (int m = 0; m < 4; ++m) A[m] += w * (a[m] / 6.0 + py[m] / 3.0) * inv;
+      for (int k = 0; k < 4; ++k)
+        for (int m = k; m < 4; ++m) {
+          const double s = -w * (a[k] * a[m] + 0.5 * (a[k] * b[m] + a[m] * b[k]) + b[k] * b[m] / 3.0) * inv3;
+          for (int x = 0; x < 3; ++x) B[k][m][x] += s * Rv[x];
+        }
+    }
+  }
+
+  // adaptive face integral: split into 4 while size > dest (distance lower bound), depth <= 7
+  ZC_HD void face(const double* F0, const double* F1, const double* F2, double h) {
+    struct Tri { double v[3][3]; int depth; };
+    Tri stack[24];
+    int top = 0;
+    for (int x = 0; x < 3; ++x) { stack[0].v[0][x] = F0[x]; stack[0].v[1][x] = F1[x]; stack[0].v[2][x] = F2[x]; }
+    stack[0].depth = 0;
+    top = 1;
+    while (top > 0) {
+      const Tri T = stack[--top];
+      const double* V0 = T.v[0];
+      const double* V1 = T.v[1];
+      const double* V2 = T.v[2];
+      double cen[3], e01[3], e02[3], e12[3];
+      for (int x = 0; x < 3; ++x) {
+        cen[x] = (V0[x] + V1[x] + V2[x]) / 3.0;
+        e01[x] = V1[x] - V0[x]; e02[x] = V2[x] - V0[x]; e12[x] = V2[x] - V1[x];
+      }
+      const double size = sqrt(fmax(zc_dot(e01, e01), fmax(zc_dot(e02, e02), zc_dot(e12, e12))));
+      double rc = 0;
+      for (int k = 0; k < 3; ++k) {
+        const double d[3] = {T.v[k][0] - cen[0], T.v[k][1] - cen[1], T.v[k][2] - cen[2]};
+        rc = fmax(rc, sqrt(zc_dot(d, d)));
+      }
+      const double dc[3] = {cen[0] - o[0], cen[1] - o[1], cen[2] - o[2]};
+      const double dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
+      if (size > dest && T.depth < 7 && top + 4 <= 24) {
+        double m01[3], m02[3], m12[3];
+        for (int x = 0; x < 3; ++x) {
+          m01[x] = 0.5 * (V0[x] + V1[x]); m02[x] = 0.5 * (V0[x] + V2[x]); m12[x] = 0.5 * (V1[x] + V2[x]);
+        }
+        const double* kids[4][3] = {{V0, m01, m02}, {m01, V1, m12}, {m02, m12, V2}, {m12, m02, m01}};
+        for (int c4 = 0; c4 < 4; ++c4) {
+          Tri& N = stack[top++];
+          for (int k = 0; k < 3; ++k)
+            for (int x = 0; x < 3; ++x) N.v[k][x] = kids[c4][k][x];
+          N.depth = T.depth + 1;
+        }
+        continue;
+      }
+      quad(V0, V1, V2, h, size, dest);
+    }
+  }
+
+  // va >= 0: o is vertex va of T (only the opposite face has h != 0)
+  ZC_HD void run(int va) {
+    for (int i = 0; i < 4; ++i) {
+      A[i] = 0;
+      for (int j = 0; j < 4; ++j)
+        for (int x = 0; x < 3; ++x) B[i][j][x] = 0;
+    }
+    for (int i = 0; i < 4; ++i) c[i] = 1.0 - zc_dot(g[i], P[i]);
+    for (int i = 0; i < 4; ++i) a[i] = (va >= 0) ? (i == va ? 1.0 : 0.0) : phi(i, o);
+    for (int j = 0; j < 4; ++j) {
+      if (va >= 0 && j != va) continue;
+      const double gn = sqrt(zc_dot(g[j], g[j]));
+      const double h = a[j] / gn;            // phi_j(o) = |g_j| h_j
+      if (fabs(h) * gn < 1e-14) continue;
+      face(P[(j + 1) % 4], P[(j + 2) % 4], P[(j + 3) % 4], h);
+    }
+    for (int k = 0; k < 4; ++k)
+      for (int m = 0; m < k; ++m)
+        for (int x = 0; x < 3; ++x) B[k][m][x] = B[m][k][x];
+  }
+};
+
+// element gradients from vertex coordinates: grad phi_i = rows of J^-1 (J cols = P_i - P_0)
+ZC_HD inline void tet_grads(const double P[4][3], double g[4][3]) {
+  double e[3][3];
+  for (int k = 0; k < 3; ++k)
+    for (int x = 0; x < 3; ++x) e[k][x] = P[k + 1][x] - P[0][x];
+  auto cross = [](const double* u, const double* v, double* w) {
+    w[0] = u[1] * v[2] - u[2] * v[1]; w[1] = u[2] * v[0] - u[0] * v[2]; w[2] = u[0] * v[1] - u[1] * v[0];
+  };
+  cross(e[1], e[2], g[1]);
+  cross(e[2], e[0], g[2]);
+  cross(e[0], e[1], g[3]);
+  const double det = zc_dot(e[0], g[1]);
+  for (int k = 1; k < 4; ++k)
+    for (int x = 0; x < 3; ++x) g[k][x] /= det;
+  for (int x = 0; x < 3; ++x) g[0][x] = -(g[1][x] + g[2][x] + g[3][x]);
+}
+
+}  // namespace pmfem

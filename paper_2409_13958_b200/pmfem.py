@@ -85,6 +85,8 @@ for _n in SYMBOLS:
 _EXPORT_DTYPES = {"parent": np.int64, "lca": np.int64, "shift": np.int32, "ring1_rowptr": np.int64,
                   "ring1_col": np.int32, "z0_rowptr": np.int64, "z0_col": np.int32, "cbox_rowptr": np.int64,
                   "cbox_col": np.int32, "stencil_s": np.int32, "perm": np.int64, "dist_bounds": np.int64}
+_EXPORT_DTYPES.update({"cbox_device_rowptr": np.int64, "cbox_device_col": np.int32,
+                       "cbox_device_val": np.float32})
 for _k in "mqu":
     _EXPORT_DTYPES["send_%s_ptr" % _k] = np.int64
     _EXPORT_DTYPES["recv_%s_ptr" % _k] = np.int64

@@ -33,9 +33,11 @@ def _csr_internal(ctx, prefix, nv, perm, iperm):
     return rows
 
 
-def _worker(rank, world, port, key, out):
+def _worker(rank, world, port, key, out, geometric=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    if geometric:
+        os.environ["PMFEM_GEOMETRIC_QHALO"] = "1"     # the q-halo rule used when C_box is GPU-built
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import torch
     from paper_2409_13958_b200 import Context
@@ -113,12 +115,13 @@ def _worker(rank, world, port, key, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("key", ["C1r1", "C3p1", "C5p2"])
-def test_dist_plan_world2(key):
+@pytest.mark.parametrize("key,geometric", [("C1r1", False), ("C3p1", False), ("C5p2", False),
+                                           ("C2p2", True), ("C5p2", True)])
+def test_dist_plan_world2(key, geometric):
     world = 2
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.start_processes(_worker, args=(world, _free_port(), key, out), nprocs=world, start_method="spawn")
+    mp.start_processes(_worker, args=(world, _free_port(), key, out, geometric), nprocs=world, start_method="spawn")
     res = [out[r] for r in range(world)]
     assert all(r[0] for r in res), res
     # contiguous, covering, slice-aligned partition
