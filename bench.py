@@ -176,6 +176,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
+    # a dedicated (non-default) stream: the library captures each evaluation into a CUDA graph
+    torch.cuda.set_stream(torch.cuda.Stream())
     dev = local
     from paper_2409_13958_b200 import Context, KERNELS
     from synth import make_config

@@ -618,6 +618,8 @@ void device_free(DeviceState& D) {
     if (p) cudaFree(p);
   for (int i = 0; i < 8; ++i)
     if (D.ev[i]) cudaEventDestroy(D.ev[i]);
+  for (auto& g : D.graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   if (D.comm) ncclCommDestroy((ncclComm_t)D.comm);
 }
 

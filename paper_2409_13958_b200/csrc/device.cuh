@@ -67,6 +67,17 @@ struct DeviceState {
   float* send_buf = nullptr;
   float* recv_buf = nullptr;
   double comm_bytes_per_eval = 0;
+  // captured evaluation graphs (pmfem_api.cu eval_graph)
+  struct GraphSlot {
+    const float* m = nullptr;
+    float* H = nullptr;
+    cudaStream_t st = nullptr;
+    int mode = -1;
+    bool timing = false;
+    cudaGraphExec_t exec = nullptr;
+  };
+  GraphSlot graphs[4];
+  int graph_next = 0;
 };
 
 void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id);

@@ -1,5 +1,6 @@
 // extern "C" entry points of libpmfem (include/pmfem.h).  No exception crosses the ABI.
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <nccl.h>
@@ -136,12 +137,52 @@ pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err) {
   });
 }
 
+// One evaluation = ~9 kernel launches (+ NCCL calls on N>1).  On a non-default stream the
+// sequence is captured once per (m, H, stream, mode, timing) into a CUDA graph and replayed
+// (launch overhead paid once); PMFEM_NO_GRAPH=1 disables it.  The legacy default stream cannot
+// be captured, so calls on it launch the kernels directly.
+static void eval_graph(pmfem_ctx ctx, const float* m, float* H, cudaStream_t st, pmfem::EvalMode mode) {
+  pmfem::DeviceState& D = ctx->D;
+  static const bool no_graph = std::getenv("PMFEM_NO_GRAPH") != nullptr;
+  if (no_graph || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
+    pmfem::device_eval(D, m, H, st, mode);
+    return;
+  }
+  for (auto& g : D.graphs)
+    if (g.exec && g.m == m && g.H == H && g.st == st && g.mode == (int)mode && g.timing == D.timing) {
+      if (cudaGraphLaunch(g.exec, st) != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, "cudaGraphLaunch failed");
+      return;
+    }
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    throw pmfem::Error(PMFEM_E_CUDA, "cudaStreamBeginCapture failed");
+  try {
+    pmfem::device_eval(D, m, H, st, mode);
+  } catch (...) {
+    cudaStreamEndCapture(st, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  if (cudaStreamEndCapture(st, &graph) != cudaSuccess || !graph)
+    throw pmfem::Error(PMFEM_E_CUDA, "cudaStreamEndCapture failed");
+  cudaGraphExec_t exec = nullptr;
+  cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+  // replace the least recently inserted slot
+  pmfem::DeviceState::GraphSlot& slot = D.graphs[D.graph_next];
+  D.graph_next = (D.graph_next + 1) % (int)(sizeof(D.graphs) / sizeof(D.graphs[0]));
+  if (slot.exec) cudaGraphExecDestroy(slot.exec);
+  slot = pmfem::DeviceState::GraphSlot{m, H, st, (int)mode, D.timing, exec};
+  if (cudaGraphLaunch(exec, st) != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, "cudaGraphLaunch failed");
+}
+
 static pmfem_status eval(pmfem_ctx ctx, const float* m, float* H, void* stream, pmfem::EvalMode mode) {
   if (!ctx) return PMFEM_E_INVALID_ARG;
   return guard(ctx, [&] {
     check_eval(ctx, m, H);
     cudaStream_t st = (cudaStream_t)stream;
-    pmfem::device_eval(ctx->D, m, H, st, mode);
+    eval_graph(ctx, m, H, st, mode);
     record_timing(ctx, st);
   });
 }

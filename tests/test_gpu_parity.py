@@ -94,3 +94,23 @@ def test_linearity_and_repeatability(pair):
     assert rel_l2(Hab, 0.5 * Ha - 2.0 * Hb) <= 1e-5
     Ha2 = _run(ctx, "demag", a, rank)
     assert rel_l2(Ha2, Ha) <= 1e-6          # only atomic-add ordering differs
+
+
+def test_graph_replay(pair):
+    """On a non-default stream each evaluation is a captured CUDA graph replayed on later calls:
+    the replay must follow new data behind the same pointers (and match the oracle)."""
+    import torch
+    key, om, ctx = pair
+    rank = ctx.internal_to_parent_rank()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        m_dev = torch.empty((om.n_parents, 3), dtype=torch.float32, device="cuda:0")
+        H = torch.empty_like(m_dev)
+        for seed in (21, 22, 23):
+            m = m_random(om.n_parents, seed=seed)
+            m_dev.copy_(torch.tensor(m[rank], dtype=torch.float32))
+            ctx.heff(m_dev, H)
+            s.synchronize()
+            out = np.zeros_like(m)
+            out[rank] = H.double().cpu().numpy()
+            assert rel_l2(out, om.heff(m, "aim")) <= TOL
