@@ -136,6 +136,16 @@ pmfem_status pmfem_heff    (pmfem_ctx ctx, const float* m, float* H, void* cuda_
  * stream and the call returns after the stream is synchronised (end-to-end path). */
 pmfem_status pmfem_heff_host(pmfem_ctx ctx, const float* m_host, float* H_host, void* cuda_stream);
 
+/* NEXT-2: `steps` classical RK4 steps of the LLG equation (P:67-71, P:101-105,
+ * Eq. llg; reading R18) dm/dt = -gamma/(1+alpha^2) [m x H + alpha m x (m x H)],
+ * H = H_ms + H_ex + H_applied (uniform, Oe), |m| renormalised to 1 after every step.
+ * m: device pointer [n_parents_local][3] fp32, updated in place.  dt in s, gamma in rad/(s Oe)
+ * (1.7595e7 for electrons).  Each step = 4 pmfem_heff evaluations + 4 fused stage kernels; on a
+ * non-default stream the step is captured once into a CUDA graph and replayed `steps` times.
+ * H_applied may be NULL (zero).  Asynchronous like the field calls. */
+pmfem_status pmfem_llg_rk4(pmfem_ctx ctx, float* m, int64_t steps, double dt, double alpha, double gamma,
+                           const double* H_applied, void* cuda_stream);
+
 pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out);
 
 /* internal_to_user[i] = original (user) node index of the parent stored in internal row i. */

@@ -288,6 +288,34 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
   else { H[3 * (n - rr.hoff)] = -gx; H[3 * (n - rr.hoff) + 1] = -gy; H[3 * (n - rr.hoff) + 2] = -gz; }
 }
 
+// ------------------------------------------------------------------ LLG RK4 stage (NEXT-2)
+// dm/dt = -g [ m x H + alpha m x (m x H) ], g = gamma / (1 + alpha^2)   (Eq. llg)
+// Stage s of classical RK4: k = f(ms, H + H_ap); acc (+)= w_s dt k; next stage state
+// m0 + c_{s+1} dt k, or (last stage) m0 <- normalize(m0 + acc).  Rank-local rows.
+__global__ void k_llg_stage(int64_t n, float* __restrict__ m0, const float* __restrict__ ms,
+                            const float* __restrict__ H, float hx, float hy, float hz, float g, float alpha,
+                            float wdt, float cnext_dt, float* __restrict__ acc, float* __restrict__ mnext,
+                            int first, int last) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float sx = ms[3 * i], sy = ms[3 * i + 1], sz = ms[3 * i + 2];
+  const float Hx = H[3 * i] + hx, Hy = H[3 * i + 1] + hy, Hz = H[3 * i + 2] + hz;
+  const float cx = sy * Hz - sz * Hy, cy = sz * Hx - sx * Hz, cz = sx * Hy - sy * Hx;        // m x H
+  const float dx = sy * cz - sz * cy, dy = sz * cx - sx * cz, dz = sx * cy - sy * cx;        // m x (m x H)
+  const float kx = -g * (cx + alpha * dx), ky = -g * (cy + alpha * dy), kz = -g * (cz + alpha * dz);
+  float ax = wdt * kx, ay = wdt * ky, az = wdt * kz;
+  if (!first) { ax += acc[3 * i]; ay += acc[3 * i + 1]; az += acc[3 * i + 2]; }
+  const float m0x = m0[3 * i], m0y = m0[3 * i + 1], m0z = m0[3 * i + 2];
+  if (!last) {
+    acc[3 * i] = ax; acc[3 * i + 1] = ay; acc[3 * i + 2] = az;
+    mnext[3 * i] = m0x + cnext_dt * kx; mnext[3 * i + 1] = m0y + cnext_dt * ky; mnext[3 * i + 2] = m0z + cnext_dt * kz;
+  } else {
+    const float nx = m0x + ax, ny = m0y + ay, nz = m0z + az;
+    const float inv = rsqrtf(nx * nx + ny * ny + nz * nz);
+    m0[3 * i] = nx * inv; m0[3 * i + 1] = ny * inv; m0[3 * i + 2] = nz * inv;
+  }
+}
+
 // ------------------------------------------------------------------ PGF table (fp64)
 // One thread per point of the octant j_a in [0, P_a/2]; the value is written to every mirror
 // position j_a and P_a - j_a (K is even on each axis: lattice reflection symmetry + periodicity
@@ -620,6 +648,9 @@ void device_free(DeviceState& D) {
     if (D.ev[i]) cudaEventDestroy(D.ev[i]);
   for (auto& g : D.graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
+  if (D.llg_exec) cudaGraphExecDestroy(D.llg_exec);
+  for (void* p : {(void*)D.llg_ms, (void*)D.llg_H, (void*)D.llg_acc})
+    if (p) cudaFree(p);
   if (D.comm) ncclCommDestroy((ncclComm_t)D.comm);
 }
 
@@ -741,6 +772,34 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   k5_grad_sum<<<thr_blocks, 256, 0, st>>>(rr, D.u, D.sl1_off, D.s_Gc, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(5);
+}
+
+}  // namespace pmfem
+
+namespace pmfem {
+
+// One classical RK4 step of the LLG equation on the rank-local rows of m (in place):
+// 4 H_eff evaluations + 4 fused stage kernels (k_llg_stage).
+void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
+                         const double Hap[3]) {
+  const int64_t n = D.hi - D.lo;
+  if (n <= 0) return;
+  if (!D.llg_ms) {
+    D.llg_ms = dalloc<float>(3 * (size_t)n);
+    D.llg_H = dalloc<float>(3 * (size_t)n);
+    D.llg_acc = dalloc<float>(3 * (size_t)n);
+  }
+  const float g = (float)(gamma / (1.0 + alpha * alpha));
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const float w[4] = {(float)(dt / 6), (float)(dt / 3), (float)(dt / 3), (float)(dt / 6)};
+  const float c[4] = {(float)(dt / 2), (float)(dt / 2), (float)dt, 0.f};
+  for (int s = 0; s < 4; ++s) {
+    const float* ms = (s == 0) ? m : D.llg_ms;
+    device_eval(D, ms, D.llg_H, st, EVAL_HEFF);
+    k_llg_stage<<<blocks, 256, 0, st>>>(n, m, ms, D.llg_H, (float)Hap[0], (float)Hap[1], (float)Hap[2], g,
+                                        (float)alpha, w[s], c[s], D.llg_acc, D.llg_ms, s == 0, s == 3);
+    CK(cudaGetLastError());
+  }
 }
 
 }  // namespace pmfem

@@ -78,7 +78,18 @@ struct DeviceState {
   };
   GraphSlot graphs[4];
   int graph_next = 0;
+  // LLG RK4 scratch (rank-local rows) and the captured RK4 step
+  float* llg_ms = nullptr;
+  float* llg_H = nullptr;
+  float* llg_acc = nullptr;
+  cudaGraphExec_t llg_exec = nullptr;
+  const float* llg_key_m = nullptr;
+  cudaStream_t llg_key_st = nullptr;
+  double llg_key[6] = {0, 0, 0, 0, 0, 0};
 };
+
+void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
+                         const double Hap[3]);
 
 void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id);
 int64_t device_build_cbox(DeviceState& D, const HostSetup& S);

@@ -187,6 +187,54 @@ static pmfem_status eval(pmfem_ctx ctx, const float* m, float* H, void* stream, 
   });
 }
 
+pmfem_status pmfem_llg_rk4(pmfem_ctx ctx, float* m, int64_t steps, double dt, double alpha, double gamma,
+                           const double* H_applied, void* stream) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    pmfem::require(!ctx->host_only, PMFEM_E_STATE, "host-only context (cuda_device = -1) cannot integrate");
+    pmfem::require(m != nullptr, PMFEM_E_INVALID_ARG, "NULL m");
+    pmfem::require(ctx->D.pgf_ready, PMFEM_E_STATE, "pmfem_build_pgf has not been called");
+    cudaSetDevice(ctx->D.device);
+    pmfem::require(steps >= 0 && dt > 0 && alpha >= 0 && gamma > 0, PMFEM_E_INVALID_ARG, "bad LLG parameters");
+    const double zero[3] = {0, 0, 0};
+    const double* hap = H_applied ? H_applied : zero;
+    pmfem::DeviceState& D = ctx->D;
+    cudaStream_t st = (cudaStream_t)stream;
+    static const bool no_graph = std::getenv("PMFEM_NO_GRAPH") != nullptr;
+    if (no_graph || st == nullptr || st == cudaStreamLegacy || st == cudaStreamPerThread) {
+      for (int64_t s = 0; s < steps; ++s) pmfem::device_llg_rk4_step(D, m, st, dt, alpha, gamma, hap);
+      return;
+    }
+    const double key[6] = {dt, alpha, gamma, hap[0], hap[1], hap[2]};
+    bool hit = D.llg_exec && D.llg_key_m == m && D.llg_key_st == st && !D.timing;
+    for (int i = 0; i < 6 && hit; ++i) hit = D.llg_key[i] == key[i];
+    if (!hit && steps > 0) {
+      if (D.llg_exec) { cudaGraphExecDestroy(D.llg_exec); D.llg_exec = nullptr; }
+      if (!D.llg_ms) pmfem::device_llg_rk4_step(D, m, st, dt, alpha, gamma, hap), --steps;   // allocates scratch
+      cudaGraph_t graph = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        throw pmfem::Error(PMFEM_E_CUDA, "cudaStreamBeginCapture failed");
+      try {
+        pmfem::device_llg_rk4_step(D, m, st, dt, alpha, gamma, hap);
+      } catch (...) {
+        cudaStreamEndCapture(st, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      if (cudaStreamEndCapture(st, &graph) != cudaSuccess || !graph)
+        throw pmfem::Error(PMFEM_E_CUDA, "cudaStreamEndCapture failed");
+      cudaError_t e = cudaGraphInstantiate(&D.llg_exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (e != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, "cudaGraphInstantiate failed");
+      D.llg_key_m = m;
+      D.llg_key_st = st;
+      for (int i = 0; i < 6; ++i) D.llg_key[i] = key[i];
+    }
+    for (int64_t s = 0; s < steps; ++s)
+      if (cudaGraphLaunch(D.llg_exec, st) != cudaSuccess) throw pmfem::Error(PMFEM_E_CUDA, "cudaGraphLaunch failed");
+  });
+}
+
 pmfem_status pmfem_demag(pmfem_ctx ctx, const float* m, float* H, void* s) { return eval(ctx, m, H, s, pmfem::EVAL_DEMAG); }
 pmfem_status pmfem_exchange(pmfem_ctx ctx, const float* m, float* H, void* s) { return eval(ctx, m, H, s, pmfem::EVAL_EXCHANGE); }
 pmfem_status pmfem_heff(pmfem_ctx ctx, const float* m, float* H, void* s) { return eval(ctx, m, H, s, pmfem::EVAL_HEFF); }

@@ -22,7 +22,7 @@ STATUS = {0: "PMFEM_OK", 1: "PMFEM_E_INVALID_ARG", 2: "PMFEM_E_MESH", 3: "PMFEM_
           7: "PMFEM_E_PGF_NOT_CONVERGED", 8: "PMFEM_E_STATE", 9: "PMFEM_E_CUDA", 10: "PMFEM_E_NCCL",
           11: "PMFEM_E_OOM"}
 
-SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
+SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_llg_rk4", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
            "pmfem_heff_host", "pmfem_query", "pmfem_get_order", "pmfem_export", "pmfem_set_timing",
            "pmfem_get_timing", "pmfem_last_error", "pmfem_destroy"]
 
@@ -70,6 +70,8 @@ _lib.pmfem_nccl_unique_id.argtypes = [ctypes.c_void_p]
 _lib.pmfem_build_pgf.argtypes = [_vp, ctypes.c_double]
 for _n in ("pmfem_demag", "pmfem_exchange", "pmfem_heff", "pmfem_heff_host"):
     getattr(_lib, _n).argtypes = [_vp, _vp, _vp, _vp]
+_lib.pmfem_llg_rk4.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                              ctypes.c_void_p, _vp]
 _lib.pmfem_query.argtypes = [_vp, ctypes.POINTER(_Info)]
 _lib.pmfem_get_order.argtypes = [_vp, ctypes.POINTER(ctypes.c_int64)]
 _lib.pmfem_export.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(ctypes.c_int64)]
@@ -194,6 +196,13 @@ class Context:
         self._check(_lib.pmfem_heff_host(self._h, _vp(m_host.data_ptr()), _vp(H_host.data_ptr()),
                                          self._stream(stream)))
         return H_host
+
+    def llg_rk4(self, m, steps, dt, alpha, gamma=1.7595e7, H_applied=(0.0, 0.0, 0.0), stream=None):
+        """`steps` RK4 steps of the LLG equation on m (float32 CUDA tensor [N'_local, 3], in place)."""
+        hap = (ctypes.c_double * 3)(*[float(v) for v in H_applied])
+        self._check(_lib.pmfem_llg_rk4(self._h, _dev_ptr(m), int(steps), float(dt), float(alpha), float(gamma),
+                                       ctypes.cast(hap, ctypes.c_void_p), self._stream(stream)))
+        return m
 
     def query(self):
         info = _Info()
