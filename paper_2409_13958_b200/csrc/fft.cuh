@@ -34,12 +34,19 @@ template <class C, class Base>
 __device__ void smem_fft(C* buf, int P, int logP, int nl, Base base, int es, const C* __restrict__ tw,
                          int tw_stride, bool inv, bool line_fast) {
   const int nb = P >> 1;
+  const bool pow2_nl = (nl & (nl - 1)) == 0;
+  const int lnl = __ffs(nl) - 1;
   for (int s = 0; s < logP; ++s) {
     const int half = 1 << s;
     const int tstep = (nb >> s) * tw_stride;
     for (int idx = threadIdx.x; idx < nl * nb; idx += blockDim.x) {
       int l, b;
-      if (line_fast) { l = idx % nl; b = idx / nl; } else { b = idx % nb; l = idx / nb; }
+      // power-of-two line counts (every line-fast call site) use shifts, not integer division
+      if (line_fast) {
+        if (pow2_nl) { l = idx & (nl - 1); b = idx >> lnl; } else { l = idx % nl; b = idx / nl; }
+      } else {
+        b = idx & (nb - 1); l = idx >> (logP - 1);
+      }
       const int j = b & (half - 1);
       const int i0 = ((b >> s) << (s + 1)) + j;
       C w = tw[j * tstep];
@@ -60,8 +67,9 @@ template <class C, class Base>
 __device__ void smem_bitrev(C* buf, int P, int logP, int nl, Base base, int es) {
   for (int idx = threadIdx.x; idx < nl * P; idx += blockDim.x) {
     // es == 1: element fastest (consecutive banks); else line fastest (lines are contiguous)
-    const int l = (es == 1) ? idx / P : idx % nl;
-    const int e = (es == 1) ? idx - l * P : idx / nl;
+    // P and (at every call site) nl are powers of two
+    const int l = (es == 1) ? (idx >> logP) : (idx & (nl - 1));
+    const int e = (es == 1) ? (idx & (P - 1)) : (idx >> (__ffs(nl) - 1));
     const int r = bitrev(e, logP);
     if (r > e) {
       C* p = buf + base(l);
@@ -92,7 +100,7 @@ __global__ void fft_x_forward(const T* __restrict__ in, typename Cx<T>::t* __res
   const int r0 = blockIdx.x * nl;
   const int nlines = min(nl, nrows - r0);
   for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    const int l = idx / M, j = idx - l * M;
+    const int l = idx >> logM, j = idx & (M - 1);
     const T* row = in + (long long)(r0 + l) * n0;
     C z;
     z.x = (2 * j < n0) ? row[2 * j] : T(0);
@@ -129,7 +137,7 @@ __global__ void fft_x_inverse(const typename Cx<T>::t* __restrict__ in, T* __res
   const int nlines = min(nl, nrows - r0);
   // Z_k = (X_k + conj X_{M-k}) + i W^{-k} (X_k - conj X_{M-k}),  k < M
   for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    const int l = idx / M, k = idx - l * M;
+    const int l = idx >> logM, k = idx & (M - 1);
     const C* row = in + rm.crow(r0 + l) * H0;
     C xk = row[k];
     C xm = cconj(row[M - k]);
@@ -142,7 +150,7 @@ __global__ void fft_x_inverse(const typename Cx<T>::t* __restrict__ in, T* __res
   __syncthreads();
   smem_fft<C>(buf, M, logM, nlines, RowBase{M}, 1, tw, 2, true, false);
   for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    const int l = idx / M, j = idx - l * M;
+    const int l = idx >> logM, j = idx & (M - 1);
     C z = buf[l * M + j];
     T* row = out + (long long)(r0 + l) * n0;
     if (2 * j < n0) row[2 * j] = z.x;
@@ -199,8 +207,8 @@ __global__ void fft_strided(typename Cx<T>::t* __restrict__ data, int P, int log
 struct PlaneBase {   // line l = (plane index l / tile, column l % tile); logP2 = 0: natural order
   int tile, plane, logP2;
   __device__ __forceinline__ int operator()(int l) const {
-    const int p = l / tile;
-    return (logP2 ? bitrev(p, logP2) : p) * plane + (l - p * tile);
+    const int p = l >> (__ffs(tile) - 1);        // tile is a power of two
+    return (logP2 ? bitrev(p, logP2) : p) * plane + (l & (tile - 1));
   }
 };
 
@@ -216,11 +224,12 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   const int c0 = blockIdx.x * tile;
   const int nc = min(tile, H0 - c0);
   const int plane = P1 * tile;
+  const int ltile = __ffs(tile) - 1, ln1 = __ffs(n1) - 1;     // tile, n1 powers of two
   // zero the whole tile (padded planes / rows must read as zero), then load the data block
   for (int idx = threadIdx.x; idx < P2 * plane; idx += blockDim.x) { C z; z.x = T(0); z.y = T(0); buf[idx] = z; }
   __syncthreads();
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
-    const int c = idx % tile, r = idx / tile, i1 = r % n1, i2 = r / n1;
+    const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
     if (c < nc)
       buf[bitrev(i2, logP2) * plane + bitrev(i1, logP1) * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
   }
@@ -235,7 +244,7 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   smem_fft<C>(buf, P2, logP2, plane, zbase, plane, tw2, 1, false, true);
   // multiply by the real spectrum G_hat[k2][k1][k0] (natural order now)
   for (int idx = threadIdx.x; idx < P2 * plane; idx += blockDim.x) {
-    const int c = idx % tile, r = idx / tile, k1 = r % P1, k2 = r / P1;
+    const int c = idx & (tile - 1), r = idx >> ltile, k1 = r & (P1 - 1), k2 = r >> logP1;
     const T g = (c < nc) ? spec[((long long)k2 * P1 + k1) * H0 + c0 + c] : T(0);
     C v = buf[idx];
     v.x *= g; v.y *= g;
@@ -250,7 +259,7 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   smem_bitrev<C>(buf, P1, logP1, n2 * tile, ybase2, tile);
   smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, tile > 1);
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
-    const int c = idx % tile, r = idx / tile, i1 = r % n1, i2 = r / n1;
+    const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
     if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * plane + i1 * tile + c];
   }
 }
