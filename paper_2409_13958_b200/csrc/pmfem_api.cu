@@ -1,5 +1,6 @@
 // extern "C" entry points of libpmfem (include/pmfem.h).  No exception crosses the ABI.
 #include <chrono>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -68,23 +69,33 @@ static pmfem_status setup_impl(pmfem_ctx* out, const pmfem_mesh* mesh, const pmf
   }
   pmfem_status st = guard(nullptr, [&] {
     double t0 = now();
+    static const bool verbose = std::getenv("PMFEM_VERBOSE") != nullptr;
+    auto stage = [&](const char* what) {
+      if (verbose) { std::fprintf(stderr, "[pmfem] %-16s %8.2f s\n", what, now() - t0); std::fflush(stderr); }
+    };
     pmfem::HostSetup& S = ctx->S;
     pmfem::setup_mesh(S, mesh, per);
+    stage("mesh/pbc");
     pmfem::setup_operators(S);
+    stage("operators");
     S.z0_ring = grid ? grid->z0_ring : 1;
     pmfem::require(grid != nullptr, PMFEM_E_INVALID_ARG, "NULL grid");
     pmfem::require(grid->z0_ring == 0 || grid->z0_ring == 1, PMFEM_E_INVALID_ARG, "z0_ring must be 0 or 1");
     S.z0_device = cuda_device;            // device contexts integrate Z0 on the GPU
     pmfem::setup_z0(S);
+    stage("z0");
     S.cbox_device = cuda_device >= 0;     // device contexts build C_box on the GPU
     pmfem::setup_aim(S, grid);
+    stage("aim");
     pmfem::setup_order(S);
     pmfem::setup_dist(S, rank, world);
+    stage("order/dist");
     S.setup_seconds = now() - t0;
     if (cuda_device >= 0) {
       ctx->host_only = false;
       ctx->D.device = cuda_device;
       pmfem::device_upload(ctx->D, S);
+      stage("device upload");
       if (world > 1) {
         pmfem::require(nccl_id != nullptr, PMFEM_E_INVALID_ARG, "NULL NCCL unique id");
         pmfem::device_init_comm(ctx->D, S, nccl_id);

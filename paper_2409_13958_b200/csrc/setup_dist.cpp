@@ -22,11 +22,13 @@ void setup_dist(HostSetup& S, int rank, int world) {
   D.world = world;
   const int64_t Np = S.Np;
   // per-row cost in bytes of the streamed operators (balanced partition)
+  // (a device-built C_box is not on the host: its per-row cost is then taken as uniform)
+  const bool have_cbox = !S.cbox.rowptr.empty();
   std::vector<double> cost(Np);
   for (int64_t i = 0; i < Np; ++i) {
     const int64_t r = S.perm[i];
     cost[i] = 64.0 + 20.0 * (S.ring1.rowptr[r + 1] - S.ring1.rowptr[r]) + 16.0 * (S.z0.rowptr[r + 1] - S.z0.rowptr[r]) +
-              8.0 * (S.cbox.rowptr[r + 1] - S.cbox.rowptr[r]);
+              (have_cbox ? 8.0 * (S.cbox.rowptr[r + 1] - S.cbox.rowptr[r]) : 0.0);
   }
   std::vector<double> pre(Np + 1, 0.0);
   for (int64_t i = 0; i < Np; ++i) pre[i + 1] = pre[i] + cost[i];
