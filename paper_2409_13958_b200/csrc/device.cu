@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include "device.cuh"
@@ -571,7 +572,8 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   {
     const size_t plane_bytes = (size_t)D.P[1] * D.P[2] * sizeof(float2);
     D.fused_tile = 0;
-    if (plane_bytes <= 200 * 1024) {
+    // PMFEM_FFT_SPLIT=1 forces the split plan (tests exercise it on small grids)
+    if (plane_bytes <= 200 * 1024 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {
       int tile = 1;
       while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && (D.H0 + 2 * tile - 1) / (2 * tile) >= 148) tile *= 2;
       D.fused_tile = tile;

@@ -36,7 +36,41 @@ __device__ void smem_fft(C* buf, int P, int logP, int nl, Base base, int es, con
   const int nb = P >> 1;
   const bool pow2_nl = (nl & (nl - 1)) == 0;
   const int lnl = __ffs(nl) - 1;
-  for (int s = 0; s < logP; ++s) {
+  // pairs of radix-2 stages (s, s+1) fused into one radix-4 pass: each thread loads 4
+  // elements, does both butterfly levels in registers -> half the syncs and smem traffic
+  int s = 0;
+  const int nq = P >> 2;
+  for (; s + 1 < logP; s += 2) {
+    const int h = 1 << s;
+    const int t1 = (nb >> s) * tw_stride;          // W_{2h}^j   = tw[j * t1]
+    const int t2 = (nb >> (s + 1)) * tw_stride;    // W_{4h}^j   = tw[j * t2]
+    for (int idx = threadIdx.x; idx < nl * nq; idx += blockDim.x) {
+      int l, b;
+      if (line_fast) {
+        if (pow2_nl) { l = idx & (nl - 1); b = idx >> lnl; } else { l = idx % nl; b = idx / nl; }
+      } else {
+        b = idx & (nq - 1); l = idx >> (logP - 2);
+      }
+      const int j = b & (h - 1);
+      const int i0 = ((b >> s) << (s + 2)) + j;
+      C w1 = tw[j * t1], w2a = tw[j * t2], w2b = tw[(j + h) * t2];
+      if (inv) { w1.y = -w1.y; w2a.y = -w2a.y; w2b.y = -w2b.y; }
+      C* p = buf + base(l) + i0 * es;
+      const int hs = h * es;
+      const C a0 = p[0], a1 = p[hs], a2 = p[2 * hs], a3 = p[3 * hs];
+      C t = cmul(w1, a1);
+      C b0, b1, b2, b3;
+      b0.x = a0.x + t.x; b0.y = a0.y + t.y; b1.x = a0.x - t.x; b1.y = a0.y - t.y;
+      t = cmul(w1, a3);
+      b2.x = a2.x + t.x; b2.y = a2.y + t.y; b3.x = a2.x - t.x; b3.y = a2.y - t.y;
+      t = cmul(w2a, b2);
+      p[0].x = b0.x + t.x; p[0].y = b0.y + t.y; p[2 * hs].x = b0.x - t.x; p[2 * hs].y = b0.y - t.y;
+      t = cmul(w2b, b3);
+      p[hs].x = b1.x + t.x; p[hs].y = b1.y + t.y; p[3 * hs].x = b1.x - t.x; p[3 * hs].y = b1.y - t.y;
+    }
+    __syncthreads();
+  }
+  for (; s < logP; ++s) {
     const int half = 1 << s;
     const int tstep = (nb >> s) * tw_stride;
     for (int idx = threadIdx.x; idx < nl * nb; idx += blockDim.x) {

@@ -114,3 +114,17 @@ def test_graph_replay(pair):
             out = np.zeros_like(m)
             out[rank] = H.double().cpu().numpy()
             assert rel_l2(out, om.heff(m, "aim")) <= TOL
+
+
+@pytest.mark.parametrize("key", ["C1r0", "C2p2", "C5p2"])
+def test_split_fft_plan(key, monkeypatch):
+    """The split FFT plan (Y, Z*G, Y' passes; used when a yz plane exceeds shared memory, e.g.
+    C4's 256^2) forced on small grids must give the same field as the oracle."""
+    monkeypatch.setenv("PMFEM_FFT_SPLIT", "1")
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    assert ctx.query()["fft_fused"] == 0
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=31)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
