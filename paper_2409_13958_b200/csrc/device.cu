@@ -720,7 +720,9 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   if (nrows <= 0) return;
   const unsigned thr_blocks = (unsigned)((nrows + 255) / 256);   // thread per row
   const unsigned warp_blocks = (unsigned)((nrows + 7) / 8);      // warp per row, 8 warps per block
-  auto mark = [&](int i) { if (D.timing) CK(cudaEventRecord(D.ev[i], st)); };
+  // external records: inside a captured graph a plain cudaEventRecord would only become an
+  // internal dependency, not a timestamp readable with cudaEventElapsedTime
+  auto mark = [&](int i) { if (D.timing) CK(cudaEventRecordWithFlags(D.ev[i], st, cudaEventRecordExternal)); };
   mark(0);
   k_to_m4<<<thr_blocks, 256, 0, st>>>(rr, m, D.m4);
   CK(cudaGetLastError());

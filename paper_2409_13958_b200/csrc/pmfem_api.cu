@@ -71,7 +71,11 @@ static pmfem_status setup_impl(pmfem_ctx* out, const pmfem_mesh* mesh, const pmf
     double t0 = now();
     static const bool verbose = std::getenv("PMFEM_VERBOSE") != nullptr;
     auto stage = [&](const char* what) {
-      if (verbose) { std::fprintf(stderr, "[pmfem] %-16s %8.2f s\n", what, now() - t0); std::fflush(stderr); }
+      if (verbose) {
+        std::fprintf(stderr, "[pmfem] %-16s %8.2f s  (cuda: %s)\n", what, now() - t0,
+                     cudaGetErrorString(cudaPeekAtLastError()));
+        std::fflush(stderr);
+      }
     };
     pmfem::HostSetup& S = ctx->S;
     pmfem::setup_mesh(S, mesh, per);
@@ -145,6 +149,11 @@ pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err) {
       pmfem::device_build_pgf(ctx->D, ctx->S, P);
     }
     ctx->S.pgf_seconds = now() - t0;
+    if (std::getenv("PMFEM_VERBOSE")) {
+      std::fprintf(stderr, "[pmfem] build_pgf        %8.2f s  (cuda: %s)\n", ctx->S.pgf_seconds,
+                   cudaGetErrorString(cudaPeekAtLastError()));
+      std::fflush(stderr);
+    }
   });
 }
 
@@ -379,7 +388,10 @@ pmfem_status pmfem_get_timing(pmfem_ctx ctx, float* ms) {
   if (!ctx || !ms) return PMFEM_E_INVALID_ARG;
   if (ctx->D.timing_pending) {
     cudaEventSynchronize(ctx->D.ev[5]);
-    for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&ctx->D.last_ms[i], ctx->D.ev[i], ctx->D.ev[i + 1]);
+    for (int i = 0; i < 5; ++i)
+      if (cudaEventElapsedTime(&ctx->D.last_ms[i], ctx->D.ev[i], ctx->D.ev[i + 1]) != cudaSuccess)
+        ctx->D.last_ms[i] = -1.f;
+    (void)cudaGetLastError();   // never leave a timing failure pending for the next evaluation
     ctx->D.timing_pending = false;
   }
   for (int i = 0; i < 8; ++i) ms[i] = ctx->D.last_ms[i];

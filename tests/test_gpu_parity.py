@@ -128,3 +128,21 @@ def test_split_fft_plan(key, monkeypatch):
     rank = ctx.internal_to_parent_rank()
     m = m_random(om.n_parents, seed=31)
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+
+
+def test_kernel_timing_in_graph(pair):
+    """Per-kernel timing events inside the captured graph are readable and leave no error."""
+    import torch
+    key, om, ctx = pair
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        m = torch.nn.functional.normalize(torch.randn(om.n_parents, 3, device="cuda:0"), dim=1).contiguous()
+        H = torch.empty_like(m)
+        ctx.set_timing(True)
+        for _ in range(3):
+            ctx.heff(m, H)
+            t = ctx.timing()
+            assert all(v > 0 for v in t.values()), t
+        ctx.set_timing(False)
+        ctx.heff(m, H)
+        s.synchronize()
