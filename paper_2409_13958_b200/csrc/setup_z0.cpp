@@ -15,6 +15,8 @@
 // on the GPU (z0_gpu.cu, one thread per (row, element image)) for device contexts.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <omp.h>
 #include "pmfem_internal.h"
 #include "z0_cone.cuh"
@@ -72,7 +74,9 @@ void setup_z0(HostSetup& S) {
   const bool on_device = S.z0_device >= 0;
   const int64_t chunk = on_device ? 400000 : Np;
   std::string err;
+  const bool verbose = std::getenv("PMFEM_VERBOSE") != nullptr;
   for (int64_t c0 = 0; c0 < Np && err.empty(); c0 += chunk) {
+    const double t_chunk = omp_get_wtime();
     const int64_t c1 = std::min(Np, c0 + chunk);
     std::vector<std::vector<Z0Item>> titems(omp_get_max_threads());
 #pragma omp parallel
@@ -217,7 +221,11 @@ void setup_z0(HostSetup& S) {
         }
       }
     }
+    const double t_enum = omp_get_wtime();
     if (on_device && err.empty()) z0_device_integrate(S, titems, rcol, rval, rules, c0, c1);
+    if (verbose)
+      std::fprintf(stderr, "[pmfem]   z0 rows %lld-%lld: enumerate %.2f s, integrate %.2f s\n", (long long)c0,
+                   (long long)c1, t_enum - t_chunk, omp_get_wtime() - t_enum);
   }
   require(err.empty(), PMFEM_E_MESH, err);
   // split diagonal (kept only in the row sum) from the off-diagonal entries
