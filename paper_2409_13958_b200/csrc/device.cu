@@ -163,83 +163,88 @@ struct GridDims { int n0, n1, n2; int per0, per1, per2; };
 __device__ __forceinline__ int wrapi(int i, int n, int per) { return per ? (i >= n ? i - n : i) : i; }
 
 // ------------------------------------------------------------------ K2 anterpolation
-// Gather form of the anterpolation (deterministic, no atomics, no memset): one thread per grid
-// point g sums w_n(g) q_n over the nodes whose stencil covers g.  Nodes are sorted by anchor
-// box (internal order), so the candidates are the node ranges of the (P+1)^3 anchor boxes
-// g - delta, read through box_ptr.  Rows outside [lo, hi) belong to other ranks (their
-// contributions arrive through the all-reduce of Q).
-template <int P>
-__device__ __forceinline__ float lagr1(float t, int d) {
-  float v = 1.f;
-#pragma unroll
-  for (int i = 0; i <= P; ++i)
-    if (i != d) v *= (t - (float)i) / (float)(d - i);
-  return v;
-}
+// Particle-to-grid scatter staged in shared memory: a CTA takes 256 consecutive (box-sorted)
+// nodes, whose stencils cover a compact block of the grid -- one x-row range when the chunk
+// stays in one (y, z) row, one z-plane band otherwise -- accumulates the (P+1)^3 weighted
+// charges there with shared-memory atomics and flushes the non-zero block points with one
+// global atomic each (2.5-6x fewer global atomics than a direct scatter).  Chunks spanning
+// several z planes fall back to direct global atomics.  Q must be zeroed first; rows outside
+// [lo, hi) belong to other ranks (their contributions arrive through the all-reduce of Q).
+constexpr int P2G_CAP = 12288;   // floats of staged grid block (48 KB)
 
 template <int P>
-__global__ void __launch_bounds__(256) k2_gather(GridDims g, const int32_t* __restrict__ box_ptr,
-                                                 const float4* __restrict__ st_t, const float* __restrict__ q,
-                                                 int64_t lo, int64_t hi, float* __restrict__ Q) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t G = (int64_t)g.n0 * g.n1 * g.n2;
-  if (gid >= G) return;
-  const int gx = (int)(gid % g.n0), gy = (int)((gid / g.n0) % g.n1), gz = (int)(gid / ((int64_t)g.n0 * g.n1));
-  float acc = 0.f;
+__global__ void __launch_bounds__(256) k2_p2g(RowRange rr, const float* __restrict__ q, const int4* __restrict__ st_s,
+                                              const float4* __restrict__ st_t, GridDims g, float* __restrict__ Q) {
+  __shared__ float blk[P2G_CAP];
+  const int64_t c0 = rr.row0 + (int64_t)blockIdx.x * blockDim.x;
+  const int64_t c1 = min(c0 + (int64_t)blockDim.x, rr.row1) - 1;
+  const int64_t n = c0 + threadIdx.x;
+  const bool valid = n <= c1;
+  const int4 sa = st_s[c0], sb = st_s[c1];
+  // block extents in unwrapped stencil indices
+  int z0 = sa.z, nz = sb.z - sa.z + P + 1, y0, ny, x0, nx;
+  if (sa.z == sb.z && sa.y == sb.y) { y0 = sa.y; ny = P + 1; x0 = sa.x; nx = sb.x - sa.x + P + 1; }
+  else if (sa.z == sb.z) { y0 = sa.y; ny = sb.y - sa.y + P + 1; x0 = 0; nx = g.n0; }
+  else { y0 = 0; ny = 0; x0 = 0; nx = 0; }
+  const bool staged = ny > 0 && (int64_t)nz * ny * nx <= P2G_CAP;
+  const int tot = staged ? nz * ny * nx : 0;
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) blk[t] = 0.f;
+  __syncthreads();
+  if (valid) {
+    const int4 s = st_s[n];
+    const float4 t = st_t[n];
+    const float qn = q[n];
+    float wx[P + 1], wy[P + 1], wz[P + 1];
+    lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
 #pragma unroll
-  for (int dz = 0; dz <= P; ++dz) {
-    int sz = gz - dz;
-    if (g.per2) { if (sz < 0) sz += g.n2; } else if (sz < 0 || sz > g.n2 - 1 - P) continue;
+    for (int k = 0; k <= P; ++k) {
 #pragma unroll
-    for (int dy = 0; dy <= P; ++dy) {
-      int sy = gy - dy;
-      if (g.per1) { if (sy < 0) sy += g.n1; } else if (sy < 0 || sy > g.n1 - 1 - P) continue;
-      // the anchor boxes gx-P..gx of one (sz, sy) line are consecutive in the box-sorted row
-      // order (x fastest): one contiguous node range (two when a periodic x wraps)
-      const int64_t line = ((int64_t)sz * g.n1 + sy) * g.n0;
-      int xr[2][2], nr = 0;
-      if (g.per0) {
-        if (gx - P >= 0) { xr[0][0] = gx - P; xr[0][1] = gx; nr = 1; }
-        else { xr[0][0] = 0; xr[0][1] = gx; xr[1][0] = g.n0 + gx - P; xr[1][1] = g.n0 - 1; nr = 2; }
-      } else {
-        const int a = max(gx - P, 0), b = min(gx, g.n0 - 1 - P);
-        if (a <= b) { xr[0][0] = a; xr[0][1] = b; nr = 1; }
-      }
-      const float wyz = 1.f;
-      for (int r = 0; r < nr; ++r) {
-        const int64_t i0 = max((int64_t)__ldg(box_ptr + line + xr[r][0]), lo);
-        const int64_t i1 = min((int64_t)__ldg(box_ptr + line + xr[r][1] + 1), hi);
-        for (int64_t i = i0; i < i1; ++i) {
-          const float4 t = __ldg(st_t + i);
-          int dx = gx - __float_as_int(t.w);        // wrapped anchor x is stored in t.w
-          if (dx < 0) dx += g.n0;
-          float wx[P + 1];
-          lagr<P>(t.x, wx);
-          float w = wx[0];
+      for (int j = 0; j <= P; ++j) {
+        const float wzy = qn * wz[k] * wy[j];
+        if (staged) {
+          float* row = blk + ((s.z + k - z0) * ny + (s.y + j - y0)) * nx;
 #pragma unroll
-          for (int k = 1; k <= P; ++k) w = (dx == k) ? wx[k] : w;
-          acc = fmaf(w * wyz * lagr1<P>(t.y, dy) * lagr1<P>(t.z, dz), __ldg(q + i), acc);
+          for (int i = 0; i <= P; ++i) {
+            int ix = s.x + i - x0;
+            if (nx == g.n0 && ix >= g.n0) ix -= g.n0;          // full-width rows wrap in place
+            atomicAdd(row + ix, wzy * wx[i]);
+          }
+        } else {
+          const int iz = wrapi(s.z + k, g.n2, g.per2), iy = wrapi(s.y + j, g.n1, g.per1);
+          float* row = Q + ((int64_t)iz * g.n1 + iy) * g.n0;
+#pragma unroll
+          for (int i = 0; i <= P; ++i) atomicAdd(row + wrapi(s.x + i, g.n0, g.per0), wzy * wx[i]);
         }
       }
     }
   }
-  Q[gid] = acc;
+  if (!staged) return;
+  __syncthreads();
+  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
+    const float v = blk[t];
+    if (v == 0.f) continue;
+    const int ix = t % nx, r = t / nx, iy = r % ny, iz = r / ny;
+    const int gx = wrapi(x0 + ix, g.n0, g.per0), gy = wrapi(y0 + iy, g.n1, g.per1), gz = wrapi(z0 + iz, g.n2, g.per2);
+    atomicAdd(Q + ((int64_t)gz * g.n1 + gy) * g.n0 + gx, v);
+  }
 }
 
 // ------------------------------------------------------------------ K4 interpolation + precorrection
-template <int P>
+// G lanes per row (8, 16 or 32, chosen from the mean C_box row length so every lane has
+// several 16-byte loads in flight); the (P+1)^3 grid gathers are spread over the same lanes.
+template <int P, int G>
 __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
                                                       const float4* __restrict__ st_t, GridDims g,
                                                       const int64_t* __restrict__ c_ptr, const int4* __restrict__ c_col4,
                                                       const float4* __restrict__ c_val4, const float* __restrict__ q,
                                                       const float* __restrict__ uloc, float* __restrict__ u) {
-  const int lane = threadIdx.x & 31;
-  const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (n >= rr.row1) return;
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
+  const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
-  const int64_t b = c_ptr[n] >> 2, e_end = c_ptr[n + 1] >> 2;
+  const int64_t b = valid ? c_ptr[n] >> 2 : 0, e_end = valid ? c_ptr[n + 1] >> 2 : 0;
 #pragma unroll 2
-  for (int64_t e = b + lane; e < e_end; e += 32) {
+  for (int64_t e = b + lane; e < e_end; e += G) {
     const int4 cc = __ldg(c_col4 + e);
     const float4 vv = __ldg(c_val4 + e);
     acc = fmaf(vv.x, q[cc.x], acc);
@@ -248,12 +253,12 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     acc = fmaf(vv.w, q[cc.w], acc);
   }
   constexpr int NS = (P + 1) * (P + 1) * (P + 1);
-  if (lane < NS) {
+  if (valid && lane < NS) {
     const int4 s = st_s[n];
     const float4 t = st_t[n];
     float wx[P + 1], wy[P + 1], wz[P + 1];
     lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
-    for (int k = lane; k < NS; k += 32) {
+    for (int k = lane; k < NS; k += G) {
       const int i = k % (P + 1), j = (k / (P + 1)) % (P + 1), l = k / ((P + 1) * (P + 1));
       const int ix = wrapi(s.x + i, g.n0, g.per0), iy = wrapi(s.y + j, g.n1, g.per1), iz = wrapi(s.z + l, g.n2, g.per2);
       float wi = 0, wj = 0, wl = 0;
@@ -263,8 +268,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) u[n] = acc + uloc[n];
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (valid && lane == 0) u[n] = acc + uloc[n];
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
@@ -542,21 +547,11 @@ void device_upload(DeviceState& D, const HostSetup& S) {
                          __int_as_float_host(s[0]));
   }
   D.rowsum = dupload(rsum); D.st_s = dupload(sts); D.st_t = dupload(stt);
-  {
-    // anchor-box row pointers (internal rows are sorted by the anchor key, x fastest)
-    const int64_t Gb = (int64_t)D.n[0] * D.n[1] * D.n[2];
-    std::vector<int32_t> bp(Gb + 1, 0);
-    for (int64_t i = 0; i < Np; ++i) {
-      const int64_t key = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
-      bp[key + 1]++;
-    }
-    for (int64_t b = 0; b < Gb; ++b) bp[b + 1] += bp[b];
-    for (int64_t i = 1; i < Np; ++i) {
-      const int64_t k0 = ((int64_t)sts[i - 1].z * D.n[1] + sts[i - 1].y) * D.n[0] + sts[i - 1].x;
-      const int64_t k1 = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
-      if (k1 < k0) throw Error(PMFEM_E_STATE, "internal rows are not sorted by anchor box");
-    }
-    D.box_ptr = dupload(bp);
+  // K2 stages chunks of consecutive rows: the rows must be sorted by anchor box (x fastest)
+  for (int64_t i = 1; i < Np; ++i) {
+    const int64_t k0 = ((int64_t)sts[i - 1].z * D.n[1] + sts[i - 1].y) * D.n[0] + sts[i - 1].x;
+    const int64_t k1 = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
+    if (k1 < k0) throw Error(PMFEM_E_STATE, "internal rows are not sorted by anchor box");
   }
   for (int a = 0; a < 3; ++a) {
     std::vector<float2> t32; std::vector<double2> t64;
@@ -602,6 +597,15 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     }
   }
   const int64_t cnnz = D.cbox_nnz;
+  {
+    // K4 group size: ~4+ int4 loads per lane; PMFEM_K4_GROUP overrides (tests)
+    const double row4 = (double)cnnz / std::max<int64_t>(Np, 1) / 4.0;
+    D.k4_group = row4 >= 96 ? 32 : (row4 >= 40 ? 16 : 8);
+    if (const char* e = std::getenv("PMFEM_K4_GROUP")) {
+      const int gsel = std::atoi(e);
+      if (gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
+    }
+  }
   D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 8 + G * 4.0;
   D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
@@ -640,7 +644,7 @@ void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
   void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_col, D.c_val,
-                  D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
+                  D.st_s, D.st_t, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
                   D.send_buf, D.recv_buf, D.send_idx[0], D.send_idx[1], D.send_idx[2],
                   D.recv_idx[0], D.recv_idx[1], D.recv_idx[2]};
@@ -719,7 +723,6 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   const int64_t nrows = D.hi - D.lo;
   if (nrows <= 0) return;
   const unsigned thr_blocks = (unsigned)((nrows + 255) / 256);   // thread per row
-  const unsigned warp_blocks = (unsigned)((nrows + 7) / 8);      // warp per row, 8 warps per block
   // external records: inside a captured graph a plain cudaEventRecord would only become an
   // internal dependency, not a timestamp readable with cudaEventElapsedTime
   auto mark = [&](int i) { if (D.timing) CK(cudaEventRecordWithFlags(D.ev[i], st, cudaEventRecordExternal)); };
@@ -739,11 +742,11 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   CK(cudaGetLastError());
   mark(1);
   const size_t G = (size_t)D.n[0] * D.n[1] * D.n[2];
-  const unsigned grid_blocks = (unsigned)((G + 255) / 256);
+  CK(cudaMemsetAsync(D.Q, 0, sizeof(float) * G, st));
   switch (D.order) {
-    case 1: k2_gather<1><<<grid_blocks, 256, 0, st>>>(g, D.box_ptr, D.st_t, D.q, D.lo, D.hi, D.Q); break;
-    case 2: k2_gather<2><<<grid_blocks, 256, 0, st>>>(g, D.box_ptr, D.st_t, D.q, D.lo, D.hi, D.Q); break;
-    default: k2_gather<3><<<grid_blocks, 256, 0, st>>>(g, D.box_ptr, D.st_t, D.q, D.lo, D.hi, D.Q); break;
+    case 1: k2_p2g<1><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
+    case 2: k2_p2g<2><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
+    default: k2_p2g<3><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
   }
   CK(cudaGetLastError());
   if (D.world > 1) NCK(ncclAllReduce(D.Q, D.Q, G, ncclFloat, ncclSum, (ncclComm_t)D.comm, st));
@@ -766,9 +769,16 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   const int4* c4 = reinterpret_cast<const int4*>(D.c_col);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   switch (D.order) {
-    case 1: k4_interp_corr<1><<<warp_blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
-    case 2: k4_interp_corr<2><<<warp_blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
-    default: k4_interp_corr<3><<<warp_blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, c4, v4, D.q, D.uloc, D.u); break;
+#define K4_LAUNCH(PP, GG)                                                                               \
+  k4_interp_corr<PP, GG><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, \
+                                                                             c4, v4, D.q, D.uloc, D.u)
+#define K4_BY_G(PP)                                                                                     \
+  (D.k4_group == 8 ? K4_LAUNCH(PP, 8) : D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
+    case 1: K4_BY_G(1); break;
+    case 2: K4_BY_G(2); break;
+    default: K4_BY_G(3); break;
+#undef K4_BY_G
+#undef K4_LAUNCH
   }
   CK(cudaGetLastError());
   halo(D, 2, D.u, 1, st);

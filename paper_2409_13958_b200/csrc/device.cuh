@@ -29,9 +29,10 @@ struct DeviceState {
   int64_t* c_ptr = nullptr;   int32_t* c_col = nullptr;
   float* c_val = nullptr;
   int64_t cbox_nnz = 0;       // unpadded entries
+  int k4_group = 32;          // lanes per row in K4 (8/16/32 from the mean padded row length)
   // stencils
   int4* st_s = nullptr;       // wrapped (periodic) / clamped anchors
-  int32_t* box_ptr = nullptr; // [G+1] first internal row of each anchor box (rows are box-sorted)
+
   float4* st_t = nullptr;     // local coordinates t - s
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32
   float* spec = nullptr;

@@ -146,3 +146,16 @@ def test_kernel_timing_in_graph(pair):
         ctx.set_timing(False)
         ctx.heff(m, H)
         s.synchronize()
+
+
+@pytest.mark.parametrize("group", ["8", "16", "32"])
+def test_k4_group_sizes(group, monkeypatch):
+    """K4 with 8, 16 or 32 lanes per row (chosen by the mean C_box row length) gives the same field."""
+    monkeypatch.setenv("PMFEM_K4_GROUP", group)
+    key = "C2p2"
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=41)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
