@@ -405,7 +405,7 @@ void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows
 
 void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
   const int tile = D.fused_tile, P1 = D.P[1], P2 = D.P[2];
-  size_t smem = (size_t)P1 * P2 * tile * sizeof(float2);
+  size_t smem = (size_t)P2 * (P1 * tile + (tile == 1 ? 1 : 0)) * sizeof(float2);   // padded planes
   auto kern = fft_yz_fused<float>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int threads = std::min(512, std::max(128, P1 * P2 * tile / 4));
@@ -565,7 +565,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   for (int i = 0; i < 8; ++i) CK(cudaEventCreate(&D.ev[i]));
   // FFT plan: fused YZ when a yz plane of `tile` columns fits in shared memory
   {
-    const size_t plane_bytes = (size_t)D.P[1] * D.P[2] * sizeof(float2);
+    const size_t plane_bytes = (size_t)(D.P[1] + 1) * D.P[2] * sizeof(float2);
     D.fused_tile = 0;
     // PMFEM_FFT_SPLIT=1 forces the split plan (tests exercise it on small grids)
     if (plane_bytes <= 200 * 1024 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {

@@ -257,44 +257,46 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   C* buf = reinterpret_cast<C*>(smem_raw);
   const int c0 = blockIdx.x * tile;
   const int nc = min(tile, H0 - c0);
-  const int plane = P1 * tile;
+  // plane stride padded by one element when tile == 1: consecutive threads then take
+  // consecutive y lines (line-fast) at a stride of P1+1 elements -> no bank conflicts
+  const int nzl = P1 * tile;                                  // z lines per CTA
+  const int pl = nzl + (tile == 1 ? 1 : 0);                   // plane stride in smem
   const int ltile = __ffs(tile) - 1, ln1 = __ffs(n1) - 1;     // tile, n1 powers of two
   // zero the whole tile (padded planes / rows must read as zero), then load the data block
-  for (int idx = threadIdx.x; idx < P2 * plane; idx += blockDim.x) { C z; z.x = T(0); z.y = T(0); buf[idx] = z; }
+  for (int idx = threadIdx.x; idx < P2 * pl; idx += blockDim.x) { C z; z.x = T(0); z.y = T(0); buf[idx] = z; }
   __syncthreads();
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
     const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
     if (c < nc)
-      buf[bitrev(i2, logP2) * plane + bitrev(i1, logP1) * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
+      buf[bitrev(i2, logP2) * pl + bitrev(i1, logP1) * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
   }
   __syncthreads();
-  // forward y on the n2 data planes: line (i2, c) base = bitrev(i2)*plane + c, stride tile
-  const PlaneBase ybase{tile, plane, logP2};
-  // line-fast only when lines are adjacent in smem (tile > 1); with tile == 1 the y lines are
-  // contiguous rows and butterfly-fast ordering avoids plane-stride bank conflicts
-  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, tile > 1);
-  // forward z on every (k1, c): base = k1*tile + c, stride plane
+  // forward y on the n2 data planes: line (i2, c) base = bitrev(i2)*pl + c, stride tile
+  const PlaneBase ybase{tile, pl, logP2};
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, true);
+  // forward z on every (k1, c): base = k1*tile + c, stride pl
   const TileBase zbase{};
-  smem_fft<C>(buf, P2, logP2, plane, zbase, plane, tw2, 1, false, true);
+  smem_fft<C>(buf, P2, logP2, nzl, zbase, pl, tw2, 1, false, true);
   // multiply by the real spectrum G_hat[k2][k1][k0] (natural order now)
-  for (int idx = threadIdx.x; idx < P2 * plane; idx += blockDim.x) {
+  for (int idx = threadIdx.x; idx < P2 * nzl; idx += blockDim.x) {
     const int c = idx & (tile - 1), r = idx >> ltile, k1 = r & (P1 - 1), k2 = r >> logP1;
     const T g = (c < nc) ? spec[((long long)k2 * P1 + k1) * H0 + c0 + c] : T(0);
-    C v = buf[idx];
+    C* pv = buf + k2 * pl + k1 * tile + c;
+    C v = *pv;
     v.x *= g; v.y *= g;
-    buf[idx] = v;
+    *pv = v;
   }
   __syncthreads();
   // inverse z (bit-reverse first); only planes i2 < n2 are needed afterwards
-  smem_bitrev<C>(buf, P2, logP2, plane, zbase, plane);
-  smem_fft<C>(buf, P2, logP2, plane, zbase, plane, tw2, 1, true, true);
+  smem_bitrev<C>(buf, P2, logP2, nzl, zbase, pl);
+  smem_fft<C>(buf, P2, logP2, nzl, zbase, pl, tw2, 1, true, true);
   // inverse y on planes i2 < n2 (natural z order now)
-  const PlaneBase ybase2{tile, plane, 0};
+  const PlaneBase ybase2{tile, pl, 0};
   smem_bitrev<C>(buf, P1, logP1, n2 * tile, ybase2, tile);
-  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, tile > 1);
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, true);
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
     const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
-    if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * plane + i1 * tile + c];
+    if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * pl + i1 * tile + c];
   }
 }
 
