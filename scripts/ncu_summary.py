@@ -78,12 +78,15 @@ def main():
         agg = OrderedDict()
         for n, t in L:
             agg.setdefault(n, []).append(t)
-        tot = sum(sum(v) for k, v in agg.items() if not k.startswith(("void at::", "at::")))
+        def is_eval(k):   # per-evaluation kernels (setup kernels and torch's own are excluded)
+            return not k.startswith(("void at::", "at::", "k_z0", "k_cbox", "k_pgf", "k_spec")) \
+                and "<double" not in k
+        tot = sum(sum(v) for k, v in agg.items() if is_eval(k))
         print("## Launch list (ncu gpu__time_duration.sum, cold-cache, serialised)\n")
-        print("| kernel | launches | mean us | share of pmfem time |")
+        print("| kernel | launches | mean us | share of one evaluation |")
         print("|---|---|---|---|")
         for k, v in agg.items():
-            share = sum(v) / tot if not k.startswith(("void at::", "at::")) else 0
+            share = sum(v) / tot if is_eval(k) else 0
             print("| %s | %d | %.2f | %.1f%% |" % (k, len(v), sum(v) / len(v), 100 * share))
         print()
     if a.rep:
