@@ -91,6 +91,9 @@ typedef struct {
   int32_t launches_per_eval;                      /* library kernels launched by one pmfem_heff   */
   int32_t fft_fused;                              /* 1: fused YZ FFT plan, 0: split plan          */
   double  comm_bytes_per_eval;                    /* bytes this rank sends+receives per evaluation */
+  int32_t k2_tile[3];                             /* K2 anterpolation grid tile (points per axis) */
+  int32_t slab_world;                             /* > 1: slab-decomposed FFT over this many ranks
+                                                     (SURVEY 8(e)); 1: FFT on the full grid      */
 } pmfem_info;
 
 /* Build a context: validate, orient, detect T-PBC pairs and fold them to LCAs,

@@ -5,8 +5,9 @@
 //   entry    : G0*(d) - sum_{a in st(n), b in st(k)} w_na w_kb G0*((a - b - img N) o Delta)
 // The host computes the same thing in setup_aim.cpp (used by host-only contexts and as the
 // reference of the GPU test); device contexts build C_box here in seconds instead of minutes.
-// Pass 1 counts the near pairs of every row, the host scans (rows padded to a multiple of 4
-// for K4's 16-byte loads), pass 2 writes columns and values.
+// Pass 1 counts the near pairs of every row, the host scans, pass 2 writes columns (in
+// increasing order, by construction) and values; the rows are then packed into the C4x
+// chunk format K4 streams (6 bytes per entry instead of 8 for a column + value CSR).
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -27,15 +28,8 @@ struct CboxGeom {
   int per[3];
   int n[3];
   int p;
-  double L[3], delta[3], rer;
-  long long nb[3];       // boxes per axis (box edge >= r_ER)
-  double blo[3], bs[3];  // box origin and edge per axis
+  double L[3], delta[3], origin[3], rer;
 };
-
-__device__ __forceinline__ long long box_of(const CboxGeom& c, double x, int a) {
-  long long b = (long long)floor((x - c.blo[a]) / c.bs[a]);
-  return b < 0 ? 0 : (b >= c.nb[a] ? c.nb[a] - 1 : b);
-}
 
 __device__ __forceinline__ void lagr_d(double t, int p, double* w) {
   for (int j = 0; j <= p; ++j) {
@@ -46,56 +40,72 @@ __device__ __forceinline__ void lagr_d(double t, int p, double* w) {
   }
 }
 
-// visit every near pair (k, img) of row n; distinct neighbour boxes (periodic axes with fewer
-// than 3 boxes visit each box once)
-template <class F>
-__device__ void for_near(const CboxGeom& c, const double* __restrict__ xw, const long long* __restrict__ bptr,
-                         const int* __restrict__ bnode, long long n, F&& f) {
-  const double xn[3] = {xw[3 * n], xw[3 * n + 1], xw[3 * n + 2]};
-  long long bn[3];
-  int lo[3], hi[3];
-  for (int a = 0; a < 3; ++a) {
-    bn[a] = box_of(c, xn[a], a);
-    if (c.per[a] && c.nb[a] < 3) { lo[a] = 0; hi[a] = (int)c.nb[a] - 1; bn[a] = 0; }
-    else { lo[a] = -1; hi[a] = 1; }
-  }
-  for (int dx = lo[0]; dx <= hi[0]; ++dx)
-    for (int dy = lo[1]; dy <= hi[1]; ++dy)
-      for (int dz = lo[2]; dz <= hi[2]; ++dz) {
-        long long bb[3] = {bn[0] + dx, bn[1] + dy, bn[2] + dz};
-        bool ok = true;
-        for (int a = 0; a < 3; ++a) {
-          if (c.per[a]) bb[a] = ((bb[a] % c.nb[a]) + c.nb[a]) % c.nb[a];
-          else ok &= (bb[a] >= 0 && bb[a] < c.nb[a]);
-        }
-        if (!ok) continue;
-        const long long b = (bb[0] * c.nb[1] + bb[1]) * c.nb[2] + bb[2];
-        for (long long i = bptr[b]; i < bptr[b + 1]; ++i) {
-          const int k = bnode[i];
-          double d[3];
-          int img[3] = {0, 0, 0};
-          bool in = true;
-          for (int a = 0; a < 3; ++a) {
-            d[a] = xn[a] - xw[3 * (long long)k + a];
-            if (c.per[a]) { img[a] = (int)rint(d[a] / c.L[a]); d[a] -= img[a] * c.L[a]; }
-            in &= fabs(d[a]) <= c.rer;
-          }
-          if (in) f(k, d, img);
-        }
-      }
+// unclamped, unwrapped stencil anchor of coordinate x on axis a (contract K5)
+__device__ __forceinline__ int anchor_of(const CboxGeom& c, double x, int a) {
+  const double t = (x - c.origin[a]) / c.delta[a];
+  return (c.p & 1) ? (int)floor(t) - (c.p - 1) / 2 : (int)floor(t + 0.5) - c.p / 2;
 }
 
-__global__ void k_cbox_count(CboxGeom c, long long Np, const double* __restrict__ xw, const long long* __restrict__ bptr,
-                             const int* __restrict__ bnode, int* __restrict__ cnt) {
+// Distinct stored anchors (wrapped on periodic axes, clamped otherwise) of every node whose
+// coordinate can lie within r_ER of x on axis a, as up to two increasing ranges.  The margin
+// of one anchor on each side covers the rounding of (x + img L) / Delta.
+__device__ int cand_ranges(const CboxGeom& c, double x, int a, int* r) {
+  int lo = anchor_of(c, x - c.rer, a) - 1, hi = anchor_of(c, x + c.rer, a) + 1;
+  const int N = c.n[a];
+  if (!c.per[a]) {
+    lo = max(lo, 0); hi = min(hi, N - 1 - c.p);
+    if (lo > hi) return 0;
+    r[0] = lo; r[1] = hi; return 1;
+  }
+  if (hi - lo + 1 >= N) { r[0] = 0; r[1] = N - 1; return 1; }
+  const int wl = ((lo % N) + N) % N, wh = ((hi % N) + N) % N;
+  if (wl <= wh) { r[0] = wl; r[1] = wh; return 1; }
+  r[0] = 0; r[1] = wh; r[2] = wl; r[3] = N - 1; return 2;
+}
+
+// Visit every near pair (k, img) of row n in increasing internal column order: internal rows
+// are sorted by stored anchor box (x fastest) and box_ptr gives each box's row range, so
+// candidate anchor lines (z, then y increasing) with their x ranges (increasing) enumerate
+// the candidates in column order; the exact near test (K8) then selects the pairs.
+template <class F>
+__device__ void for_near(const CboxGeom& c, const double* __restrict__ xw, const int* __restrict__ box_ptr,
+                         long long n, F&& f) {
+  const double xn[3] = {xw[3 * n], xw[3 * n + 1], xw[3 * n + 2]};
+  int rx[4], ry[4], rz[4];
+  const int nx = cand_ranges(c, xn[0], 0, rx), ny = cand_ranges(c, xn[1], 1, ry), nz = cand_ranges(c, xn[2], 2, rz);
+  for (int iz = 0; iz < nz; ++iz)
+    for (int z = rz[2 * iz]; z <= rz[2 * iz + 1]; ++z)
+      for (int iy = 0; iy < ny; ++iy)
+        for (int y = ry[2 * iy]; y <= ry[2 * iy + 1]; ++y) {
+          const long long line = ((long long)z * c.n[1] + y) * c.n[0];
+          for (int ix = 0; ix < nx; ++ix) {
+            const int k0 = box_ptr[line + rx[2 * ix]], k1 = box_ptr[line + rx[2 * ix + 1] + 1];
+            for (int k = k0; k < k1; ++k) {
+              double d[3];
+              int img[3] = {0, 0, 0};
+              bool in = true;
+              for (int a = 0; a < 3; ++a) {
+                d[a] = xn[a] - xw[3 * (long long)k + a];
+                if (c.per[a]) { img[a] = (int)rint(d[a] / c.L[a]); d[a] -= img[a] * c.L[a]; }
+                in &= fabs(d[a]) <= c.rer;
+              }
+              if (in) f(k, d, img);
+            }
+          }
+        }
+}
+
+__global__ void k_cbox_count(CboxGeom c, long long Np, const double* __restrict__ xw, const int* __restrict__ box_ptr,
+                             int* __restrict__ cnt) {
   const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= Np) return;
   int k_cnt = 0;
-  for_near(c, xw, bptr, bnode, n, [&](int, const double*, const int*) { ++k_cnt; });
+  for_near(c, xw, box_ptr, n, [&](int, const double*, const int*) { ++k_cnt; });
   cnt[n] = k_cnt;
 }
 
-__global__ void k_cbox_fill(CboxGeom c, long long Np, const double* __restrict__ xw, const long long* __restrict__ bptr,
-                            const int* __restrict__ bnode, const int* __restrict__ s_unw, const double* __restrict__ t_loc,
+__global__ void k_cbox_fill(CboxGeom c, long long Np, const double* __restrict__ xw, const int* __restrict__ box_ptr,
+                            const int* __restrict__ s_unw, const double* __restrict__ t_loc,
                             const long long* __restrict__ rowptr, int* __restrict__ col, float* __restrict__ val) {
   const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= Np) return;
@@ -103,7 +113,7 @@ __global__ void k_cbox_fill(CboxGeom c, long long Np, const double* __restrict__
   double wn[3][4];
   for (int a = 0; a < 3; ++a) lagr_d(t_loc[3 * n + a], p, wn[a]);
   long long o = rowptr[n];
-  for_near(c, xw, bptr, bnode, n, [&](int k, const double* d, const int* img) {
+  for_near(c, xw, box_ptr, n, [&](int k, const double* d, const int* img) {
     const double r = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
     double v = r > 0 ? 1.0 / r : 0.0;
     double wk[3][4], cw[3][7];
@@ -132,7 +142,49 @@ __global__ void k_cbox_fill(CboxGeom c, long long Np, const double* __restrict__
     val[o] = (float)(v - gm);
     ++o;
   });
-  for (; o < rowptr[n + 1]; ++o) { col[o] = (int)n; val[o] = 0.f; }   // padding to 4
+}
+
+// ---- C4x: chunks of 4 consecutive entries of a (column-sorted) row, per chunk a float4 of
+// values and a 64-bit header = base column (28 bits) + three 12-bit column deltas.  A delta
+// above 4095 (a jump to the next anchor plane) closes the chunk early; unused slots repeat
+// the previous column (delta 0) with value 0, so every gathered q is one of the row's own.
+constexpr int C4X_DBITS = 12;
+constexpr long long C4X_DMAX = (1 << C4X_DBITS) - 1;
+
+__global__ void k_c4x_count(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                            long long* __restrict__ nch) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long chunks = 0;
+  int pos = 4, prev = 0;
+  for (long long e = rowptr[n]; e < rowptr[n + 1]; ++e) {
+    const int k = col[e];
+    if (pos == 4 || k - prev > C4X_DMAX) { ++chunks; pos = 0; }
+    ++pos; prev = k;
+  }
+  nch[n] = chunks;
+}
+
+__global__ void k_c4x_fill(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                           const float* __restrict__ val, const long long* __restrict__ cptr,
+                           unsigned long long* __restrict__ hdr, float* __restrict__ cval) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long ch = cptr[n] - 1;
+  int pos = 4, prev = 0;
+  unsigned long long h = 0;
+  for (long long e = rowptr[n]; e < rowptr[n + 1]; ++e) {
+    const int k = col[e];
+    if (pos == 4 || k - prev > C4X_DMAX) {
+      if (ch >= cptr[n]) { for (; pos < 4; ++pos) cval[4 * ch + pos] = 0.f; hdr[ch] = h; }
+      ++ch; pos = 0; h = (unsigned long long)k;
+    } else {
+      h |= (unsigned long long)(k - prev) << (28 + C4X_DBITS * (pos - 1));
+    }
+    cval[4 * ch + pos] = val[e];
+    ++pos; prev = k;
+  }
+  if (ch >= cptr[n]) { for (; pos < 4; ++pos) cval[4 * ch + pos] = 0.f; hdr[ch] = h; }
 }
 
 template <class T>
@@ -152,16 +204,17 @@ T* dup_c(const std::vector<T>& v) {
 
 }  // namespace
 
-// Builds D.c_ptr / D.c_col / D.c_val (internal order) on the device.  Returns the number of
-// (unpadded) entries.
+// Builds the C4x arrays D.c_ptr (chunk offsets) / D.c_hdr / D.c_val in internal order on the
+// device.  Needs D.box_ptr (anchor-box row pointers of the internal order).  Returns the number
+// of near pairs.
 int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   CKC(cudaSetDevice(D.device));
   const int64_t Np = S.Np;
+  if (Np >= (int64_t(1) << 28)) throw Error(PMFEM_E_INVALID_ARG, "C4x column base holds 28 bits: N' < 2^28 required");
   const int p = S.order;
-  const double rer = S.rer_scale * std::max(S.delta[0], std::max(S.delta[1], S.delta[2]));
   CboxGeom c{};
   c.p = p;
-  c.rer = rer;
+  c.rer = S.rer_scale * std::max(S.delta[0], std::max(S.delta[1], S.delta[2]));
   std::vector<double> xw(3 * Np), tl(3 * Np);
   std::vector<int> su(3 * Np);
   for (int64_t i = 0; i < Np; ++i) {
@@ -177,54 +230,45 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
     c.n[a] = S.grid_n[a];
     c.L[a] = S.L[a];
     c.delta[a] = S.delta[a];
-    double lo = 1e300, hi = -1e300;
-    for (int64_t i = 0; i < Np; ++i) { lo = std::min(lo, xw[3 * i + a]); hi = std::max(hi, xw[3 * i + a]); }
-    if (S.periodic[a]) { c.blo[a] = 0; c.nb[a] = std::max<long long>(1, (long long)std::floor(S.L[a] / rer)); c.bs[a] = S.L[a] / c.nb[a]; }
-    else { c.blo[a] = lo; c.nb[a] = (long long)std::floor((hi - lo) / rer) + 1; c.bs[a] = rer; }
-  }
-  // box lists (same box rule as the host's setup_aim)
-  const long long nbox = c.nb[0] * c.nb[1] * c.nb[2];
-  std::vector<long long> key(Np), bptr(nbox + 1, 0);
-  for (int64_t i = 0; i < Np; ++i) {
-    long long bb[3];
-    for (int a = 0; a < 3; ++a) {
-      long long b = (long long)std::floor((xw[3 * i + a] - c.blo[a]) / c.bs[a]);
-      bb[a] = std::min<long long>(std::max<long long>(b, 0), c.nb[a] - 1);
-    }
-    key[i] = (bb[0] * c.nb[1] + bb[1]) * c.nb[2] + bb[2];
-    bptr[key[i] + 1]++;
-  }
-  for (long long b = 0; b < nbox; ++b) bptr[b + 1] += bptr[b];
-  std::vector<int> bnode(Np);
-  {
-    std::vector<long long> fill(bptr.begin(), bptr.end() - 1);
-    for (int64_t i = 0; i < Np; ++i) bnode[fill[key[i]]++] = (int)i;
+    c.origin[a] = S.origin[a];
   }
   double* d_xw = dup_c(xw);
   double* d_tl = dup_c(tl);
   int* d_su = dup_c(su);
-  long long* d_bptr = dup_c(bptr);
-  int* d_bnode = dup_c(bnode);
   int* d_cnt = dalloc_c<int>(Np);
   const unsigned blocks = (unsigned)((Np + 127) / 128);
-  k_cbox_count<<<blocks, 128>>>(c, Np, d_xw, d_bptr, d_bnode, d_cnt);
+  k_cbox_count<<<blocks, 128>>>(c, Np, d_xw, D.box_ptr, d_cnt);
   CKC(cudaGetLastError());
   std::vector<int> cnt(Np);
   CKC(cudaMemcpy(cnt.data(), d_cnt, sizeof(int) * Np, cudaMemcpyDeviceToHost));
   std::vector<long long> ptr(Np + 1, 0);
-  int64_t nnz = 0;
-  for (int64_t i = 0; i < Np; ++i) { ptr[i + 1] = ptr[i] + (cnt[i] + 3) / 4 * 4; nnz += cnt[i]; }
+  for (int64_t i = 0; i < Np; ++i) ptr[i + 1] = ptr[i] + cnt[i];
+  const int64_t nnz = ptr[Np];
   long long* d_ptr = dup_c(ptr);
-  int* d_col = dalloc_c<int>(ptr[Np]);
-  float* d_val = dalloc_c<float>(ptr[Np]);
-  k_cbox_fill<<<blocks, 128>>>(c, Np, d_xw, d_bptr, d_bnode, d_su, d_tl, d_ptr, d_col, d_val);
+  int* d_col = dalloc_c<int>(nnz);
+  float* d_val = dalloc_c<float>(nnz);
+  k_cbox_fill<<<blocks, 128>>>(c, Np, d_xw, D.box_ptr, d_su, d_tl, d_ptr, d_col, d_val);
+  CKC(cudaGetLastError());
+  // encode C4x
+  long long* d_nch = dalloc_c<long long>(Np);
+  k_c4x_count<<<blocks, 128>>>(Np, d_ptr, d_col, d_nch);
+  CKC(cudaGetLastError());
+  std::vector<long long> nch(Np), cptr(Np + 1, 0);
+  CKC(cudaMemcpy(nch.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < Np; ++i) cptr[i + 1] = cptr[i] + nch[i];
+  long long* d_cptr = dup_c(cptr);
+  unsigned long long* d_hdr = dalloc_c<unsigned long long>(cptr[Np]);
+  float* d_cval = dalloc_c<float>(4 * cptr[Np]);
+  k_c4x_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_cptr, d_hdr, d_cval);
   CKC(cudaGetLastError());
   CKC(cudaDeviceSynchronize());
-  cudaFree(d_xw); cudaFree(d_tl); cudaFree(d_su); cudaFree(d_bptr); cudaFree(d_bnode); cudaFree(d_cnt);
-  D.c_ptr = reinterpret_cast<int64_t*>(d_ptr);
-  D.c_col = d_col;
-  D.c_val = d_val;
+  cudaFree(d_xw); cudaFree(d_tl); cudaFree(d_su); cudaFree(d_cnt); cudaFree(d_nch);
+  cudaFree(d_ptr); cudaFree(d_col); cudaFree(d_val);
+  D.c_ptr = reinterpret_cast<int64_t*>(d_cptr);
+  D.c_hdr = d_hdr;
+  D.c_val = d_cval;
   D.cbox_nnz = nnz;
+  D.cbox_chunks = cptr[Np];
   return nnz;
 }
 

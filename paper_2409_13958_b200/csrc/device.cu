@@ -163,108 +163,212 @@ struct GridDims { int n0, n1, n2; int per0, per1, per2; };
 __device__ __forceinline__ int wrapi(int i, int n, int per) { return per ? (i >= n ? i - n : i) : i; }
 
 // ------------------------------------------------------------------ K2 anterpolation
-// Particle-to-grid scatter staged in shared memory: a CTA takes 256 consecutive (box-sorted)
-// nodes, whose stencils cover a compact block of the grid -- one x-row range when the chunk
-// stays in one (y, z) row, one z-plane band otherwise -- accumulates the (P+1)^3 weighted
-// charges there with shared-memory atomics and flushes the non-zero block points with one
-// global atomic each (2.5-6x fewer global atomics than a direct scatter).  Chunks spanning
-// several z planes fall back to direct global atomics.  Q must be zeroed first; rows outside
-// [lo, hi) belong to other ranks (their contributions arrive through the all-reduce of Q).
-constexpr int P2G_CAP = 12288;   // floats of staged grid block (48 KB)
+// Tiled particle-to-grid: one CTA owns a T0 x T1 x T2 tile of the grid (the tiles partition
+// it, so every grid point is written exactly once -- no memset, no global atomics).  The nodes
+// whose (P+1)^3 stencil can reach the tile are those anchored in [tile - P, tile_end) per axis;
+// rows are sorted by anchor box (x fastest), so they are the contiguous row ranges of the
+// tile's (T2+P) x (T1+P) anchor lines, read through box_ptr.  A warp takes one line at a time,
+// lanes take its nodes.  Shared-memory fp32 atomics are CAS loops on sm_100 (ATOMS.CAST.SPIN),
+// so the tile accumulates in 32-bit fixed point with the native integer ATOMS.ADD: a first
+// sweep finds max|q| and the largest anchor-box population m_b of the tile's halo, which bound
+// every partial sum by 2 m_b (P+1)^3 max|q| (|Lagrange weight| <= 1 on the stencil interval,
+// x2 margin); the scale is the power of two that maps that bound to 2^30 (no overflow), so a
+// contribution is rounded to ~1e-7 of max|q| -- the level of fp32 accumulation -- and the sum is
+// order-independent (deterministic).  Each node is read by up to prod_a (T_a+P)/T_a tiles.
+// Rows outside [lo, hi) belong to other ranks (their contributions arrive with the Q reduction).
+struct TileDims { int t0, t1, t2; };
+
+// distinct anchors whose stencil can touch [a0, a0+T): up to two ranges [r0,r1],[r2,r3]
+__device__ __forceinline__ int anchor_ranges(int a0, int T, int n, int per, int P, int* r) {
+  if (per) {
+    if (T + P >= n) { r[0] = 0; r[1] = n - 1; return 1; }
+    if (a0 - P >= 0) { r[0] = a0 - P; r[1] = a0 + T - 1; return 1; }
+    r[0] = 0; r[1] = a0 + T - 1; r[2] = n + a0 - P; r[3] = n - 1; return 2;
+  }
+  r[0] = max(a0 - P, 0); r[1] = min(a0 + T - 1, n - 1 - P);
+  return r[0] <= r[1] ? 1 : 0;
+}
+
+// dynamic shared memory of k2_tile: the int tile, then per candidate segment (anchor line x
+// x range) its first row and the exclusive prefix of the segment sizes
+__host__ __device__ __forceinline__ int k2_nseg(int t1, int t2, int P) { return 2 * (t1 + P) * (t2 + P); }
 
 template <int P>
-__global__ void __launch_bounds__(256) k2_p2g(RowRange rr, const float* __restrict__ q, const int4* __restrict__ st_s,
-                                              const float4* __restrict__ st_t, GridDims g, float* __restrict__ Q) {
-  __shared__ float blk[P2G_CAP];
-  const int64_t c0 = rr.row0 + (int64_t)blockIdx.x * blockDim.x;
-  const int64_t c1 = min(c0 + (int64_t)blockDim.x, rr.row1) - 1;
-  const int64_t n = c0 + threadIdx.x;
-  const bool valid = n <= c1;
-  const int4 sa = st_s[c0], sb = st_s[c1];
-  // block extents in unwrapped stencil indices
-  int z0 = sa.z, nz = sb.z - sa.z + P + 1, y0, ny, x0, nx;
-  if (sa.z == sb.z && sa.y == sb.y) { y0 = sa.y; ny = P + 1; x0 = sa.x; nx = sb.x - sa.x + P + 1; }
-  else if (sa.z == sb.z) { y0 = sa.y; ny = sb.y - sa.y + P + 1; x0 = 0; nx = g.n0; }
-  else { y0 = 0; ny = 0; x0 = 0; nx = 0; }
-  const bool staged = ny > 0 && (int64_t)nz * ny * nx <= P2G_CAP;
-  const int tot = staged ? nz * ny * nx : 0;
-  for (int t = threadIdx.x; t < tot; t += blockDim.x) blk[t] = 0.f;
+__global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const int32_t* __restrict__ box_ptr,
+                                               const int4* __restrict__ st_s, const float4* __restrict__ st_t,
+                                               const float* __restrict__ q, int64_t lo, int64_t hi, int box_max,
+                                               float* __restrict__ Q) {
+  extern __shared__ int tile[];
+  __shared__ int red_q;
+  __shared__ int wsum[8];
+  const int T0 = td.t0, T1 = td.t1, T2 = td.t2, vol = T0 * T1 * T2;
+  int* seg_beg = tile + vol;
+  int* seg_cum = seg_beg + k2_nseg(T1, T2, P);
+  const int nt0 = g.n0 / T0, nt1 = g.n1 / T1;
+  const int bx = blockIdx.x % nt0, by = (blockIdx.x / nt0) % nt1, bz = blockIdx.x / (nt0 * nt1);
+  const int x0 = bx * T0, y0 = by * T1, z0 = bz * T2;
+  for (int i = threadIdx.x; i < vol; i += blockDim.x) tile[i] = 0;
+  if (threadIdx.x == 0) red_q = 0;
+  int rz[4], ry[4], rx[4];
+  const int nz = anchor_ranges(z0, T2, g.n2, g.per2, P, rz);
+  const int ny = anchor_ranges(y0, T1, g.n1, g.per1, P, ry);
+  const int nx = anchor_ranges(x0, T0, g.n0, g.per0, P, rx);
+  const int cz = nz == 0 ? 0 : (rz[1] - rz[0] + 1) + (nz == 2 ? rz[3] - rz[2] + 1 : 0);
+  const int cy = ny == 0 ? 0 : (ry[1] - ry[0] + 1) + (ny == 2 ? ry[3] - ry[2] + 1 : 0);
+  const int nseg = cz * cy * nx;
+  // segment table: rows [box_ptr(line + xa), box_ptr(line + xb + 1)) clipped to [lo, hi)
+  constexpr int PER = 8;                                   // segments per thread in the scan
+  int cnt[PER];
+  int mysum = 0;
+  const int s0 = threadIdx.x * PER;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int sg = s0 + u;
+    cnt[u] = 0;
+    if (sg < nseg) {
+      const int line = sg / nx, r = sg - line * nx;
+      const int iz = line / cy, iy = line - iz * cy;
+      const int sz = iz <= rz[1] - rz[0] ? rz[0] + iz : rz[2] + iz - (rz[1] - rz[0] + 1);
+      const int sy = iy <= ry[1] - ry[0] ? ry[0] + iy : ry[2] + iy - (ry[1] - ry[0] + 1);
+      const int64_t lb = ((int64_t)sz * g.n1 + sy) * g.n0;
+      const int64_t i0 = max((int64_t)__ldg(box_ptr + lb + rx[2 * r]), lo);
+      const int64_t i1 = min((int64_t)__ldg(box_ptr + lb + rx[2 * r + 1] + 1), hi);
+      seg_beg[sg] = (int)i0;
+      cnt[u] = i1 > i0 ? (int)(i1 - i0) : 0;
+    }
+    mysum += cnt[u];
+  }
+  // block exclusive scan of the per-thread sums
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int incl = mysum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
   __syncthreads();
-  if (valid) {
-    const int4 s = st_s[n];
-    const float4 t = st_t[n];
-    const float qn = q[n];
-    float wx[P + 1], wy[P + 1], wz[P + 1];
-    lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+  int woff = 0, total = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) { const int v = wsum[w]; if (w < warp) woff += v; total += v; }
+  int run = woff + incl - mysum;
 #pragma unroll
-    for (int k = 0; k <= P; ++k) {
+  for (int u = 0; u < PER; ++u) {
+    const int sg = s0 + u;
+    if (sg < nseg) seg_cum[sg] = run;
+    run += cnt[u];
+  }
+  if (threadIdx.x == 0) seg_cum[nseg] = total;
+  __syncthreads();
+  // flattened node f -> (segment, row): binary search in seg_cum
+  auto row_of = [&](int f) {
+    int a = 0, b = nseg;                                   // seg_cum[a] <= f < seg_cum[b]
+    while (b - a > 1) { const int m = (a + b) >> 1; if (seg_cum[m] <= f) a = m; else b = m; }
+    return (int64_t)seg_beg[a] + (f - seg_cum[a]);
+  };
+  // sweep 1: max |q| over the halo nodes
+  float qm = 0.f;
+  for (int f = threadIdx.x; f < total; f += blockDim.x) qm = fmaxf(qm, fabsf(__ldg(q + row_of(f))));
 #pragma unroll
-      for (int j = 0; j <= P; ++j) {
-        const float wzy = qn * wz[k] * wy[j];
-        if (staged) {
-          float* row = blk + ((s.z + k - z0) * ny + (s.y + j - y0)) * nx;
+  for (int o = 16; o > 0; o >>= 1) qm = fmaxf(qm, __shfl_xor_sync(0xffffffffu, qm, o));
+  if (lane == 0) atomicMax(&red_q, __float_as_int(qm));
+  __syncthreads();
+  const float qmax = __int_as_float(red_q);
+  const int P3 = (P + 1) * (P + 1) * (P + 1);
+  // power-of-two scale: 2 box_max (P+1)^3 qmax * scale <= 2^30
+  const float scale = qmax > 0.f ? exp2f(floorf(log2f(1073741824.f / (2.f * (float)box_max * (float)P3 * qmax)))) : 0.f;
+  // sweep 2: fixed-point scatter into the tile
+  if (qmax > 0.f) {
+    for (int f = threadIdx.x; f < total; f += blockDim.x) {
+      const int64_t i = row_of(f);
+      const int4 s = __ldg(st_s + i);
+      const float4 t = __ldg(st_t + i);
+      const float qn = __ldg(q + i) * scale;
+      float wx[P + 1], wy[P + 1], wz[P + 1];
+      lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+      int lx[P + 1], ly[P + 1], lz[P + 1];
 #pragma unroll
-          for (int i = 0; i <= P; ++i) {
-            int ix = s.x + i - x0;
-            if (nx == g.n0 && ix >= g.n0) ix -= g.n0;          // full-width rows wrap in place
-            atomicAdd(row + ix, wzy * wx[i]);
-          }
-        } else {
-          const int iz = wrapi(s.z + k, g.n2, g.per2), iy = wrapi(s.y + j, g.n1, g.per1);
-          float* row = Q + ((int64_t)iz * g.n1 + iy) * g.n0;
+      for (int k = 0; k <= P; ++k) {
+        int a = wrapi(s.x + k, g.n0, g.per0) - x0; lx[k] = (a >= 0 && a < T0) ? a : -1;
+        a = wrapi(s.y + k, g.n1, g.per1) - y0;     ly[k] = (a >= 0 && a < T1) ? a : -1;
+        a = wrapi(s.z + k, g.n2, g.per2) - z0;     lz[k] = (a >= 0 && a < T2) ? a : -1;
+      }
 #pragma unroll
-          for (int i = 0; i <= P; ++i) atomicAdd(row + wrapi(s.x + i, g.n0, g.per0), wzy * wx[i]);
+      for (int k = 0; k <= P; ++k) {
+        if (lz[k] < 0) continue;
+#pragma unroll
+        for (int j = 0; j <= P; ++j) {
+          if (ly[j] < 0) continue;
+          const float wzy = qn * wz[k] * wy[j];
+          int* row = tile + (lz[k] * T1 + ly[j]) * T0;
+#pragma unroll
+          for (int l = 0; l <= P; ++l)
+            if (lx[l] >= 0) atomicAdd(row + lx[l], __float2int_rn(wzy * wx[l]));
         }
       }
     }
   }
-  if (!staged) return;
   __syncthreads();
-  for (int t = threadIdx.x; t < tot; t += blockDim.x) {
-    const float v = blk[t];
-    if (v == 0.f) continue;
-    const int ix = t % nx, r = t / nx, iy = r % ny, iz = r / ny;
-    const int gx = wrapi(x0 + ix, g.n0, g.per0), gy = wrapi(y0 + iy, g.n1, g.per1), gz = wrapi(z0 + iz, g.n2, g.per2);
-    atomicAdd(Q + ((int64_t)gz * g.n1 + gy) * g.n0 + gx, v);
+  const float inv = qmax > 0.f ? 1.f / scale : 0.f;
+  for (int i = threadIdx.x; i < vol; i += blockDim.x) {
+    const int ix = i % T0, r = i / T0, iy = r % T1, iz = r / T1;
+    Q[((int64_t)(z0 + iz) * g.n1 + (y0 + iy)) * g.n0 + x0 + ix] = (float)tile[i] * inv;
   }
 }
 
 // ------------------------------------------------------------------ K4 interpolation + precorrection
 // G lanes per row (8, 16 or 32, chosen from the mean C_box row length so every lane has
-// several 16-byte loads in flight); the (P+1)^3 grid gathers are spread over the same lanes.
+// several loads in flight); the (P+1)^3 grid gathers are spread over the same lanes.  C_box
+// is streamed in the C4x format (cbox_gpu.cu): per chunk one 16-byte value load and one
+// 8-byte header (base column + three 12-bit deltas) -- consecutive lanes take consecutive
+// chunks, so the q gathers of a lane group mostly hit the same few lines.
 template <int P, int G>
 __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
                                                       const float4* __restrict__ st_t, GridDims g,
-                                                      const int64_t* __restrict__ c_ptr, const int4* __restrict__ c_col4,
+                                                      const int64_t* __restrict__ c_ptr, const unsigned long long* __restrict__ c_hdr,
                                                       const float4* __restrict__ c_val4, const float* __restrict__ q,
                                                       const float* __restrict__ uloc, float* __restrict__ u) {
   const int lane = threadIdx.x & (G - 1);
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
-  const int64_t b = valid ? c_ptr[n] >> 2 : 0, e_end = valid ? c_ptr[n + 1] >> 2 : 0;
+  const int64_t b = valid ? c_ptr[n] : 0, e_end = valid ? c_ptr[n + 1] : 0;
 #pragma unroll 2
   for (int64_t e = b + lane; e < e_end; e += G) {
-    const int4 cc = __ldg(c_col4 + e);
+    const unsigned long long h = __ldg(c_hdr + e);
     const float4 vv = __ldg(c_val4 + e);
-    acc = fmaf(vv.x, q[cc.x], acc);
-    acc = fmaf(vv.y, q[cc.y], acc);
-    acc = fmaf(vv.z, q[cc.z], acc);
-    acc = fmaf(vv.w, q[cc.w], acc);
+    const int k0 = (int)(h & 0xFFFFFFFull);
+    const int k1 = k0 + (int)((h >> 28) & 0xFFF);
+    const int k2 = k1 + (int)((h >> 40) & 0xFFF);
+    const int k3 = k2 + (int)(h >> 52);
+    acc = fmaf(vv.x, q[k0], acc);
+    acc = fmaf(vv.y, q[k1], acc);
+    acc = fmaf(vv.z, q[k2], acc);
+    acc = fmaf(vv.w, q[k3], acc);
   }
-  constexpr int NS = (P + 1) * (P + 1) * (P + 1);
-  if (valid && lane < NS) {
+  // interpolation: lane r < (P+1)^2 takes one (y, z) stencil row and its P+1 x-consecutive
+  // grid values (index maths once per row, not per point)
+  constexpr int NR = (P + 1) * (P + 1);
+  if (valid && lane < NR) {
     const int4 s = st_s[n];
     const float4 t = st_t[n];
     float wx[P + 1], wy[P + 1], wz[P + 1];
     lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
-    for (int k = lane; k < NS; k += G) {
-      const int i = k % (P + 1), j = (k / (P + 1)) % (P + 1), l = k / ((P + 1) * (P + 1));
-      const int ix = wrapi(s.x + i, g.n0, g.per0), iy = wrapi(s.y + j, g.n1, g.per1), iz = wrapi(s.z + l, g.n2, g.per2);
-      float wi = 0, wj = 0, wl = 0;
+    int ix[P + 1];
 #pragma unroll
-      for (int a = 0; a <= P; ++a) { if (a == i) wi = wx[a]; if (a == j) wj = wy[a]; if (a == l) wl = wz[a]; }
-      acc = fmaf(wi * wj * wl, U[((int64_t)iz * g.n1 + iy) * g.n0 + ix], acc);
+    for (int i = 0; i <= P; ++i) ix[i] = wrapi(s.x + i, g.n0, g.per0);
+    for (int r = lane; r < NR; r += G) {
+      const int jy = r % (P + 1), jz = r / (P + 1);
+      float wyz = 0.f;
+#pragma unroll
+      for (int a = 0; a <= P; ++a)
+#pragma unroll
+        for (int b = 0; b <= P; ++b)
+          if (a == jy && b == jz) wyz = wy[a] * wz[b];
+      const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+      float v = 0.f;
+#pragma unroll
+      for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(row + ix[i]), v);
+      acc = fmaf(wyz, v, acc);
     }
   }
 #pragma unroll
@@ -403,6 +507,39 @@ void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows
   CK(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------- slab-decomposed convolution
+// (SURVEY 8(e)): rank r owns the z planes [r nzl, (r+1) nzl) of the grid for the X and Y
+// passes and the k0 columns [h_r, h_r + H_r) of the half spectrum for the Z pass; two
+// all-to-all transposes move the spectrum between the two layouts.
+//   z-slab layout Cz [nzl][P1][H0]   x-slab layout Cx [P2][P1][H_r]
+// Block (r -> p) = Cz_r[:, :, h_p : h_p + H_p] packed as [nzl][P1][H_p]; it lands in Cx_p at
+// plane offset r nzl (contiguous), so only the sender packs and only the return path unpacks.
+__host__ __device__ __forceinline__ int slab_h0(int p, int H0, int W) { return p * (H0 / W) + min(p, H0 % W); }
+__host__ __device__ __forceinline__ int slab_hn(int p, int H0, int W) { return H0 / W + (p < H0 % W ? 1 : 0); }
+
+// pack (dir 0): Cz[rows][H0] cols [h_p, h_p+H_p) -> buf + p*rows*(h_p) ... contiguous [rows][H_p] blocks
+// unpack (dir 1): the reverse.  blockIdx.y = peer p.
+__global__ void k_slab_pack(float2* __restrict__ cz, float2* __restrict__ buf, int64_t rows, int H0, int W, int dir) {
+  const int p = blockIdx.y;
+  const int h = slab_h0(p, H0, W), hn = slab_hn(p, H0, W);
+  float2* blk = buf + rows * (int64_t)h;                  // blocks are stored back to back
+  const int64_t tot = rows * hn;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / hn;
+    const int c = (int)(i - r * hn);
+    if (dir == 0) blk[i] = cz[r * H0 + h + c];
+    else cz[r * H0 + h + c] = blk[i];
+  }
+}
+
+// spectrum slice for rank r: spec [P2 P1][H0] cols [h_r, h_r+H_r) -> [P2 P1][H_r]
+__global__ void k_spec_slice(const float* __restrict__ spec, float* __restrict__ out, int64_t rows, int H0, int h, int hn) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * hn) return;
+  const int64_t r = i / hn;
+  out[i] = spec[r * H0 + h + (int)(i - r * hn)];
+}
+
 void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
   const int tile = D.fused_tile, P1 = D.P[1], P2 = D.P[2];
   size_t smem = (size_t)P2 * (P1 * tile + (tile == 1 ? 1 : 0)) * sizeof(float2);   // padded planes
@@ -504,31 +641,6 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.m4 = dalloc<float4>(Np);
   CK(cudaMemset(D.m4, 0, sizeof(float4) * (size_t)Np));
 
-  // ---- C_box: CSR with rows padded to a multiple of 4 (built on the GPU when cbox_device)
-  if (S.cbox_device) {
-    device_build_cbox(D, S);
-  } else {
-    std::vector<int64_t> ptr(Np + 1, 0);
-    for (int64_t i = 0; i < Np; ++i) {
-      int64_t r = S.perm[i];
-      int64_t len = S.cbox.rowptr[r + 1] - S.cbox.rowptr[r];
-      ptr[i + 1] = ptr[i] + (len + 3) / 4 * 4;
-    }
-    std::vector<int32_t> col(ptr[Np]);
-    std::vector<float> val(ptr[Np], 0.f);
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t i = 0; i < Np; ++i) {
-      int64_t r = S.perm[i];
-      std::vector<std::pair<int32_t, int64_t>> tmp;
-      for (int64_t e = S.cbox.rowptr[r]; e < S.cbox.rowptr[r + 1]; ++e) tmp.push_back({(int32_t)S.iperm[S.cbox.col[e]], e});
-      std::sort(tmp.begin(), tmp.end());
-      int64_t o = ptr[i];
-      for (auto& pr : tmp) { col[o] = pr.first; val[o] = (float)S.cbox.val[pr.second]; ++o; }
-      for (; o < ptr[i + 1]; ++o) col[o] = (int32_t)i;
-    }
-    D.c_ptr = dupload(ptr); D.c_col = dupload(col); D.c_val = dupload(val);
-    D.cbox_nnz = S.cbox.nnz();
-  }
   std::vector<float4> rsum(2 * Np), stt(Np);
   std::vector<int4> sts(Np);
   for (int64_t i = 0; i < Np; ++i) {
@@ -547,18 +659,52 @@ void device_upload(DeviceState& D, const HostSetup& S) {
                          __int_as_float_host(s[0]));
   }
   D.rowsum = dupload(rsum); D.st_s = dupload(sts); D.st_t = dupload(stt);
-  // K2 stages chunks of consecutive rows: the rows must be sorted by anchor box (x fastest)
-  for (int64_t i = 1; i < Np; ++i) {
-    const int64_t k0 = ((int64_t)sts[i - 1].z * D.n[1] + sts[i - 1].y) * D.n[0] + sts[i - 1].x;
-    const int64_t k1 = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
-    if (k1 < k0) throw Error(PMFEM_E_STATE, "internal rows are not sorted by anchor box");
+  // K2 reads the rows of each anchor line through box_ptr: rows must be sorted by anchor box
+  {
+    const int64_t Gb = (int64_t)D.n[0] * D.n[1] * D.n[2];
+    std::vector<int32_t> bp(Gb + 1, 0);
+    for (int64_t i = 0; i < Np; ++i) {
+      const int64_t key = ((int64_t)sts[i].z * D.n[1] + sts[i].y) * D.n[0] + sts[i].x;
+      if (i > 0) {
+        const int64_t k0 = ((int64_t)sts[i - 1].z * D.n[1] + sts[i - 1].y) * D.n[0] + sts[i - 1].x;
+        if (key < k0) throw Error(PMFEM_E_STATE, "internal rows are not sorted by anchor box");
+      }
+      bp[key + 1]++;
+    }
+    D.box_max = 1;
+    for (int64_t b = 0; b < Gb; ++b) { D.box_max = std::max(D.box_max, bp[b + 1]); bp[b + 1] += bp[b]; }
+    D.box_ptr = dupload(bp);
+    // K2 tile: ~G/600 points (>= 4 CTAs per SM), 512..8192 points, grown by doubling the
+    // shortest axis (x first on ties) so the tile stays compact; PMFEM_K2_TILE=t0,t1,t2 overrides
+    int64_t target = 512;
+    while (target < 8192 && target * 2 * 600 <= Gb) target *= 2;
+    int t[3] = {1, 1, 1};
+    while ((int64_t)t[0] * t[1] * t[2] < target) {
+      int best = -1;
+      for (int a = 0; a < 3; ++a)
+        if (t[a] < D.n[a] && (best < 0 || t[a] < t[best])) best = a;
+      if (best < 0) break;
+      t[best] *= 2;
+    }
+    if (const char* e = std::getenv("PMFEM_K2_TILE")) {
+      int a0, a1, a2;
+      if (std::sscanf(e, "%d,%d,%d", &a0, &a1, &a2) == 3 && a0 > 0 && a1 > 0 && a2 > 0 && D.n[0] % a0 == 0 &&
+          D.n[1] % a1 == 0 && D.n[2] % a2 == 0 && a0 * a1 * a2 <= 12288 && k2_nseg(a1, a2, D.order) <= 2048) {
+        t[0] = a0; t[1] = a1; t[2] = a2;
+      }
+    }
+    for (int a = 0; a < 3; ++a) D.k2_tile[a] = t[a];
   }
+  // ---- C_box: built on the device in internal order, stored in the chunked C4x format
+  if (!S.cbox_device) throw Error(PMFEM_E_STATE, "device contexts build C_box on the device");
+  device_build_cbox(D, S);
   for (int a = 0; a < 3; ++a) {
     std::vector<float2> t32; std::vector<double2> t64;
     twiddles<float>(D.P[a], t32); twiddles<double>(D.P[a], t64);
     D.tw32[a] = dupload(t32); D.tw64[a] = dupload(t64);
   }
   D.q = dalloc<float>(Np); D.uloc = dalloc<float>(Np); D.u = dalloc<float>(Np);
+  CK(cudaMemset(D.q, 0, sizeof(float) * (size_t)Np));
   D.Q = dalloc<float>((size_t)D.n[0] * D.n[1] * D.n[2]);
   D.C = dalloc<float2>((size_t)D.H0 * D.P[1] * D.P[2]);
   D.spec = dalloc<float>((size_t)D.H0 * D.P[1] * D.P[2]);
@@ -575,6 +721,27 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     }
   }
   D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5
+  // slab-decomposed convolution: NCCL ranks, or simulated ranks on one device (tests)
+  {
+    int W = 1;
+    if (D.world > 1) {
+      if (D.n[2] % D.world == 0 && D.H0 >= D.world && std::getenv("PMFEM_NO_SLAB") == nullptr) W = D.world;
+    } else if (const char* e = std::getenv("PMFEM_SLAB_SIM")) {
+      const int w = std::atoi(e);
+      if (w > 1 && D.n[2] % w == 0 && D.H0 >= w) W = w;
+    }
+    D.slab_world = W;
+    if (W > 1) {
+      const int64_t plane = (int64_t)D.P[1], nzl = D.n[2] / W;
+      const int64_t Hr = D.world > 1 ? slab_hn(D.rank, D.H0, W) : D.H0;
+      D.slab_cx = dalloc<float2>((size_t)D.P[2] * plane * Hr);
+      D.slab_spec = dalloc<float>((size_t)D.P[2] * plane * Hr);
+      D.slab_buf = dalloc<float2>((size_t)(D.world > 1 ? nzl : D.n[2]) * plane * D.H0);
+      D.fused_tile = 0;
+      // per rank: X, Y, pack, Z, unpack, Y', X' (+ W-1 sends/receives and the copies in NCCL)
+      D.launches_per_eval = 5 + 7 * (D.world > 1 ? 1 : W);
+    }
+  }
   // compulsory bytes per launch: every array read or written once (gathered m, q, u once),
   // actual entries only (SELL padding is overhead, not algorithmic traffic)
   const double G = (double)D.n[0] * D.n[1] * D.n[2];
@@ -582,7 +749,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   for (int64_t i = 0; i < Np; ++i) { nsh += lenz[i]; n1e += len1[i]; }
   // K1 window = m -> float4 copy (12 + 16) + K1 (m4 16, row sums 32, slice offsets ~0, q, u_loc, H_ex)
   D.kernel_bytes[0] = Np * (12.0 + 16 + 16 + 32 + 4 + 4 + 12) + nsh * 16 + n1e * 16;
-  D.kernel_bytes[1] = Np * (4.0 + 16) + G * 4.0 * 2;          // q + local t, box_ptr, Q write
+  D.kernel_bytes[1] = Np * (4.0 + 16 + 16) + G * 4.0 * 2;     // q + anchors + local t, box_ptr, Q write
   {
     const double Hc = (double)D.H0;
     const double spec_b = Hc * D.P[1] * D.P[2] * 4;
@@ -598,15 +765,17 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   }
   const int64_t cnnz = D.cbox_nnz;
   {
-    // K4 group size: ~4+ int4 loads per lane; PMFEM_K4_GROUP overrides (tests)
-    const double row4 = (double)cnnz / std::max<int64_t>(Np, 1) / 4.0;
+    // K4 group size: ~4+ chunks per lane; PMFEM_K4_GROUP overrides (tests)
+    const double row4 = (double)D.cbox_chunks / std::max<int64_t>(Np, 1);
     D.k4_group = row4 >= 96 ? 32 : (row4 >= 40 ? 16 : 8);
     if (const char* e = std::getenv("PMFEM_K4_GROUP")) {
       const int gsel = std::atoi(e);
       if (gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
     }
   }
-  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 8 + G * 4.0;
+  // C_box in C4x: 4-byte value + 2 bytes of chunk header per near pair (chunk padding, ~3-10 %,
+  // is format overhead, not algorithmic traffic)
+  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 6 + G * 4.0;
   D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
 
@@ -634,6 +803,17 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
   const int64_t nspec = (int64_t)H0 * P1 * P2;
   k_spec_finish<<<(unsigned)((nspec + 255) / 256), 256>>>(C, D.spec, nspec, 1.0 / (double)tot);
   CK(cudaGetLastError());
+  if (D.slab_world > 1) {   // spectrum slices of the x-slab layout
+    const int W = D.slab_world;
+    const int64_t rows = (int64_t)P1 * P2;
+    for (int p = 0; p < W; ++p) {
+      if (D.world > 1 && p != D.rank) continue;
+      const int h = slab_h0(p, H0, W), hn = slab_hn(p, H0, W);
+      float* out = D.slab_spec + (D.world > 1 ? 0 : rows * h);
+      k_spec_slice<<<(unsigned)((rows * hn + 255) / 256), 256>>>(D.spec, out, rows, H0, h, hn);
+      CK(cudaGetLastError());
+    }
+  }
   CK(cudaDeviceSynchronize());
   cudaFree(K);
   cudaFree(C);
@@ -643,10 +823,10 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
 void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
-  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_col, D.c_val,
-                  D.st_s, D.st_t, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
+  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_val,
+                  D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
-                  D.send_buf, D.recv_buf, D.send_idx[0], D.send_idx[1], D.send_idx[2],
+                  D.send_buf, D.recv_buf, D.slab_cx, D.slab_buf, D.slab_spec, D.send_idx[0], D.send_idx[1], D.send_idx[2],
                   D.recv_idx[0], D.recv_idx[1], D.recv_idx[2]};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -676,7 +856,12 @@ void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id) {
   D.comm = comm;
   int64_t sbuf = 0, rbuf = 0;
   const int width[3] = {4, 1, 1};   // m travels as the float4 copy
-  D.comm_bytes_per_eval = 4.0 * (double)D.n[0] * D.n[1] * D.n[2] * 2.0 * (P.world - 1) / P.world;  // ring all-reduce
+  // grid traffic sent per rank: ring all-reduce of Q (replicated FFT), or reduce-scatter +
+  // all-gather of Q plus the two spectrum transposes (slab FFT)
+  const double Gq = 4.0 * (double)D.n[0] * D.n[1] * D.n[2] * (P.world - 1) / P.world;
+  D.comm_bytes_per_eval = 2.0 * Gq;
+  if (D.slab_world > 1)
+    D.comm_bytes_per_eval += 2.0 * 8.0 * (double)(D.n[2] / P.world) * D.P[1] * (D.H0 - slab_hn(P.rank, D.H0, P.world));
   for (int k = 0; k < 3; ++k) {
     D.send_ptr[k] = P.send_ptr[k];
     D.recv_ptr[k] = P.recv_ptr[k];
@@ -715,6 +900,94 @@ void halo(DeviceState& D, int k, float* v, int w, cudaStream_t st) {
     CK(cudaGetLastError());
   }
 }
+
+// ---- slab-decomposed FFT convolution; D.slab_world > 1
+// per-rank phases, shared by the NCCL path and the single-device simulation (PMFEM_SLAB_SIM)
+void slab_phase_fwd(const DeviceState& D, const float* Qs, float2* Cz, float2* sbuf, int W, cudaStream_t st) {
+  const int n0 = D.n[0], n1 = D.n[1], nzl = D.n[2] / W, P0 = D.P[0], P1 = D.P[1], H0 = D.H0;
+  launch_x<float>(true, Qs, Cz, nullptr, nzl * n1, n0, P0, n1, P1, D.tw32[0], st);
+  launch_strided<float>(Cz, P1, H0, H0, nzl, (long long)P1 * H0, n1, P1, 0, nullptr, 0, 0, D.tw32[1], st);
+  const int64_t rows = (int64_t)nzl * P1;
+  k_slab_pack<<<dim3((unsigned)std::min<int64_t>(1024, (rows * (H0 / W + 1) + 255) / 256), W), 256, 0, st>>>(Cz, sbuf, rows, H0, W, 0);
+  CK(cudaGetLastError());
+}
+void slab_phase_z(const DeviceState& D, float2* Cx, const float* spec_r, int Hr, cudaStream_t st) {
+  const int P1 = D.P[1];
+  launch_strided<float>(Cx, D.P[2], (long long)P1 * Hr, Hr, P1, Hr, D.n[2], D.n[2], 2, spec_r, (long long)P1 * Hr, Hr,
+                        D.tw32[2], st);
+}
+void slab_phase_inv(const DeviceState& D, float2* rbuf, float2* Cz, float* Us, int W, cudaStream_t st) {
+  const int n0 = D.n[0], n1 = D.n[1], nzl = D.n[2] / W, P0 = D.P[0], P1 = D.P[1], H0 = D.H0;
+  const int64_t rows = (int64_t)nzl * P1;
+  k_slab_pack<<<dim3((unsigned)std::min<int64_t>(1024, (rows * (H0 / W + 1) + 255) / 256), W), 256, 0, st>>>(Cz, rbuf, rows, H0, W, 1);
+  CK(cudaGetLastError());
+  launch_strided<float>(Cz, P1, H0, H0, nzl, (long long)P1 * H0, P1, n1, 1, nullptr, 0, 0, D.tw32[1], st);
+  launch_x<float>(false, nullptr, Cz, Us, nzl * n1, n0, P0, n1, P1, D.tw32[0], st);
+}
+
+// NCCL path: Q holds this rank's partial anterpolation on the full grid; on return Q holds
+// the full U on every rank.  reduce-scatter (z slabs) -> X, Y -> all-to-all -> Z*G -> all-to-all
+// -> Y', X' -> all-gather.
+void slab_conv_nccl(DeviceState& D, cudaStream_t st) {
+  const int W = D.world, r = D.rank, H0 = D.H0, P1 = D.P[1];
+  const int nzl = D.n[2] / W;
+  const size_t slab = (size_t)nzl * D.n[1] * D.n[0];
+  ncclComm_t comm = (ncclComm_t)D.comm;
+  NCK(ncclReduceScatter(D.Q, D.Q + r * slab, slab, ncclFloat, ncclSum, comm, st));
+  slab_phase_fwd(D, D.Q + r * slab, D.C, D.slab_buf, W, st);
+  const int Hr = slab_hn(r, H0, W);
+  const int64_t rows = (int64_t)nzl * P1;
+  NCK(ncclGroupStart());
+  for (int p = 0; p < W; ++p) {
+    if (p == r) continue;
+    NCK(ncclSend(D.slab_buf + rows * slab_h0(p, H0, W), (size_t)(rows * slab_hn(p, H0, W) * 2), ncclFloat, p, comm, st));
+    NCK(ncclRecv(D.slab_cx + (int64_t)p * rows * Hr, (size_t)(rows * Hr * 2), ncclFloat, p, comm, st));
+  }
+  NCK(ncclGroupEnd());
+  CK(cudaMemcpyAsync(D.slab_cx + (int64_t)r * rows * Hr, D.slab_buf + rows * slab_h0(r, H0, W),
+                     sizeof(float2) * rows * Hr, cudaMemcpyDeviceToDevice, st));
+  slab_phase_z(D, D.slab_cx, D.slab_spec, Hr, st);
+  NCK(ncclGroupStart());
+  for (int p = 0; p < W; ++p) {
+    if (p == r) continue;
+    NCK(ncclSend(D.slab_cx + (int64_t)p * rows * Hr, (size_t)(rows * Hr * 2), ncclFloat, p, comm, st));
+    NCK(ncclRecv(D.slab_buf + rows * slab_h0(p, H0, W), (size_t)(rows * slab_hn(p, H0, W) * 2), ncclFloat, p, comm, st));
+  }
+  NCK(ncclGroupEnd());
+  CK(cudaMemcpyAsync(D.slab_buf + rows * slab_h0(r, H0, W), D.slab_cx + (int64_t)r * rows * Hr,
+                     sizeof(float2) * rows * Hr, cudaMemcpyDeviceToDevice, st));
+  slab_phase_inv(D, D.slab_buf, D.C, D.Q + r * slab, W, st);
+  NCK(ncclAllGather(D.Q + r * slab, D.Q, slab, ncclFloat, comm, st));
+}
+
+// The same decomposition with W simulated ranks on this device (test mode, PMFEM_SLAB_SIM=W):
+// every rank's phase runs in turn and the transposes are device copies of exactly the blocks
+// the NCCL path sends.  Q holds the full anterpolated grid (= the reduce-scatter result of
+// every rank); each rank's U slab lands in place (= the all-gather result).
+void slab_conv_sim(DeviceState& D, cudaStream_t st) {
+  const int W = D.slab_world, H0 = D.H0, P1 = D.P[1], P2 = D.P[2];
+  const int nzl = D.n[2] / W;
+  const size_t slab = (size_t)nzl * D.n[1] * D.n[0];
+  const int64_t rows = (int64_t)nzl * P1;
+  for (int r = 0; r < W; ++r) slab_phase_fwd(D, D.Q + r * slab, D.C + (int64_t)r * rows * H0, D.slab_buf + (int64_t)r * rows * H0, W, st);
+  for (int r = 0; r < W; ++r)
+    for (int p = 0; p < W; ++p) {
+      const int64_t hp = slab_h0(p, H0, W), np = slab_hn(p, H0, W);
+      CK(cudaMemcpyAsync(D.slab_cx + (int64_t)P2 * P1 * hp + r * rows * np, D.slab_buf + (int64_t)r * rows * H0 + rows * hp,
+                         sizeof(float2) * rows * np, cudaMemcpyDeviceToDevice, st));
+    }
+  for (int p = 0; p < W; ++p) {
+    const int64_t hp = slab_h0(p, H0, W);
+    slab_phase_z(D, D.slab_cx + (int64_t)P2 * P1 * hp, D.slab_spec + (int64_t)P2 * P1 * hp, slab_hn(p, H0, W), st);
+  }
+  for (int r = 0; r < W; ++r)
+    for (int p = 0; p < W; ++p) {
+      const int64_t hp = slab_h0(p, H0, W), np = slab_hn(p, H0, W);
+      CK(cudaMemcpyAsync(D.slab_buf + (int64_t)r * rows * H0 + rows * hp, D.slab_cx + (int64_t)P2 * P1 * hp + r * rows * np,
+                         sizeof(float2) * rows * np, cudaMemcpyDeviceToDevice, st));
+    }
+  for (int r = 0; r < W; ++r) slab_phase_inv(D, D.slab_buf + (int64_t)r * rows * H0, D.C + (int64_t)r * rows * H0, D.Q + r * slab, W, st);
+}
 }  // namespace
 
 // m, H: [hi-lo][3] rank-local rows (the full [N'][3] on a single GPU)
@@ -742,16 +1015,29 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   CK(cudaGetLastError());
   mark(1);
   const size_t G = (size_t)D.n[0] * D.n[1] * D.n[2];
-  CK(cudaMemsetAsync(D.Q, 0, sizeof(float) * G, st));
-  switch (D.order) {
-    case 1: k2_p2g<1><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
-    case 2: k2_p2g<2><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
-    default: k2_p2g<3><<<thr_blocks, 256, 0, st>>>(rr, D.q, D.st_s, D.st_t, g, D.Q); break;
+  {
+    const TileDims td{D.k2_tile[0], D.k2_tile[1], D.k2_tile[2]};
+    const unsigned nt = (unsigned)(G / ((size_t)td.t0 * td.t1 * td.t2));
+    const size_t smem = sizeof(int) * ((size_t)td.t0 * td.t1 * td.t2 + 2 * k2_nseg(td.t1, td.t2, D.order) + 1);
+#define K2_LAUNCH(PP)                                                                                 \
+  do {                                                                                                \
+    CK(cudaFuncSetAttribute(k2_tile<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    k2_tile<PP><<<nt, 256, smem, st>>>(g, td, D.box_ptr, D.st_s, D.st_t, D.q, D.lo, D.hi, D.box_max, D.Q); \
+  } while (0)
+    switch (D.order) {
+      case 1: K2_LAUNCH(1); break;
+      case 2: K2_LAUNCH(2); break;
+      default: K2_LAUNCH(3); break;
+    }
+#undef K2_LAUNCH
   }
   CK(cudaGetLastError());
-  if (D.world > 1) NCK(ncclAllReduce(D.Q, D.Q, G, ncclFloat, ncclSum, (ncclComm_t)D.comm, st));
+  if (D.world > 1 && D.slab_world <= 1) NCK(ncclAllReduce(D.Q, D.Q, G, ncclFloat, ncclSum, (ncclComm_t)D.comm, st));
   mark(2);
-  {
+  if (D.slab_world > 1) {
+    if (D.world > 1) slab_conv_nccl(D, st);
+    else slab_conv_sim(D, st);
+  } else {
     const int n0 = D.n[0], n1 = D.n[1], n2 = D.n[2], P0 = D.P[0], P1 = D.P[1], P2 = D.P[2], H0 = D.H0;
     launch_x<float>(true, D.Q, D.C, nullptr, n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
     if (D.fused_tile) {
@@ -766,12 +1052,11 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   }
   halo(D, 1, D.q, 1, st);
   mark(3);
-  const int4* c4 = reinterpret_cast<const int4*>(D.c_col);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
   k4_interp_corr<PP, GG><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, \
-                                                                             c4, v4, D.q, D.uloc, D.u)
+                                                                             D.c_hdr, v4, D.q, D.uloc, D.u)
 #define K4_BY_G(PP)                                                                                     \
   (D.k4_group == 8 ? K4_LAUNCH(PP, 8) : D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
     case 1: K4_BY_G(1); break;

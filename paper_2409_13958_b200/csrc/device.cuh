@@ -25,13 +25,19 @@ struct DeviceState {
   float4* s_Gc = nullptr;      // (Gx, Gy, Gz, column bits) for the first sl1 width entries
   float4* m4 = nullptr;        // [N'] internal float4 copy of m (one 16-byte gather per entry)
   float4* rowsum = nullptr;    // [N'][2] (sum_m D_nm, 0), (sum_m Z_nm, 0)
-  // C_box, CSR with rows padded to a multiple of 4 entries (col = row, val = 0)
-  int64_t* c_ptr = nullptr;   int32_t* c_col = nullptr;
-  float* c_val = nullptr;
-  int64_t cbox_nnz = 0;       // unpadded entries
+  // C_box in the C4x format (cbox_gpu.cu): per row a range of chunks of 4 column-sorted
+  // entries; per chunk 4 fp32 values + a 64-bit header (base column, three 12-bit deltas)
+  int64_t* c_ptr = nullptr;           // [N'+1] chunk offsets
+  unsigned long long* c_hdr = nullptr;
+  float* c_val = nullptr;             // [chunks][4]
+  int64_t cbox_nnz = 0;               // near pairs (entries without chunk padding)
+  int64_t cbox_chunks = 0;
   int k4_group = 32;          // lanes per row in K4 (8/16/32 from the mean padded row length)
   // stencils
   int4* st_s = nullptr;       // wrapped (periodic) / clamped anchors
+  int32_t* box_ptr = nullptr; // [G+1] first internal row of each anchor box (rows are box-sorted)
+  int k2_tile[3] = {8, 8, 8}; // K2 grid tile per axis (divides n)
+  int box_max = 1;            // largest anchor-box population (K2 fixed-point bound)
 
   float4* st_t = nullptr;     // local coordinates t - s
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32
@@ -48,6 +54,11 @@ struct DeviceState {
   float* Q = nullptr;         // real grid [n2][n1][n0] (also holds U after the inverse)
   float2* C = nullptr;        // complex half spectrum [P2][P1][H0]
   float* m_stage = nullptr;   // pmfem_heff_host staging
+  // slab-decomposed convolution (world > 1, or PMFEM_SLAB_SIM=W simulated ranks on one device)
+  int slab_world = 1;
+  float2* slab_cx = nullptr;  // x-slab spectrum [P2][P1][H_r] (simulation: all ranks back to back)
+  float2* slab_buf = nullptr; // transpose send / receive blocks [nzl][P1][H0]
+  float* slab_spec = nullptr; // spectrum slice [P2][P1][H_r]
   float* H_stage = nullptr;
   // timing
   bool timing = false;

@@ -220,12 +220,24 @@ __global__ void fft_strided(typename Cx<T>::t* __restrict__ data, int P, int log
   smem_fft<C>(buf, P, logP, TILE, TileBase{}, TILE, tw, 1, mode == 1, true);
   if (mode == 2) {
     const T* sp = spec + (long long)blockIdx.y * spec_plane_stride + c0;
-    for (int idx = threadIdx.x; idx < P * TILE; idx += blockDim.x) {
-      const int e = idx / TILE, c = idx - e * TILE;
-      const T g = (c < nc) ? sp[e * spec_es + c] : T(0);
-      C v = buf[e * TILE + c];
-      v.x *= g; v.y *= g;
-      buf[e * TILE + c] = v;
+    constexpr int SB = 8;
+    for (int base = threadIdx.x; base < P * TILE; base += SB * blockDim.x) {
+      T gv[SB];
+#pragma unroll
+      for (int b = 0; b < SB; ++b) {
+        const int idx = base + b * blockDim.x;
+        const int e = idx / TILE, c = idx - e * TILE;
+        gv[b] = (idx < P * TILE && c < nc) ? __ldg(sp + e * spec_es + c) : T(0);
+      }
+#pragma unroll
+      for (int b = 0; b < SB; ++b) {
+        const int idx = base + b * blockDim.x;
+        if (idx < P * TILE) {
+          C v = buf[idx];
+          v.x *= gv[b]; v.y *= gv[b];
+          buf[idx] = v;
+        }
+      }
     }
     __syncthreads();
     smem_bitrev<C>(buf, P, logP, TILE, TileBase{}, TILE);
@@ -277,14 +289,28 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   // forward z on every (k1, c): base = k1*tile + c, stride pl
   const TileBase zbase{};
   smem_fft<C>(buf, P2, logP2, nzl, zbase, pl, tw2, 1, false, true);
-  // multiply by the real spectrum G_hat[k2][k1][k0] (natural order now)
-  for (int idx = threadIdx.x; idx < P2 * nzl; idx += blockDim.x) {
-    const int c = idx & (tile - 1), r = idx >> ltile, k1 = r & (P1 - 1), k2 = r >> logP1;
-    const T g = (c < nc) ? spec[((long long)k2 * P1 + k1) * H0 + c0 + c] : T(0);
-    C* pv = buf + k2 * pl + k1 * tile + c;
-    C v = *pv;
-    v.x *= g; v.y *= g;
-    *pv = v;
+  // multiply by the real spectrum G_hat[k2][k1][k0] (natural order now); the spectrum loads
+  // are issued 8 at a time per thread so their latency overlaps
+  constexpr int SB = 8;
+  for (int base = threadIdx.x; base < P2 * nzl; base += SB * blockDim.x) {
+    T gv[SB];
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const int idx = base + b * blockDim.x;
+      const int c = idx & (tile - 1), r = idx >> ltile, k1 = r & (P1 - 1), k2 = r >> logP1;
+      gv[b] = (idx < P2 * nzl && c < nc) ? __ldg(spec + ((long long)k2 * P1 + k1) * H0 + c0 + c) : T(0);
+    }
+#pragma unroll
+    for (int b = 0; b < SB; ++b) {
+      const int idx = base + b * blockDim.x;
+      if (idx < P2 * nzl) {
+        const int c = idx & (tile - 1), r = idx >> ltile, k1 = r & (P1 - 1), k2 = r >> logP1;
+        C* pv = buf + k2 * pl + k1 * tile + c;
+        C v = *pv;
+        v.x *= gv[b]; v.y *= gv[b];
+        *pv = v;
+      }
+    }
   }
   __syncthreads();
   // inverse z (bit-reverse first); only planes i2 < n2 are needed afterwards

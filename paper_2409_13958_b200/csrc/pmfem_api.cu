@@ -300,6 +300,8 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
   out->bytes_per_eval_algorithmic = tot;
   out->launches_per_eval = ctx->D.launches_per_eval;
   out->fft_fused = ctx->D.fused_tile > 0;
+  for (int a = 0; a < 3; ++a) out->k2_tile[a] = ctx->D.k2_tile[a];
+  out->slab_world = ctx->D.slab_world;
   out->comm_bytes_per_eval = ctx->D.comm_bytes_per_eval;
   out->setup_seconds = S.setup_seconds;
   out->pgf_seconds = S.pgf_seconds;
@@ -345,18 +347,34 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     else if (n == "perm") put(S.perm.data(), S.Np, 8);
     else if (n == "dist_bounds") put(S.dist.bounds.data(), (int64_t)S.dist.bounds.size(), 8);
     else if (n.rfind("cbox_device_", 0) == 0) {
-      // the device-built C_box (internal order, rows padded to 4), copied back for tests
+      // the device-built C_box (internal order), decoded from its C4x chunks for tests: every
+      // chunk slot is returned (padding slots repeat the previous column with value 0)
       pmfem::require(!ctx->host_only && S.cbox_device, PMFEM_E_STATE, "C_box was not built on the device");
       const pmfem::DeviceState& D = ctx->D;
       std::vector<int64_t> ptr(S.Np + 1);
       cudaMemcpy(ptr.data(), D.c_ptr, sizeof(int64_t) * (S.Np + 1), cudaMemcpyDeviceToHost);
       const std::string tail = n.substr(12);
-      if (tail == "rowptr") put(ptr.data(), S.Np + 1, 8);
-      else if (tail == "col" || tail == "val") {
-        *count = ptr[S.Np];
-        if (dst && ptr[S.Np])
-          cudaMemcpy(dst, tail == "col" ? (const void*)D.c_col : (const void*)D.c_val, 4 * (size_t)ptr[S.Np],
-                     cudaMemcpyDeviceToHost);
+      const int64_t nch = ptr[S.Np];
+      if (tail == "rowptr") {
+        for (auto& v : ptr) v *= 4;
+        put(ptr.data(), S.Np + 1, 8);
+      } else if (tail == "val") {
+        *count = 4 * nch;
+        if (dst && nch) cudaMemcpy(dst, D.c_val, sizeof(float) * 4 * (size_t)nch, cudaMemcpyDeviceToHost);
+      } else if (tail == "col") {
+        *count = 4 * nch;
+        if (dst && nch) {
+          std::vector<unsigned long long> h(nch);
+          cudaMemcpy(h.data(), D.c_hdr, sizeof(unsigned long long) * (size_t)nch, cudaMemcpyDeviceToHost);
+          int32_t* c = static_cast<int32_t*>(dst);
+          for (int64_t i = 0; i < nch; ++i) {
+            int32_t k = (int32_t)(h[i] & 0xFFFFFFFull);
+            c[4 * i] = k;
+            for (int j = 0; j < 3; ++j) { k += (int32_t)((h[i] >> (28 + 12 * j)) & 0xFFF); c[4 * i + 1 + j] = k; }
+          }
+        }
+      } else if (tail == "chunks") {
+        put(&D.cbox_chunks, 1, 8);
       } else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
     }
     else if (n.rfind("send_", 0) == 0 || n.rfind("recv_", 0) == 0) {

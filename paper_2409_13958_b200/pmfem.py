@@ -58,7 +58,8 @@ class _Info(ctypes.Structure):
                 ("bytes_per_eval_algorithmic", ctypes.c_double), ("setup_seconds", ctypes.c_double),
                 ("pgf_seconds", ctypes.c_double), ("kernel_bytes", ctypes.c_double * 8),
                 ("launches_per_eval", ctypes.c_int32), ("fft_fused", ctypes.c_int32),
-                ("comm_bytes_per_eval", ctypes.c_double)]
+                ("comm_bytes_per_eval", ctypes.c_double), ("k2_tile", ctypes.c_int32 * 3),
+                ("slab_world", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p
@@ -208,7 +209,7 @@ class Context:
         info = _Info()
         self._check(_lib.pmfem_query(self._h, ctypes.byref(info)))
         out = {k: getattr(info, k) for k, _ in _Info._fields_}
-        for k in ("grid", "fft", "kernel_bytes"):
+        for k in ("grid", "fft", "kernel_bytes", "k2_tile"):
             out[k] = list(out[k])
         return out
 

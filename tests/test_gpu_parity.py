@@ -159,3 +159,35 @@ def test_k4_group_sizes(group, monkeypatch):
     rank = ctx.internal_to_parent_rank()
     m = m_random(om.n_parents, seed=41)
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+
+
+@pytest.mark.parametrize("key,tile", [("C2p2", "1,1,1"), ("C2p2", "32,32,4"), ("C2p2", "4,2,4"),
+                                      ("C3p1", "2,8,1"), ("C4p3", "2,2,2"), ("C4p3", "16,16,16"),
+                                      ("C5p2", "128,1,2"), ("C1r0", "8,1,16")])
+def test_k2_tile_shapes(key, tile, monkeypatch):
+    """K2's grid tiles (smaller than the stencil, a whole periodic axis, a whole padded
+    non-periodic axis, single points) partition the grid: every shape gives the oracle's field."""
+    monkeypatch.setenv("PMFEM_K2_TILE", tile)
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    assert ctx.query()["k2_tile"] == [int(v) for v in tile.split(",")]
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=51)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+
+
+@pytest.mark.parametrize("key,world", [("C1r0", 2), ("C1r0", 4), ("C2p2", 2), ("C2p2", 4), ("C3p1", 4),
+                                       ("C3p1", 8), ("C4p3", 8), ("C5p2", 4)])
+def test_slab_fft_simulated_ranks(key, world, monkeypatch):
+    """Slab-decomposed convolution: z slabs for X/Y, k0 slabs for Z * G_hat, two
+    transposes.  PMFEM_SLAB_SIM=W runs every rank's passes on this device with the transposes as
+    device copies of exactly the blocks the NCCL path sends (uneven k0 splits included)."""
+    monkeypatch.setenv("PMFEM_SLAB_SIM", str(world))
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    assert ctx.query()["slab_world"] == world
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=61)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
