@@ -277,8 +277,22 @@ def main():
         kernels[k] = {"ms": ms, "bytes": kb[i], "GBps": kb[i] / (ms * 1e-3) / 1e9 if ms > 0 else None}
     dom = max(KERNELS, key=lambda k: kernels[k]["ms"])
     ach = kernels[dom]["GBps"]
+    for k in KERNELS:
+        if kernels[k]["GBps"] is not None:
+            kernels[k]["frac_hbm"] = kernels[k]["GBps"] / peaks["hbm_gbs"]
+    # traffic: DRAM bytes per launch of the dominant kernel from the committed ncu --set full
+    # capture of this config (profiles/traffic.json, written by scripts/ncu_traffic.py)
+    traffic, traffic_src = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(a.config, {}).get(dom)
+        if tr is not None and world == 1:
+            traffic, traffic_src = tr["dram_bytes"], "%s (%s)" % (tr["report"], tr["note"])
+    except Exception:
+        pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
+                "frac": ach / peaks["hbm_gbs"], "traffic": traffic, "traffic_source": traffic_src,
+                "algorithmic_bytes": kb[KERNELS.index(dom)], "peak_source": peak_src,
                 "share_of_step": kernels[dom]["ms"] / float(np.mean(step_ms))}
     alg_total = sum(kb[:5])
     line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": world, "steps": a.steps,
@@ -289,8 +303,11 @@ def main():
                        "nnz_ring1": info["nnz_ring1"], "nnz_z0": info["nnz_z0"], "nnz_cbox": info["nnz_cbox"],
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": "single GPU" if world == 1 else
-                       "slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + all-reduce of the "
-                       "anterpolated grid, replicated FFT" % world, "n_parents_local": Nloc},
+                       ("slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + slab-decomposed FFT "
+                        "(reduce-scatter, 2 all-to-all transposes, all-gather)" % world if info["slab_world"] > 1 else
+                        "slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + all-reduce of the "
+                        "anterpolated grid, replicated FFT" % world), "n_parents_local": Nloc,
+                       "k2_tile": info["k2_tile"]},
             "nodes_per_s": value * Np, "setup_s": t_setup, "build_pgf_s": t_pgf,
             "bytes_per_eval_algorithmic": alg_total,
             "eval_GBps_algorithmic": alg_total / (tot_ms / a.steps * 1e-3) / 1e9,
