@@ -87,7 +87,7 @@ __global__ void k_to_m4(RowRange rr, const float* __restrict__ m, float4* __rest
   m4[n] = make_float4(m[3 * h], m[3 * h + 1], m[3 * h + 2], 0.f);
 }
 
-__global__ void __launch_bounds__(256) k1_local_in(
+__global__ void __launch_bounds__(256, 5) k1_local_in(
     RowRange rr, const float4* __restrict__ m4, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
     const float4* __restrict__ s_zc, const float4* __restrict__ s_LD, const float4* __restrict__ rowsum,
     float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H, int write_hex) {
@@ -332,18 +332,30 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
   const int64_t b = valid ? c_ptr[n] : 0, e_end = valid ? c_ptr[n + 1] : 0;
-#pragma unroll 2
-  for (int64_t e = b + lane; e < e_end; e += G) {
-    const unsigned long long h = __ldg(c_hdr + e);
-    const float4 vv = __ldg(c_val4 + e);
-    const int k0 = (int)(h & 0xFFFFFFFull);
-    const int k1 = k0 + (int)((h >> 28) & 0xFFF);
-    const int k2 = k1 + (int)((h >> 40) & 0xFFF);
-    const int k3 = k2 + (int)(h >> 52);
-    acc = fmaf(vv.x, q[k0], acc);
-    acc = fmaf(vv.y, q[k1], acc);
-    acc = fmaf(vv.z, q[k2], acc);
-    acc = fmaf(vv.w, q[k3], acc);
+  // batches of 4 chunks per lane: all header/value loads of a batch are issued before its
+  // gathers, so each lane keeps 8 streaming loads and then 16 gathers in flight
+  constexpr int UB = 4;
+  for (int64_t e0 = b + lane; e0 < e_end; e0 += UB * G) {
+    unsigned long long h[UB];
+    float4 vv[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int64_t e = e0 + (int64_t)u * G;
+      if (e < e_end) { h[u] = __ldg(c_hdr + e); vv[u] = __ldg(c_val4 + e); }
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      if (e0 + (int64_t)u * G < e_end) {
+        const int k0 = (int)(h[u] & 0xFFFFFFFull);
+        const int k1 = k0 + (int)((h[u] >> 28) & 0xFFF);
+        const int k2 = k1 + (int)((h[u] >> 40) & 0xFFF);
+        const int k3 = k2 + (int)(h[u] >> 52);
+        acc = fmaf(vv[u].x, __ldg(q + k0), acc);
+        acc = fmaf(vv[u].y, __ldg(q + k1), acc);
+        acc = fmaf(vv[u].z, __ldg(q + k2), acc);
+        acc = fmaf(vv[u].w, __ldg(q + k3), acc);
+      }
+    }
   }
   // interpolation: lane r < (P+1)^2 takes one (y, z) stencil row and its P+1 x-consecutive
   // grid values (index maths once per row, not per point)
@@ -468,19 +480,34 @@ void twiddles(int P, std::vector<typename Cx<T>::t>& tw) {
   }
 }
 
-constexpr int TILE = 16;
+template <class T, int TL>
+void launch_strided_t(typename Cx<T>::t* data, int P, long long es, int ncol, int nplanes, long long plane_stride,
+                      int nin, int nout, int mode, const T* spec, long long spec_es, long long spec_ps,
+                      const typename Cx<T>::t* tw, cudaStream_t st) {
+  using C = typename Cx<T>::t;
+  size_t smem = (size_t)P * (TL + 1) * sizeof(C);                   // lines + twiddle table
+  auto kern = fft_strided<T, TL>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((ncol + TL - 1) / TL, nplanes);
+  // a thread holds FftBudget<C>::V values per Stockham pass: TL * P <= V * threads
+  const int threads = std::max(128, (TL * P / FftBudget<C>::V + 31) / 32 * 32);
+  kern<<<grid, threads, smem, st>>>(data, P, ilog2(P), es, ncol, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw);
+  CK(cudaGetLastError());
+}
 
+// column tile: 16 columns while the CTA stays at <= 256 threads (~100-130 registers each),
+// fewer columns for long lines
 template <class T>
 void launch_strided(typename Cx<T>::t* data, int P, long long es, int ncol, int nplanes, long long plane_stride,
                     int nin, int nout, int mode, const T* spec, long long spec_es, long long spec_ps,
                     const typename Cx<T>::t* tw, cudaStream_t st) {
   using C = typename Cx<T>::t;
-  size_t smem = (size_t)P * TILE * sizeof(C);
-  auto kern = fft_strided<T, TILE>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((ncol + TILE - 1) / TILE, nplanes);
-  kern<<<grid, 256, smem, st>>>(data, P, ilog2(P), es, ncol, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw);
-  CK(cudaGetLastError());
+  const int cap = 256 * FftBudget<C>::V;               // TL * P <= cap
+  if (16 * P <= cap) launch_strided_t<T, 16>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
+  else if (8 * P <= cap) launch_strided_t<T, 8>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
+  else if (4 * P <= cap) launch_strided_t<T, 4>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
+  else if (2 * P <= cap) launch_strided_t<T, 2>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
+  else throw Error(PMFEM_E_INVALID_ARG, "FFT length too large for one CTA");
 }
 
 template <class T>
@@ -490,11 +517,13 @@ void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows
   const int M = P0 / 2;
   // lines per CTA: enough CTAs to cover 2 waves of 148 SMs, at most 4096 complex per CTA
   int nl = std::max(1, std::min(4096 / std::max(M, 1), nrows / 296));
-  size_t smem = (size_t)nl * M * sizeof(C);
+  size_t smem = ((size_t)nl * (M + 1) + M) * sizeof(C);              // padded lines + twiddle table
   RowMap rm{n1, P1};
   int blocks = (nrows + nl - 1) / nl;
-  int threads = std::min(256, std::max(64, nl * M / 2));
+  // a thread holds FftBudget<C>::V values per Stockham pass: nl * M <= V * threads
+  int threads = std::max(64, (nl * M + FftBudget<C>::V - 1) / FftBudget<C>::V);
   threads = (threads + 31) / 32 * 32;
+  if (threads > 1024) throw Error(PMFEM_E_INVALID_ARG, "FFT length too large for one CTA");
   if (fwd) {
     auto kern = fft_x_forward<T>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -542,10 +571,11 @@ __global__ void k_spec_slice(const float* __restrict__ spec, float* __restrict__
 
 void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
   const int tile = D.fused_tile, P1 = D.P[1], P2 = D.P[2];
-  size_t smem = (size_t)P2 * (P1 * tile + (tile == 1 ? 1 : 0)) * sizeof(float2);   // padded planes
+  size_t smem = ((size_t)P2 * (P1 * tile + 1) + std::max(P1, P2)) * sizeof(float2);   // padded planes + twiddles
   auto kern = fft_yz_fused<float>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int threads = std::min(512, std::max(128, P1 * P2 * tile / 4));
+  // a thread holds 32 values per Stockham pass: P1 * P2 * tile <= 32 * threads
+  int threads = std::max(128, P1 * P2 * tile / 32);
   threads = (threads + 31) / 32 * 32;
   kern<<<(D.H0 + tile - 1) / tile, threads, smem, st>>>(D.C, D.n[1], P1, ilog2(P1), D.n[2], P2, ilog2(P2), D.H0,
                                                          tile, D.spec, D.tw32[1], D.tw32[2]);
@@ -714,9 +744,13 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     const size_t plane_bytes = (size_t)(D.P[1] + 1) * D.P[2] * sizeof(float2);
     D.fused_tile = 0;
     // PMFEM_FFT_SPLIT=1 forces the split plan (tests exercise it on small grids)
-    if (plane_bytes <= 200 * 1024 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {
+    // (<= 16384 complex per CTA: 512 threads x 32 values per Stockham pass, ~96 registers each)
+    const int64_t plane = (int64_t)D.P[1] * D.P[2];
+    if (plane_bytes <= 200 * 1024 && plane <= 16384 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {
       int tile = 1;
-      while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && (D.H0 + 2 * tile - 1) / (2 * tile) >= 148) tile *= 2;
+      while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && plane * tile * 2 <= 16384 &&
+             (D.H0 + 2 * tile - 1) / (2 * tile) >= 148)
+        tile *= 2;
       D.fused_tile = tile;
     }
   }

@@ -1,0 +1,10 @@
+# round-1 session 3: Stockham radix-8 FFT passes, K4 batched chunk loads, K1 launch bounds
+set -x
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py > gpurun_out/bench_c2.log 2>&1; echo bench=$?
+timeout 900 python bench.py --config C3 --steps 20 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1; echo c3=$?
+timeout 900 python bench.py --config C5 --steps 20 --no-cpu-baseline > gpurun_out/bench_c5.log 2>&1; echo c5=$?
+for k in k4_interp fft_yz fft_x_forward; do
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 -o gpurun_out/prof_c3_$k -f python scripts/profile_eval.py --config C3 --evals 2 > gpurun_out/ncu_c3_$k.log 2>&1; echo full3_$k=$?
+done
