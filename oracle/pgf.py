@@ -20,14 +20,20 @@ EULER_GAMMA = 0.57721566490153286061
 
 
 class PgfSpec:
-    """Periodic axes + periods.  ``axes`` lists the periodic axes (len 1, 2 or 3)."""
+    """Periodic axes + periods.  ``axes`` lists the periodic axes (len 1, 2 or 3; 0 = the
+    non-periodic free-space kernel of NEXT-3)."""
 
     def __init__(self, periodic, lattice, alpha=None, tol=1e-15):
         self.axes = [a for a in range(3) if periodic[a]]
         self.free = [a for a in range(3) if not periodic[a]]
         self.dim = len(self.axes)
         if self.dim == 0:
-            raise ValueError("non-periodic PGF is out of scope (NEXT-3)")
+            # non-periodic mode (SURVEY 8(f) NEXT-3): the free-space kernel G0 = 1/|r| (P:188),
+            # no images, regularised self value 0
+            self.L = np.zeros(0)
+            self.alpha = None
+            self.n_real, self.m_recip = [], []
+            return
         self.L = np.array([float(lattice[a]) for a in self.axes])
         self.alpha = alpha if alpha is not None else math.sqrt(math.pi) / self.L.min()
         # cutoffs: erfc(x) < tol for x > xr; exp(-k^2/4a^2) < tol for k > kr
@@ -109,6 +115,9 @@ def pgf_self(spec):
 
 
 def _pgf(r, spec, self_term):
+    if spec.dim == 0:
+        # free space: G0(r) = 1/|r|; lim_{r->0} [G0(r) - 1/r] = 0
+        return np.zeros(r.shape[0]) if self_term else 1.0 / np.linalg.norm(r, axis=1)
     a = spec.alpha
     rp = np.stack([_wrap_half(r[:, ax], spec.L[i]) for i, ax in enumerate(spec.axes)], axis=1)
     rf = r[:, spec.free] if spec.free else np.zeros((r.shape[0], 0))

@@ -87,7 +87,7 @@ __global__ void k_to_m4(RowRange rr, const float* __restrict__ m, float4* __rest
   m4[n] = make_float4(m[3 * h], m[3 * h + 1], m[3 * h + 2], 0.f);
 }
 
-__global__ void __launch_bounds__(256, 5) k1_local_in(
+__global__ void __launch_bounds__(256) k1_local_in(
     RowRange rr, const float4* __restrict__ m4, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
     const float4* __restrict__ s_zc, const float4* __restrict__ s_LD, const float4* __restrict__ rowsum,
     float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H, int write_hex) {
@@ -332,30 +332,18 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
   const int64_t b = valid ? c_ptr[n] : 0, e_end = valid ? c_ptr[n + 1] : 0;
-  // batches of 4 chunks per lane: all header/value loads of a batch are issued before its
-  // gathers, so each lane keeps 8 streaming loads and then 16 gathers in flight
-  constexpr int UB = 4;
-  for (int64_t e0 = b + lane; e0 < e_end; e0 += UB * G) {
-    unsigned long long h[UB];
-    float4 vv[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int64_t e = e0 + (int64_t)u * G;
-      if (e < e_end) { h[u] = __ldg(c_hdr + e); vv[u] = __ldg(c_val4 + e); }
-    }
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      if (e0 + (int64_t)u * G < e_end) {
-        const int k0 = (int)(h[u] & 0xFFFFFFFull);
-        const int k1 = k0 + (int)((h[u] >> 28) & 0xFFF);
-        const int k2 = k1 + (int)((h[u] >> 40) & 0xFFF);
-        const int k3 = k2 + (int)(h[u] >> 52);
-        acc = fmaf(vv[u].x, __ldg(q + k0), acc);
-        acc = fmaf(vv[u].y, __ldg(q + k1), acc);
-        acc = fmaf(vv[u].z, __ldg(q + k2), acc);
-        acc = fmaf(vv[u].w, __ldg(q + k3), acc);
-      }
-    }
+#pragma unroll 2
+  for (int64_t e = b + lane; e < e_end; e += G) {
+    const unsigned long long h = __ldg(c_hdr + e);
+    const float4 vv = __ldg(c_val4 + e);
+    const int k0 = (int)(h & 0xFFFFFFFull);
+    const int k1 = k0 + (int)((h >> 28) & 0xFFF);
+    const int k2 = k1 + (int)((h >> 40) & 0xFFF);
+    const int k3 = k2 + (int)(h >> 52);
+    acc = fmaf(vv.x, q[k0], acc);
+    acc = fmaf(vv.y, q[k1], acc);
+    acc = fmaf(vv.z, q[k2], acc);
+    acc = fmaf(vv.w, q[k3], acc);
   }
   // interpolation: lane r < (P+1)^2 takes one (y, z) stencil row and its P+1 x-consecutive
   // grid values (index maths once per row, not per point)
@@ -490,7 +478,8 @@ void launch_strided_t(typename Cx<T>::t* data, int P, long long es, int ncol, in
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((ncol + TL - 1) / TL, nplanes);
   // a thread holds FftBudget<C>::V values per Stockham pass: TL * P <= V * threads
-  const int threads = std::max(128, (TL * P / FftBudget<C>::V + 31) / 32 * 32);
+  // (~16 values per thread, at most 256 threads: ~100-130 registers each)
+  const int threads = std::max(128, std::min(256, (TL * P / 16 + 31) / 32 * 32));
   kern<<<grid, threads, smem, st>>>(data, P, ilog2(P), es, ncol, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw);
   CK(cudaGetLastError());
 }
@@ -517,11 +506,14 @@ void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows
   const int M = P0 / 2;
   // lines per CTA: enough CTAs to cover 2 waves of 148 SMs, at most 4096 complex per CTA
   int nl = std::max(1, std::min(4096 / std::max(M, 1), nrows / 296));
+  while (nl & (nl - 1)) nl &= nl - 1;                                // power of two (line-fast shifts)
   size_t smem = ((size_t)nl * (M + 1) + M) * sizeof(C);              // padded lines + twiddle table
   RowMap rm{n1, P1};
   int blocks = (nrows + nl - 1) / nl;
   // a thread holds FftBudget<C>::V values per Stockham pass: nl * M <= V * threads
-  int threads = std::max(64, (nl * M + FftBudget<C>::V - 1) / FftBudget<C>::V);
+  // (and ~8 values per thread for latency hiding, at most 512 threads)
+  int threads = std::max(64, std::min(512, nl * M / 8));
+  threads = std::max(threads, (nl * M + FftBudget<C>::V - 1) / FftBudget<C>::V);
   threads = (threads + 31) / 32 * 32;
   if (threads > 1024) throw Error(PMFEM_E_INVALID_ARG, "FFT length too large for one CTA");
   if (fwd) {
@@ -575,7 +567,9 @@ void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
   auto kern = fft_yz_fused<float>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   // a thread holds 32 values per Stockham pass: P1 * P2 * tile <= 32 * threads
-  int threads = std::max(128, P1 * P2 * tile / 32);
+  // (~8 values per thread for latency hiding, at most 512 threads at ~96 registers)
+  int threads = std::max(128, std::min(512, P1 * P2 * tile / 8));
+  threads = std::max(threads, P1 * P2 * tile / 32);
   threads = (threads + 31) / 32 * 32;
   kern<<<(D.H0 + tile - 1) / tile, threads, smem, st>>>(D.C, D.n[1], P1, ilog2(P1), D.n[2], P2, ilog2(P2), D.H0,
                                                          tile, D.spec, D.tw32[1], D.tw32[2]);

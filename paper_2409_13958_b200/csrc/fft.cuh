@@ -96,13 +96,16 @@ __device__ __forceinline__ void sk_pass(C* buf, int P, int logP, int logNs, int 
   const int logT = logP - LR, T = 1 << logT;
   const int items = nl << logT;
   const int Ns = 1 << logNs;
+  const int lnl = (nl & (nl - 1)) == 0 ? __ffs(nl) - 1 : -1;       // log2(nl) if a power of two
   C v[IT][R];
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const int w = threadIdx.x + it * blockDim.x;
     if (w < items) {
       int l, j;
-      if (LF) { l = w % nl; j = w / nl; } else { j = w & (T - 1); l = w >> logT; }
+      if (LF) {
+        if (lnl >= 0) { l = w & (nl - 1); j = w >> lnl; } else { l = w % nl; j = w / nl; }
+      } else { j = w & (T - 1); l = w >> logT; }
       const C* p = buf + base(l);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -118,7 +121,9 @@ __device__ __forceinline__ void sk_pass(C* buf, int P, int logP, int logNs, int 
     const int w = threadIdx.x + it * blockDim.x;
     if (w < items) {
       int l, j;
-      if (LF) { l = w % nl; j = w / nl; } else { j = w & (T - 1); l = w >> logT; }
+      if (LF) {
+        if (lnl >= 0) { l = w & (nl - 1); j = w >> lnl; } else { l = w % nl; j = w / nl; }
+      } else { j = w & (T - 1); l = w >> logT; }
       const int k = j & (Ns - 1);
       if (logNs > 0) {
         // W_{Ns R}^{r k} = W_P^{r k P / (Ns R)}

@@ -78,6 +78,8 @@ PM_HD inline double pm_incbessel(const PgfDev& P, double a, double b) {
 // r given in cartesian components; self = true returns G_reg(0) (r ignored).
 PM_HD inline double pgf_eval(const PgfDev& P, const double r_in[3], bool self) {
   const double pi = 3.14159265358979323846;
+  if (P.dim == 0)   // non-periodic mode (NEXT-3): G0 = 1/|r|, regularised self value 0
+    return self ? 0.0 : 1.0 / sqrt(r_in[0] * r_in[0] + r_in[1] * r_in[1] + r_in[2] * r_in[2]);
   const double a = P.alpha;
   double rp[3] = {0, 0, 0}, rf[2] = {0, 0};
   for (int i = 0; i < P.dim; ++i) {

@@ -41,7 +41,7 @@ PgfParams make_pgf_params(const int periodic[3], const double L[3]) {
     if (!periodic[a]) P.ax[k++] = a;
   double Lmin = 1e300;
   for (int i = 0; i < P.dim; ++i) Lmin = std::min(Lmin, P.L[i]);
-  P.alpha = std::sqrt(M_PI) / Lmin;
+  P.alpha = P.dim > 0 ? std::sqrt(M_PI) / Lmin : 1.0;   // dim 0: free space, alpha unused
   const double kmax = 2.0 * P.alpha * std::sqrt(-std::log(1e-15)) * 1.1;
   for (int i = 0; i < 3; ++i) {
     if (i < P.dim) {

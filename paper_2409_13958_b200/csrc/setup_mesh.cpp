@@ -95,7 +95,7 @@ void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* p
     if (S.periodic[a]) require(S.L[a] > 0, PMFEM_E_INVALID_ARG, "non-positive period");
     nper += S.periodic[a];
   }
-  require(nper >= 1, PMFEM_E_INVALID_ARG, "at least one periodic axis is required (non-periodic mode is NEXT-3)");
+  (void)nper;   // nper == 0: non-periodic mode, free-space kernel, 2N padding on every axis
 
   // materials per tet
   S.Ms_tet.resize(S.T);

@@ -19,6 +19,9 @@ CONFIGS = {
     "C3": "1D-periodic nanowire segments (non-touching), ~1M nodes, 512x64x64 AIM grid",
     "C4": "3D-periodic BCC spheres protruding beyond the cell, ~10M nodes, 256^3 AIM grid",
     "C5": "1D-periodic waveguide strip (touching), ~2M nodes, 2048x64x8 AIM grid",
+    # non-periodic mode: not a BASELINE.json workload
+    "N1": "non-periodic isolated cube, ~1k nodes, 16^3 AIM grid (32^3 FFT)",
+    "N2": "non-periodic isolated sphere, ~30k nodes, 32^3 AIM grid (64^3 FFT)",
 }
 
 
@@ -29,7 +32,7 @@ def _round_cells(length, h):
 def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
     """Return dict(mesh, periodic, L, grid, Ms, Aex, name, desc)."""
     if seed is None:
-        seed = 1000 + int(name[1:])
+        seed = (1000 if name[0] == "C" else 2000) + int(name[1:])
     c = float(coarsen)
     if name == "C1":
         L = 100 * NM
@@ -92,6 +95,26 @@ def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
         mesh = kuhn_voxel_mesh(mask, h, wrap=(True, False, False), jitter=jitter, seed=seed, name=name)
         periodic = (1, 0, 0); lattice = (L, 0.0, 0.0)
         g = grid or (max(16, int(2048 // c)), max(8, int(64 // c)), max(4, int(round(8 / c))))
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "N1":
+        L = 100 * NM
+        n = cells or max(2, int(round(10 / c)))
+        h = L / n
+        mask = np.ones((n, n, n), bool)
+        mesh = kuhn_voxel_mesh(mask, h, wrap=(False, False, False), jitter=jitter, seed=seed, name=name)
+        periodic = (0, 0, 0); lattice = (0.0, 0.0, 0.0)
+        g = grid or (max(8, int(16 // c)),) * 3
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "N2":
+        R = 60 * NM; h = 4 * NM * c
+        n = int(math.ceil(R / h))
+        cc = (np.arange(-n, n) + 0.5) * h
+        X, Y, Z = np.meshgrid(cc, cc, cc, indexing="ij")
+        keep = X ** 2 + Y ** 2 + Z ** 2 <= R * R
+        mesh = kuhn_voxel_mesh(keep, h, origin=(-n * h,) * 3, wrap=(False, False, False),
+                               jitter=jitter, seed=seed, name=name)
+        periodic = (0, 0, 0); lattice = (0.0, 0.0, 0.0)
+        g = grid or (max(8, int(32 // c)),) * 3
         Ms, Aex = 637.0, 1.4e-6
     else:
         raise KeyError(name)

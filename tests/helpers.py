@@ -13,6 +13,8 @@ SMALL = {
     "C3p1": dict(cfg=("C3", 12), grid=(64, 8, 8), order=1, s=2.0, ring=0),
     "C4p3": dict(cfg=("C4", 40), grid=(16, 16, 16), order=3, s=1.5, ring=0),
     "C5p2": dict(cfg=("C5", 16), grid=(128, 8, 4), order=2, s=2.0, ring=0),
+    # non-periodic mode (NEXT-3): isolated cube, free-space kernel, 2N padding on every axis
+    "N1p2": dict(cfg=("N1", 2), grid=(16, 16, 16), order=2, s=2.0, ring=1),
 }
 
 

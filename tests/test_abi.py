@@ -33,9 +33,9 @@ def test_error_path_no_gpu():
     xyz = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float)
     tets = np.array([[0, 1, 2, 3]])
     try:
-        Context(xyz, tets, (0, 0, 0), (0, 0, 0), (8, 8, 8), device=-1)
+        Context(xyz, tets, (1, 0, 0), (0, 0, 0), (8, 8, 8), device=-1)
     except PmfemError as e:
-        assert e.status == 1 and "periodic" in str(e)
+        assert e.status == 1 and "period" in str(e)
     else:
         raise AssertionError("expected PMFEM_E_INVALID_ARG")
     try:
