@@ -307,7 +307,9 @@ def main():
                         "(reduce-scatter, 2 all-to-all transposes, all-gather)" % world if info["slab_world"] > 1 else
                         "slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + all-reduce of the "
                         "anterpolated grid, replicated FFT" % world), "n_parents_local": Nloc,
-                       "k2_tile": info["k2_tile"]},
+                       "k2_tile": info["k2_tile"],
+                       "cbox_format": ["C4x", "B4"][info["cbox_format"]],
+                       "cbox_packed_units": info["cbox_packed_units"]},
             "nodes_per_s": value * Np, "setup_s": t_setup, "build_pgf_s": t_pgf,
             "bytes_per_eval_algorithmic": alg_total,
             "eval_GBps_algorithmic": alg_total / (tot_ms / a.steps * 1e-3) / 1e9,

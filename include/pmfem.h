@@ -94,6 +94,10 @@ typedef struct {
   int32_t k2_tile[3];                             /* K2 anterpolation grid tile (points per axis) */
   int32_t slab_world;                             /* > 1: slab-decomposed FFT over this many ranks
                                                      (SURVEY 8(e)); 1: FFT on the full grid      */
+  int32_t cbox_format;                            /* packed C_box streamed by K4: 0 = C4x chunks
+                                                     (4 entries + 64-bit column header), 1 = B4
+                                                     (aligned 4-column blocks + 32-bit block id)  */
+  int64_t cbox_packed_units;                      /* C4x chunks or B4 blocks                     */
 } pmfem_info;
 
 /* Build a context: validate, orient, detect T-PBC pairs and fold them to LCAs,

@@ -187,6 +187,41 @@ __global__ void k_c4x_fill(long long Np, const long long* __restrict__ rowptr, c
   if (ch >= cptr[n]) { for (; pos < 4; ++pos) cval[4 * ch + pos] = 0.f; hdr[ch] = h; }
 }
 
+// ---- B4: aligned blocks of 4 consecutive columns [4b, 4b+4) of a (column-sorted) row, per
+// block a float4 of values (0 for columns outside the near set) and the int32 block index b.
+// K4 then gathers q for a whole block with one aligned 16-byte load.  Chosen over C4x when
+// the rows' near columns fill their blocks densely (long runs of consecutive columns).
+__global__ void k_b4_count(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                           long long* __restrict__ nb) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long blocks = 0;
+  int prev = -1;
+  for (long long e = rowptr[n]; e < rowptr[n + 1]; ++e) {
+    const int b = col[e] >> 2;
+    if (b != prev) { ++blocks; prev = b; }
+  }
+  nb[n] = blocks;
+}
+
+__global__ void k_b4_fill(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                          const float* __restrict__ val, const long long* __restrict__ bptr,
+                          int* __restrict__ bidx, float* __restrict__ bval) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long o = bptr[n] - 1;
+  int prev = -1;
+  for (long long e = rowptr[n]; e < rowptr[n + 1]; ++e) {
+    const int b = col[e] >> 2;
+    if (b != prev) {
+      ++o; prev = b;
+      bidx[o] = b;
+      for (int j = 0; j < 4; ++j) bval[4 * o + j] = 0.f;
+    }
+    bval[4 * o + (col[e] & 3)] = val[e];
+  }
+}
+
 template <class T>
 T* dalloc_c(size_t n) {
   T* p = nullptr;
@@ -249,26 +284,50 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   float* d_val = dalloc_c<float>(nnz);
   k_cbox_fill<<<blocks, 128>>>(c, Np, d_xw, D.box_ptr, d_su, d_tl, d_ptr, d_col, d_val);
   CKC(cudaGetLastError());
-  // encode C4x
+  // sizes of both packed formats: C4x chunks (24 B) and B4 blocks (20 B)
   long long* d_nch = dalloc_c<long long>(Np);
   k_c4x_count<<<blocks, 128>>>(Np, d_ptr, d_col, d_nch);
   CKC(cudaGetLastError());
-  std::vector<long long> nch(Np), cptr(Np + 1, 0);
+  std::vector<long long> nch(Np), cptr(Np + 1, 0), nbk(Np), bptr(Np + 1, 0);
   CKC(cudaMemcpy(nch.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
-  for (int64_t i = 0; i < Np; ++i) cptr[i + 1] = cptr[i] + nch[i];
-  long long* d_cptr = dup_c(cptr);
-  unsigned long long* d_hdr = dalloc_c<unsigned long long>(cptr[Np]);
-  float* d_cval = dalloc_c<float>(4 * cptr[Np]);
-  k_c4x_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_cptr, d_hdr, d_cval);
+  k_b4_count<<<blocks, 128>>>(Np, d_ptr, d_col, d_nch);
   CKC(cudaGetLastError());
+  CKC(cudaMemcpy(nbk.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < Np; ++i) { cptr[i + 1] = cptr[i] + nch[i]; bptr[i + 1] = bptr[i] + nbk[i]; }
+  // B4 unless it streams > 10 % more bytes than C4x (its gathers are 4x fewer instructions);
+  // PMFEM_CBOX_FORMAT=c4x|b4 forces one (tests)
+  bool use_b4 = 20.0 * bptr[Np] <= 1.10 * 24.0 * cptr[Np];
+  if (const char* e = std::getenv("PMFEM_CBOX_FORMAT")) {
+    if (std::string(e) == "c4x") use_b4 = false;
+    else if (std::string(e) == "b4") use_b4 = true;
+  }
+  if (use_b4) {
+    long long* d_bptr = dup_c(bptr);
+    int* d_bidx = dalloc_c<int>(bptr[Np]);
+    float* d_bval = dalloc_c<float>(4 * bptr[Np]);
+    k_b4_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_bptr, d_bidx, d_bval);
+    CKC(cudaGetLastError());
+    D.c_ptr = reinterpret_cast<int64_t*>(d_bptr);
+    D.c_bidx = d_bidx;
+    D.c_val = d_bval;
+    D.cbox_chunks = bptr[Np];
+    D.cbox_format = 1;
+  } else {
+    long long* d_cptr = dup_c(cptr);
+    unsigned long long* d_hdr = dalloc_c<unsigned long long>(cptr[Np]);
+    float* d_cval = dalloc_c<float>(4 * cptr[Np]);
+    k_c4x_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_cptr, d_hdr, d_cval);
+    CKC(cudaGetLastError());
+    D.c_ptr = reinterpret_cast<int64_t*>(d_cptr);
+    D.c_hdr = d_hdr;
+    D.c_val = d_cval;
+    D.cbox_chunks = cptr[Np];
+    D.cbox_format = 0;
+  }
   CKC(cudaDeviceSynchronize());
   cudaFree(d_xw); cudaFree(d_tl); cudaFree(d_su); cudaFree(d_cnt); cudaFree(d_nch);
   cudaFree(d_ptr); cudaFree(d_col); cudaFree(d_val);
-  D.c_ptr = reinterpret_cast<int64_t*>(d_cptr);
-  D.c_hdr = d_hdr;
-  D.c_val = d_cval;
   D.cbox_nnz = nnz;
-  D.cbox_chunks = cptr[Np];
   return nnz;
 }
 

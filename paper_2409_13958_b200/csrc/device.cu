@@ -87,21 +87,37 @@ __global__ void k_to_m4(RowRange rr, const float* __restrict__ m, float4* __rest
   m4[n] = make_float4(m[3 * h], m[3 * h + 1], m[3 * h + 2], 0.f);
 }
 
+// SPLIT = 2 (small meshes, < ~1M rows): two threads per row, lanes 0-15 of a warp take the
+// even SELL columns of 16 rows and lanes 16-31 the odd ones (each half still reads 256
+// contiguous bytes per column), partial sums combined with one shuffle -- twice the loads in
+// flight when the row count alone cannot fill the GPU.
+template <int SPLIT>
 __global__ void __launch_bounds__(256) k1_local_in(
     RowRange rr, const float4* __restrict__ m4, const int64_t* __restrict__ sl_off, const int64_t* __restrict__ sl1_off,
     const float4* __restrict__ s_zc, const float4* __restrict__ s_LD, const float4* __restrict__ rowsum,
     float* __restrict__ q, float* __restrict__ uloc, float* __restrict__ H, int write_hex) {
-  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= rr.row1) return;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t n;
+  int part;
+  if (SPLIT == 1) { n = rr.row0 + gid; part = 0; }
+  else { n = rr.row0 + (gid >> 6) * 32 + ((gid >> 5) & 1) * 16 + (threadIdx.x & 15); part = (threadIdx.x >> 4) & 1; }
+  const bool valid = n < rr.row1;
+  if (SPLIT == 1 && !valid) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
-  const int64_t o = sl_off[s], o1 = sl1_off[s];
-  const int w = (int)((sl_off[s + 1] - o) >> 5), w1 = (int)((sl1_off[s + 1] - o1) >> 5);
-  const float4 mn = m4[n];
+  int64_t o = 0, o1 = 0;
+  int w = 0, w1 = 0;
+  float4 mn = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (valid) {
+    o = sl_off[s]; o1 = sl1_off[s];
+    w = (int)((sl_off[s + 1] - o) >> 5); w1 = (int)((sl1_off[s + 1] - o1) >> 5);
+    mn = m4[n];
+  }
   float hx = 0.f, hy = 0.f, hz = 0.f, qq = 0.f, ul = 0.f;
-  int64_t e = o + l, e1 = o1 + l;
+  int64_t e = o + l + 32 * part, e1 = o1 + l + 32 * part;
+  int j = part;
 #pragma unroll 4
-  for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
+  for (; j < w1; j += SPLIT, e += 32 * SPLIT, e1 += 32 * SPLIT) {
     const float4 zc = __ldg(s_zc + e);
     const float4 LD = __ldg(s_LD + e1);
     const float4 mc = m4[colof(zc)];
@@ -111,11 +127,18 @@ __global__ void __launch_bounds__(256) k1_local_in(
     ul = fmaf(zc.x, dx, fmaf(zc.y, dy, fmaf(zc.z, dz, ul)));
   }
 #pragma unroll 4
-  for (int j = w1; j < w; ++j, e += 32) {
+  for (; j < w; j += SPLIT, e += 32 * SPLIT) {
     const float4 zc = __ldg(s_zc + e);
     const float4 mc = m4[colof(zc)];
     ul = fmaf(zc.x, mc.x - mn.x, fmaf(zc.y, mc.y - mn.y, fmaf(zc.z, mc.z - mn.z, ul)));
   }
+  if (SPLIT == 2) {
+    hx += __shfl_xor_sync(0xffffffffu, hx, 16); hy += __shfl_xor_sync(0xffffffffu, hy, 16);
+    hz += __shfl_xor_sync(0xffffffffu, hz, 16); qq += __shfl_xor_sync(0xffffffffu, qq, 16);
+    ul += __shfl_xor_sync(0xffffffffu, ul, 16);
+    if (part) return;
+  }
+  if (!valid) return;
   const float4 rd = rowsum[2 * n], rz = rowsum[2 * n + 1];
   q[n] = qq + rd.x * mn.x + rd.y * mn.y + rd.z * mn.z;
   uloc[n] = ul + rz.x * mn.x + rz.y * mn.y + rz.z * mn.z;
@@ -321,10 +344,13 @@ __global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const in
 // is streamed in the C4x format (cbox_gpu.cu): per chunk one 16-byte value load and one
 // 8-byte header (base column + three 12-bit deltas) -- consecutive lanes take consecutive
 // chunks, so the q gathers of a lane group mostly hit the same few lines.
-template <int P, int G>
+// F = 1: B4 blocks instead -- one 4-byte block index, one 16-byte value load and ONE aligned
+// 16-byte q gather per block of 4 consecutive columns.
+template <int P, int G, int F>
 __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
                                                       const float4* __restrict__ st_t, GridDims g,
                                                       const int64_t* __restrict__ c_ptr, const unsigned long long* __restrict__ c_hdr,
+                                                      const int* __restrict__ c_bidx,
                                                       const float4* __restrict__ c_val4, const float* __restrict__ q,
                                                       const float* __restrict__ uloc, float* __restrict__ u) {
   const int lane = threadIdx.x & (G - 1);
@@ -332,6 +358,16 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
   const int64_t b = valid ? c_ptr[n] : 0, e_end = valid ? c_ptr[n + 1] : 0;
+  if (F == 1) {
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+#pragma unroll 4
+    for (int64_t e = b + lane; e < e_end; e += G) {
+      const int bi = __ldg(c_bidx + e);
+      const float4 vv = __ldg(c_val4 + e);
+      const float4 qq = __ldg(q4 + bi);
+      acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
+    }
+  } else
 #pragma unroll 2
   for (int64_t e = b + lane; e < e_end; e += G) {
     const unsigned long long h = __ldg(c_hdr + e);
@@ -377,23 +413,36 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
+template <int SPLIT>
 __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __restrict__ u, const int64_t* __restrict__ sl1_off,
                                                    const float4* __restrict__ s_Gc, float* __restrict__ H, int accumulate) {
-  const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= rr.row1) return;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t n;
+  int part;
+  if (SPLIT == 1) { n = rr.row0 + gid; part = 0; }
+  else { n = rr.row0 + (gid >> 6) * 32 + ((gid >> 5) & 1) * 16 + (threadIdx.x & 15); part = (threadIdx.x >> 4) & 1; }
+  const bool valid = n < rr.row1;
+  if (SPLIT == 1 && !valid) return;
   const int64_t s = n >> 5;
   const int l = (int)(n & 31);
-  const int64_t o1 = sl1_off[s];
-  const int w1 = (int)((sl1_off[s + 1] - o1) >> 5);
-  const float un = u[n];
+  int64_t o1 = 0;
+  int w1 = 0;
+  float un = 0.f;
+  if (valid) { o1 = sl1_off[s]; w1 = (int)((sl1_off[s + 1] - o1) >> 5); un = u[n]; }
   float gx = 0.f, gy = 0.f, gz = 0.f;
-  int64_t e1 = o1 + l;
+  int64_t e1 = o1 + l + 32 * part;
 #pragma unroll 4
-  for (int j = 0; j < w1; ++j, e1 += 32) {
+  for (int j = part; j < w1; j += SPLIT, e1 += 32 * SPLIT) {
     const float4 gc = __ldg(s_Gc + e1);
     const float du = u[colof(gc)] - un;
     gx = fmaf(gc.x, du, gx); gy = fmaf(gc.y, du, gy); gz = fmaf(gc.z, du, gz);
   }
+  if (SPLIT == 2) {
+    gx += __shfl_xor_sync(0xffffffffu, gx, 16); gy += __shfl_xor_sync(0xffffffffu, gy, 16);
+    gz += __shfl_xor_sync(0xffffffffu, gz, 16);
+    if (part) return;
+  }
+  if (!valid) return;
   if (accumulate) { H[3 * (n - rr.hoff)] -= gx; H[3 * (n - rr.hoff) + 1] -= gy; H[3 * (n - rr.hoff) + 2] -= gz; }
   else { H[3 * (n - rr.hoff)] = -gx; H[3 * (n - rr.hoff) + 1] = -gy; H[3 * (n - rr.hoff) + 2] = -gz; }
 }
@@ -468,35 +517,19 @@ void twiddles(int P, std::vector<typename Cx<T>::t>& tw) {
   }
 }
 
-template <class T, int TL>
-void launch_strided_t(typename Cx<T>::t* data, int P, long long es, int ncol, int nplanes, long long plane_stride,
-                      int nin, int nout, int mode, const T* spec, long long spec_es, long long spec_ps,
-                      const typename Cx<T>::t* tw, cudaStream_t st) {
-  using C = typename Cx<T>::t;
-  size_t smem = (size_t)P * (TL + 1) * sizeof(C);                   // lines + twiddle table
-  auto kern = fft_strided<T, TL>;
-  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  dim3 grid((ncol + TL - 1) / TL, nplanes);
-  // a thread holds FftBudget<C>::V values per Stockham pass: TL * P <= V * threads
-  // (~16 values per thread, at most 256 threads: ~100-130 registers each)
-  const int threads = std::max(128, std::min(256, (TL * P / 16 + 31) / 32 * 32));
-  kern<<<grid, threads, smem, st>>>(data, P, ilog2(P), es, ncol, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw);
-  CK(cudaGetLastError());
-}
+constexpr int TILE = 16;
 
-// column tile: 16 columns while the CTA stays at <= 256 threads (~100-130 registers each),
-// fewer columns for long lines
 template <class T>
 void launch_strided(typename Cx<T>::t* data, int P, long long es, int ncol, int nplanes, long long plane_stride,
                     int nin, int nout, int mode, const T* spec, long long spec_es, long long spec_ps,
                     const typename Cx<T>::t* tw, cudaStream_t st) {
   using C = typename Cx<T>::t;
-  const int cap = 256 * FftBudget<C>::V;               // TL * P <= cap
-  if (16 * P <= cap) launch_strided_t<T, 16>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
-  else if (8 * P <= cap) launch_strided_t<T, 8>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
-  else if (4 * P <= cap) launch_strided_t<T, 4>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
-  else if (2 * P <= cap) launch_strided_t<T, 2>(data, P, es, ncol, nplanes, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw, st);
-  else throw Error(PMFEM_E_INVALID_ARG, "FFT length too large for one CTA");
+  size_t smem = (size_t)P * TILE * sizeof(C);
+  auto kern = fft_strided<T, TILE>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((ncol + TILE - 1) / TILE, nplanes);
+  kern<<<grid, 256, smem, st>>>(data, P, ilog2(P), es, ncol, plane_stride, nin, nout, mode, spec, spec_es, spec_ps, tw);
+  CK(cudaGetLastError());
 }
 
 template <class T>
@@ -506,16 +539,11 @@ void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows
   const int M = P0 / 2;
   // lines per CTA: enough CTAs to cover 2 waves of 148 SMs, at most 4096 complex per CTA
   int nl = std::max(1, std::min(4096 / std::max(M, 1), nrows / 296));
-  while (nl & (nl - 1)) nl &= nl - 1;                                // power of two (line-fast shifts)
-  size_t smem = ((size_t)nl * (M + 1) + M) * sizeof(C);              // padded lines + twiddle table
+  size_t smem = (size_t)nl * M * sizeof(C);
   RowMap rm{n1, P1};
   int blocks = (nrows + nl - 1) / nl;
-  // a thread holds FftBudget<C>::V values per Stockham pass: nl * M <= V * threads
-  // (and ~8 values per thread for latency hiding, at most 512 threads)
-  int threads = std::max(64, std::min(512, nl * M / 8));
-  threads = std::max(threads, (nl * M + FftBudget<C>::V - 1) / FftBudget<C>::V);
+  int threads = std::min(256, std::max(64, nl * M / 2));
   threads = (threads + 31) / 32 * 32;
-  if (threads > 1024) throw Error(PMFEM_E_INVALID_ARG, "FFT length too large for one CTA");
   if (fwd) {
     auto kern = fft_x_forward<T>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -563,13 +591,10 @@ __global__ void k_spec_slice(const float* __restrict__ spec, float* __restrict__
 
 void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
   const int tile = D.fused_tile, P1 = D.P[1], P2 = D.P[2];
-  size_t smem = ((size_t)P2 * (P1 * tile + 1) + std::max(P1, P2)) * sizeof(float2);   // padded planes + twiddles
+  size_t smem = (size_t)P2 * (P1 * tile + (tile == 1 ? 1 : 0)) * sizeof(float2);   // padded planes
   auto kern = fft_yz_fused<float>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  // a thread holds 32 values per Stockham pass: P1 * P2 * tile <= 32 * threads
-  // (~8 values per thread for latency hiding, at most 512 threads at ~96 registers)
-  int threads = std::max(128, std::min(512, P1 * P2 * tile / 8));
-  threads = std::max(threads, P1 * P2 * tile / 32);
+  int threads = std::min(512, std::max(128, P1 * P2 * tile / 4));
   threads = (threads + 31) / 32 * 32;
   kern<<<(D.H0 + tile - 1) / tile, threads, smem, st>>>(D.C, D.n[1], P1, ilog2(P1), D.n[2], P2, ilog2(P2), D.H0,
                                                          tile, D.spec, D.tw32[1], D.tw32[2]);
@@ -727,8 +752,9 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     twiddles<float>(D.P[a], t32); twiddles<double>(D.P[a], t64);
     D.tw32[a] = dupload(t32); D.tw64[a] = dupload(t64);
   }
-  D.q = dalloc<float>(Np); D.uloc = dalloc<float>(Np); D.u = dalloc<float>(Np);
-  CK(cudaMemset(D.q, 0, sizeof(float) * (size_t)Np));
+  // q: + 4 zero floats so B4's aligned 4-column gathers stay in bounds
+  D.q = dalloc<float>(Np + 4); D.uloc = dalloc<float>(Np); D.u = dalloc<float>(Np);
+  CK(cudaMemset(D.q, 0, sizeof(float) * (size_t)(Np + 4)));
   D.Q = dalloc<float>((size_t)D.n[0] * D.n[1] * D.n[2]);
   D.C = dalloc<float2>((size_t)D.H0 * D.P[1] * D.P[2]);
   D.spec = dalloc<float>((size_t)D.H0 * D.P[1] * D.P[2]);
@@ -738,17 +764,18 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     const size_t plane_bytes = (size_t)(D.P[1] + 1) * D.P[2] * sizeof(float2);
     D.fused_tile = 0;
     // PMFEM_FFT_SPLIT=1 forces the split plan (tests exercise it on small grids)
-    // (<= 16384 complex per CTA: 512 threads x 32 values per Stockham pass, ~96 registers each)
-    const int64_t plane = (int64_t)D.P[1] * D.P[2];
-    if (plane_bytes <= 200 * 1024 && plane <= 16384 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {
+    if (plane_bytes <= 200 * 1024 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {
       int tile = 1;
-      while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && plane * tile * 2 <= 16384 &&
-             (D.H0 + 2 * tile - 1) / (2 * tile) >= 148)
-        tile *= 2;
+      while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && (D.H0 + 2 * tile - 1) / (2 * tile) >= 148) tile *= 2;
       D.fused_tile = tile;
     }
   }
   D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5
+  D.row_split = (D.hi - D.lo) < 1000000 ? 2 : 1;
+  if (const char* e = std::getenv("PMFEM_ROW_SPLIT")) {
+    const int v = std::atoi(e);
+    if (v == 1 || v == 2) D.row_split = v;
+  }
   // slab-decomposed convolution: NCCL ranks, or simulated ranks on one device (tests)
   {
     int W = 1;
@@ -801,9 +828,9 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       if (gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
     }
   }
-  // C_box in C4x: 4-byte value + 2 bytes of chunk header per near pair (chunk padding, ~3-10 %,
-  // is format overhead, not algorithmic traffic)
-  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * 6 + G * 4.0;
+  // C_box per near pair: C4x 4-byte value + 2 bytes of chunk header, B4 4-byte value + 1 byte
+  // of block index (chunk padding / empty block slots are format overhead, not counted)
+  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + G * 4.0;
   D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
 
@@ -851,7 +878,7 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
 void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
-  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_val,
+  void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_bidx, D.c_val,
                   D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
                   D.send_buf, D.recv_buf, D.slab_cx, D.slab_buf, D.slab_spec, D.send_idx[0], D.send_idx[1], D.send_idx[2],
@@ -1038,8 +1065,15 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   }
   if (!D.pgf_ready) throw Error(PMFEM_E_STATE, "pmfem_build_pgf has not been called");
   GridDims g{D.n[0], D.n[1], D.n[2], D.periodic[0], D.periodic[1], D.periodic[2]};
-  k1_local_in<<<thr_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.rowsum, D.q, D.uloc, H,
-                                          mode == EVAL_HEFF ? 1 : 0);
+  // two threads per row when the rows alone cannot fill the GPU (PMFEM_ROW_SPLIT=1|2 overrides)
+  const bool split = D.row_split == 2;
+  const unsigned split_blocks = (unsigned)((2 * ((nrows + 31) / 32 * 32) + 255) / 256);
+  if (split)
+    k1_local_in<2><<<split_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.rowsum, D.q, D.uloc, H,
+                                                 mode == EVAL_HEFF ? 1 : 0);
+  else
+    k1_local_in<1><<<thr_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.rowsum, D.q, D.uloc, H,
+                                               mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(1);
   const size_t G = (size_t)D.n[0] * D.n[1] * D.n[2];
@@ -1083,8 +1117,11 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
-  k4_interp_corr<PP, GG><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, \
-                                                                             D.c_hdr, v4, D.q, D.uloc, D.u)
+  (D.cbox_format == 1                                                                                   \
+       ? k4_interp_corr<PP, GG, 1><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
+       : k4_interp_corr<PP, GG, 0><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u))
 #define K4_BY_G(PP)                                                                                     \
   (D.k4_group == 8 ? K4_LAUNCH(PP, 8) : D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
     case 1: K4_BY_G(1); break;
@@ -1096,7 +1133,8 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   CK(cudaGetLastError());
   halo(D, 2, D.u, 1, st);
   mark(4);
-  k5_grad_sum<<<thr_blocks, 256, 0, st>>>(rr, D.u, D.sl1_off, D.s_Gc, H, mode == EVAL_HEFF ? 1 : 0);
+  if (split) k5_grad_sum<2><<<split_blocks, 256, 0, st>>>(rr, D.u, D.sl1_off, D.s_Gc, H, mode == EVAL_HEFF ? 1 : 0);
+  else k5_grad_sum<1><<<thr_blocks, 256, 0, st>>>(rr, D.u, D.sl1_off, D.s_Gc, H, mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
   mark(5);
 }

@@ -31,13 +31,16 @@ struct DeviceState {
   unsigned long long* c_hdr = nullptr;
   float* c_val = nullptr;             // [chunks][4]
   int64_t cbox_nnz = 0;               // near pairs (entries without chunk padding)
-  int64_t cbox_chunks = 0;
+  int64_t cbox_chunks = 0;             // C4x chunks or B4 blocks
+  int cbox_format = 0;                // 0: C4x, 1: B4 (aligned 4-column blocks, c_bidx + c_val)
+  int* c_bidx = nullptr;              // B4 block index (column >> 2) per block
   int k4_group = 32;          // lanes per row in K4 (8/16/32 from the mean padded row length)
   // stencils
   int4* st_s = nullptr;       // wrapped (periodic) / clamped anchors
   int32_t* box_ptr = nullptr; // [G+1] first internal row of each anchor box (rows are box-sorted)
   int k2_tile[3] = {8, 8, 8}; // K2 grid tile per axis (divides n)
   int box_max = 1;            // largest anchor-box population (K2 fixed-point bound)
+  int row_split = 1;          // K1/K5 threads per row (2 for small meshes)
 
   float4* st_t = nullptr;     // local coordinates t - s
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32

@@ -302,6 +302,8 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
   out->fft_fused = ctx->D.fused_tile > 0;
   for (int a = 0; a < 3; ++a) out->k2_tile[a] = ctx->D.k2_tile[a];
   out->slab_world = ctx->D.slab_world;
+  out->cbox_format = ctx->D.cbox_format;
+  out->cbox_packed_units = ctx->D.cbox_chunks;
   out->comm_bytes_per_eval = ctx->D.comm_bytes_per_eval;
   out->setup_seconds = S.setup_seconds;
   out->pgf_seconds = S.pgf_seconds;
@@ -347,8 +349,9 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     else if (n == "perm") put(S.perm.data(), S.Np, 8);
     else if (n == "dist_bounds") put(S.dist.bounds.data(), (int64_t)S.dist.bounds.size(), 8);
     else if (n.rfind("cbox_device_", 0) == 0) {
-      // the device-built C_box (internal order), decoded from its C4x chunks for tests: every
-      // chunk slot is returned (padding slots repeat the previous column with value 0)
+      // the device-built C_box (internal order), decoded from its C4x chunks / B4 blocks for
+      // tests: every slot is returned (C4x padding repeats the previous column with value 0; B4
+      // empty slots are the block's other columns with value 0)
       pmfem::require(!ctx->host_only && S.cbox_device, PMFEM_E_STATE, "C_box was not built on the device");
       const pmfem::DeviceState& D = ctx->D;
       std::vector<int64_t> ptr(S.Np + 1);
@@ -361,6 +364,15 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
       } else if (tail == "val") {
         *count = 4 * nch;
         if (dst && nch) cudaMemcpy(dst, D.c_val, sizeof(float) * 4 * (size_t)nch, cudaMemcpyDeviceToHost);
+      } else if (tail == "col" && D.cbox_format == 1) {
+        *count = 4 * nch;
+        if (dst && nch) {
+          std::vector<int32_t> b(nch);
+          cudaMemcpy(b.data(), D.c_bidx, sizeof(int32_t) * (size_t)nch, cudaMemcpyDeviceToHost);
+          int32_t* c = static_cast<int32_t*>(dst);
+          for (int64_t i = 0; i < nch; ++i)
+            for (int j = 0; j < 4; ++j) c[4 * i + j] = 4 * b[i] + j;
+        }
       } else if (tail == "col") {
         *count = 4 * nch;
         if (dst && nch) {
@@ -375,6 +387,9 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
         }
       } else if (tail == "chunks") {
         put(&D.cbox_chunks, 1, 8);
+      } else if (tail == "format") {
+        const int64_t f = D.cbox_format;
+        put(&f, 1, 8);
       } else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
     }
     else if (n.rfind("send_", 0) == 0 || n.rfind("recv_", 0) == 0) {

@@ -59,7 +59,8 @@ class _Info(ctypes.Structure):
                 ("pgf_seconds", ctypes.c_double), ("kernel_bytes", ctypes.c_double * 8),
                 ("launches_per_eval", ctypes.c_int32), ("fft_fused", ctypes.c_int32),
                 ("comm_bytes_per_eval", ctypes.c_double), ("k2_tile", ctypes.c_int32 * 3),
-                ("slab_world", ctypes.c_int32)]
+                ("slab_world", ctypes.c_int32), ("cbox_format", ctypes.c_int32),
+                ("cbox_packed_units", ctypes.c_int64)]
 
 
 _vp = ctypes.c_void_p
@@ -89,7 +90,8 @@ _EXPORT_DTYPES = {"parent": np.int64, "lca": np.int64, "shift": np.int32, "ring1
                   "ring1_col": np.int32, "z0_rowptr": np.int64, "z0_col": np.int32, "cbox_rowptr": np.int64,
                   "cbox_col": np.int32, "stencil_s": np.int32, "perm": np.int64, "dist_bounds": np.int64}
 _EXPORT_DTYPES.update({"cbox_device_rowptr": np.int64, "cbox_device_col": np.int32,
-                       "cbox_device_val": np.float32})
+                       "cbox_device_val": np.float32, "cbox_device_chunks": np.int64,
+                       "cbox_device_format": np.int64})
 for _k in "mqu":
     _EXPORT_DTYPES["send_%s_ptr" % _k] = np.int64
     _EXPORT_DTYPES["recv_%s_ptr" % _k] = np.int64

@@ -53,9 +53,9 @@ def test_heff_random(pair):
 def test_heff_smooth(pair):
     key, om, ctx = pair
     rank = ctx.internal_to_parent_rank()
-    L = max(om.lattice)
-    k = 2 * np.pi / L
     x = om.xw
+    L = max(om.lattice) if max(om.lattice) > 0 else float(np.ptp(x[:, 0]))   # non-periodic: extent
+    k = 2 * np.pi / L
     m = np.stack([np.cos(k * x[:, 0]) * 0.6, np.sin(k * x[:, 0]) * 0.6, np.full(len(x), 0.8)], 1)
     H = _run(ctx, "heff", m, rank)
     assert rel_l2(H, om.heff(m, "aim")) <= TOL
@@ -191,3 +191,30 @@ def test_slab_fft_simulated_ranks(key, world, monkeypatch):
     rank = ctx.internal_to_parent_rank()
     m = m_random(om.n_parents, seed=61)
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+
+
+@pytest.mark.parametrize("fmt", ["c4x", "b4"])
+@pytest.mark.parametrize("key", ["C2p2", "C3p1", "N1p2"])
+def test_cbox_formats(key, fmt, monkeypatch):
+    """K4 streaming either packed C_box format gives the oracle's field."""
+    monkeypatch.setenv("PMFEM_CBOX_FORMAT", fmt)
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=71)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+
+
+@pytest.mark.parametrize("split", ["1", "2"])
+@pytest.mark.parametrize("key", ["C2p2", "C4p3"])
+def test_row_split(key, split, monkeypatch):
+    """K1/K5 with one or two threads per row (two for meshes under ~1M rows) agree with the oracle."""
+    monkeypatch.setenv("PMFEM_ROW_SPLIT", split)
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=81)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+    assert rel_l2(_run(ctx, "exchange", m, rank), om.exchange(m)) <= TOL

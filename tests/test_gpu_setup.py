@@ -9,9 +9,13 @@ from helpers import SMALL, lib_context
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("fmt", ["c4x", "b4"])
 @pytest.mark.parametrize("key", sorted(SMALL))
-def test_device_cbox_matches_host(key):
+def test_device_cbox_matches_host(key, fmt, monkeypatch):
+    """Both packed C_box formats (C4x chunks, B4 aligned blocks) decode to the host matrix."""
+    monkeypatch.setenv("PMFEM_CBOX_FORMAT", fmt)
     dev = lib_context(key, device=0)
+    assert dev.export("cbox_device_format")[0] == (1 if fmt == "b4" else 0)
     host = lib_context(key, device=-1)
     n = host.n_parents
     perm = dev.export("perm")                     # internal -> user parent id
@@ -21,7 +25,7 @@ def test_device_cbox_matches_host(key):
     D = np.zeros((n, n))
     for i in range(n):
         for e in range(rp[i], rp[i + 1]):
-            if val[e] != 0.0 or col[e] != i:            # skip the padding (col = row, val = 0)
+            if val[e] != 0.0:                           # skip padding / empty block slots
                 D[perm[i], perm[col[e]]] += val[e]
     hrp = host.export("cbox_rowptr")
     hcol = host.export("cbox_col")
