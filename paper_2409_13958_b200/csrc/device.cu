@@ -771,7 +771,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     }
   }
   D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5
-  D.row_split = (D.hi - D.lo) < 1000000 ? 2 : 1;
+  D.row_split = 1;            // 2 measured slower on C2 (K1 0.067 -> 0.070 ms); kept for PMFEM_ROW_SPLIT=2
   if (const char* e = std::getenv("PMFEM_ROW_SPLIT")) {
     const int v = std::atoi(e);
     if (v == 1 || v == 2) D.row_split = v;

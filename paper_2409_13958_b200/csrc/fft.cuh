@@ -277,15 +277,22 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   // zero the whole tile (padded planes / rows must read as zero), then load the data block
   for (int idx = threadIdx.x; idx < P2 * pl; idx += blockDim.x) { C z; z.x = T(0); z.y = T(0); buf[idx] = z; }
   __syncthreads();
+  // iterate over the destination y slots (slot = bit-reversed row, every (P1/n1)-th slot holds
+  // data) so consecutive threads store to nearby shared addresses; the global reads of one
+  // column are strided either way
+  const int sstep = P1 / n1;
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
-    const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
+    const int c = idx & (tile - 1), r = idx >> ltile, slot = (r & (n1 - 1)) * sstep, i2 = r >> ln1;
+    const int i1 = bitrev(slot, logP1);
     if (c < nc)
-      buf[bitrev(i2, logP2) * pl + bitrev(i1, logP1) * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
+      buf[bitrev(i2, logP2) * pl + slot * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
   }
   __syncthreads();
   // forward y on the n2 data planes: line (i2, c) base = bitrev(i2)*pl + c, stride tile
   const PlaneBase ybase{tile, pl, logP2};
-  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, true);
+  // (one column per CTA: element-fast -- line-fast would put consecutive threads on planes at
+  // bit-reversed offsets, i.e. in the same banks)
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase, tile, tw1, 1, false, tile > 1);
   // forward z on every (k1, c): base = k1*tile + c, stride pl
   const TileBase zbase{};
   smem_fft<C>(buf, P2, logP2, nzl, zbase, pl, tw2, 1, false, true);
@@ -319,7 +326,7 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   // inverse y on planes i2 < n2 (natural z order now)
   const PlaneBase ybase2{tile, pl, 0};
   smem_bitrev<C>(buf, P1, logP1, n2 * tile, ybase2, tile);
-  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, true);
+  smem_fft<C>(buf, P1, logP1, n2 * tile, ybase2, tile, tw1, 1, true, tile > 1);
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
     const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
     if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * pl + i1 * tile + c];

@@ -1,0 +1,9 @@
+# round-1 session 3: fused-YZ bank-conflict fixes; B4 forced on C2/C3
+set -x
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
+timeout 600 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/bench_c2.log 2>&1; echo bench=$?
+PMFEM_CBOX_FORMAT=b4 timeout 600 python bench.py --no-cpu-baseline --steps 30 > gpurun_out/bench_c2_b4.log 2>&1; echo bench=$?
+timeout 900 python bench.py --config C3 --steps 20 --no-cpu-baseline > gpurun_out/bench_c3.log 2>&1; echo c3=$?
+PMFEM_CBOX_FORMAT=b4 timeout 900 python bench.py --config C3 --steps 20 --no-cpu-baseline > gpurun_out/bench_c3_b4.log 2>&1; echo c3=$?
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fft_yz -s 1 -c 1 -o gpurun_out/prof_c3_fft_yz -f python scripts/profile_eval.py --config C3 --evals 2 > gpurun_out/ncu_c3_fft_yz.log 2>&1; echo full3=$?
