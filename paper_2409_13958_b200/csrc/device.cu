@@ -213,7 +213,8 @@ __device__ __forceinline__ int anchor_ranges(int a0, int T, int n, int per, int 
 }
 
 // dynamic shared memory of k2_tile: the int tile, then per candidate segment (anchor line x
-// x range) its first row and the exclusive prefix of the segment sizes
+// x range) its first row and the exclusive prefix of the segment sizes, then the row map
+// (2 x tile volume entries)
 __host__ __device__ __forceinline__ int k2_nseg(int t1, int t2, int P) { return 2 * (t1 + P) * (t2 + P); }
 
 template <int P>
@@ -282,8 +283,19 @@ __global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const in
   }
   if (threadIdx.x == 0) seg_cum[nseg] = total;
   __syncthreads();
-  // flattened node f -> (segment, row): binary search in seg_cum
-  auto row_of = [&](int f) {
+  // flattened node f -> row: a shared row map when it fits (2 x tile volume entries), filled
+  // by a warp per segment; otherwise a binary search in seg_cum
+  int* rows = seg_cum + nseg + 1;
+  const bool mapped = total <= 2 * vol;
+  if (mapped) {
+    for (int sg = warp; sg < nseg; sg += (int)(blockDim.x >> 5)) {
+      const int c0 = seg_cum[sg], cn = seg_cum[sg + 1] - c0, b0 = seg_beg[sg];
+      for (int k = lane; k < cn; k += 32) rows[c0 + k] = b0 + k;
+    }
+    __syncthreads();
+  }
+  auto row_of = [&](int f) -> int64_t {
+    if (mapped) return rows[f];
     int a = 0, b = nseg;                                   // seg_cum[a] <= f < seg_cum[b]
     while (b - a > 1) { const int m = (a + b) >> 1; if (seg_cum[m] <= f) a = m; else b = m; }
     return (int64_t)seg_beg[a] + (f - seg_cum[a]);
@@ -723,10 +735,10 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     D.box_max = 1;
     for (int64_t b = 0; b < Gb; ++b) { D.box_max = std::max(D.box_max, bp[b + 1]); bp[b + 1] += bp[b]; }
     D.box_ptr = dupload(bp);
-    // K2 tile: ~G/600 points (>= 4 CTAs per SM), 512..8192 points, grown by doubling the
+    // K2 tile: ~G/600 points (>= 4 CTAs per SM), 256..4096 points, grown by doubling the
     // shortest axis (x first on ties) so the tile stays compact; PMFEM_K2_TILE=t0,t1,t2 overrides
-    int64_t target = 512;
-    while (target < 8192 && target * 2 * 600 <= Gb) target *= 2;
+    int64_t target = 256;
+    while (target < 4096 && target * 2 * 600 <= Gb) target *= 2;
     int t[3] = {1, 1, 1};
     while ((int64_t)t[0] * t[1] * t[2] < target) {
       int best = -1;
@@ -1080,7 +1092,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   {
     const TileDims td{D.k2_tile[0], D.k2_tile[1], D.k2_tile[2]};
     const unsigned nt = (unsigned)(G / ((size_t)td.t0 * td.t1 * td.t2));
-    const size_t smem = sizeof(int) * ((size_t)td.t0 * td.t1 * td.t2 + 2 * k2_nseg(td.t1, td.t2, D.order) + 1);
+    const size_t smem = sizeof(int) * ((size_t)3 * td.t0 * td.t1 * td.t2 + 2 * k2_nseg(td.t1, td.t2, D.order) + 1);
 #define K2_LAUNCH(PP)                                                                                 \
   do {                                                                                                \
     CK(cudaFuncSetAttribute(k2_tile<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
