@@ -575,8 +575,7 @@ void launch_x(bool fwd, const T* rin, typename Cx<T>::t* cio, T* rout, int nrows
 //   z-slab layout Cz [nzl][P1][H0]   x-slab layout Cx [P2][P1][H_r]
 // Block (r -> p) = Cz_r[:, :, h_p : h_p + H_p] packed as [nzl][P1][H_p]; it lands in Cx_p at
 // plane offset r nzl (contiguous), so only the sender packs and only the return path unpacks.
-__host__ __device__ __forceinline__ int slab_h0(int p, int H0, int W) { return p * (H0 / W) + min(p, H0 % W); }
-__host__ __device__ __forceinline__ int slab_hn(int p, int H0, int W) { return H0 / W + (p < H0 % W ? 1 : 0); }
+// slab_h0 / slab_hn: device.cuh
 
 // pack (dir 0): Cz[rows][H0] cols [h_p, h_p+H_p) -> buf + p*rows*(h_p) ... contiguous [rows][H_p] blocks
 // unpack (dir 1): the reverse.  blockIdx.y = peer p.

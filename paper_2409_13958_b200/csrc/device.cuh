@@ -8,6 +8,11 @@
 
 namespace pmfem {
 
+// slab-decomposed FFT: rank p owns the k0 columns [slab_h0, slab_h0 + slab_hn) of
+// the H0-column half spectrum (uneven splits: the first H0 % W ranks get one more column)
+__host__ __device__ __forceinline__ int slab_h0(int p, int H0, int W) { return p * (H0 / W) + (p < H0 % W ? p : H0 % W); }
+__host__ __device__ __forceinline__ int slab_hn(int p, int H0, int W) { return H0 / W + (p < H0 % W ? 1 : 0); }
+
 struct DeviceState {
   int device = -1;
   int64_t Np = 0;

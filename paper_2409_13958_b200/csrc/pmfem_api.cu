@@ -348,6 +348,14 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     else if (n == "grid_origin") put(S.origin, 3, 8);
     else if (n == "perm") put(S.perm.data(), S.Np, 8);
     else if (n == "dist_bounds") put(S.dist.bounds.data(), (int64_t)S.dist.bounds.size(), 8);
+    else if (n == "slab_kranges") {
+      // per rank (first k0 column, count) of the slab-decomposed FFT's x slabs, world = this
+      // context's world (the z slabs are n2 / world planes each)
+      const int W = S.dist.world, H0 = S.fft_n[0] / 2 + 1;
+      std::vector<int64_t> r(2 * W);
+      for (int p = 0; p < W; ++p) { r[2 * p] = pmfem::slab_h0(p, H0, W); r[2 * p + 1] = pmfem::slab_hn(p, H0, W); }
+      put(r.data(), 2 * W, 8);
+    }
     else if (n.rfind("cbox_device_", 0) == 0) {
       // the device-built C_box (internal order), decoded from its C4x chunks / B4 blocks for
       // tests: every slot is returned (C4x padding repeats the previous column with value 0; B4
