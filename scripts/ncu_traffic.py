@@ -38,7 +38,7 @@ def main():
         rd = float(r[h.index("dram__bytes_read.sum")]) * scale[units[h.index("dram__bytes_read.sum")]]
         wr = float(r[h.index("dram__bytes_write.sum")]) * scale[units[h.index("dram__bytes_write.sum")]]
         tu = units[h.index("gpu__time_duration.sum")]
-        us = float(r[h.index("gpu__time_duration.sum")]) * {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(tu, 1.0)
+        us = float(r[h.index("gpu__time_duration.sum")]) * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(tu, 1.0)
         ent[key] = {"dram_bytes": rd + wr, "dram_read": rd, "dram_write": wr, "ncu_us": us,
                     "report": os.path.basename(a.rep), "note": a.note}
         print(a.config, key, "%.1f MB" % ((rd + wr) / 1e6), "%.1f us" % us)
