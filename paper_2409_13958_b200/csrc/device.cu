@@ -379,6 +379,33 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
       const float4 qq = __ldg(q4 + bi);
       acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
     }
+  } else if (F == 2) {
+    // C4x with vector gathers for run chunks (deltas 1,1,1): the 4 consecutive q values come
+    // from one or two aligned 16-byte loads instead of four scalar ones
+    const float4* q4 = reinterpret_cast<const float4*>(q);
+#pragma unroll 2
+    for (int64_t e = b + lane; e < e_end; e += G) {
+      const unsigned long long h = __ldg(c_hdr + e);
+      const float4 vv = __ldg(c_val4 + e);
+      const int k0 = (int)(h & 0xFFFFFFFull);
+      float a0, a1, a2, a3;
+      if ((h >> 28) == 0x001001001ull) {
+        const int o = k0 & 3;
+        const float4 lo = __ldg(q4 + (k0 >> 2));
+        float4 hi = lo;
+        if (o) hi = __ldg(q4 + (k0 >> 2) + 1);
+        a0 = o == 0 ? lo.x : o == 1 ? lo.y : o == 2 ? lo.z : lo.w;
+        a1 = o == 0 ? lo.y : o == 1 ? lo.z : o == 2 ? lo.w : hi.x;
+        a2 = o == 0 ? lo.z : o == 1 ? lo.w : o == 2 ? hi.x : hi.y;
+        a3 = o == 0 ? lo.w : o == 1 ? hi.x : o == 2 ? hi.y : hi.z;
+      } else {
+        const int k1 = k0 + (int)((h >> 28) & 0xFFF);
+        const int k2 = k1 + (int)((h >> 40) & 0xFFF);
+        const int k3 = k2 + (int)(h >> 52);
+        a0 = __ldg(q + k0); a1 = __ldg(q + k1); a2 = __ldg(q + k2); a3 = __ldg(q + k3);
+      }
+      acc = fmaf(vv.x, a0, fmaf(vv.y, a1, fmaf(vv.z, a2, fmaf(vv.w, a3, acc))));
+    }
   } else
 #pragma unroll 2
   for (int64_t e = b + lane; e < e_end; e += G) {
@@ -782,6 +809,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     }
   }
   D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5
+  D.k4_vec = std::getenv("PMFEM_K4_VEC") != nullptr && std::atoi(std::getenv("PMFEM_K4_VEC")) == 1;
   D.row_split = 1;            // 2 measured slower on C2 (K1 0.067 -> 0.070 ms); kept for PMFEM_ROW_SPLIT=2
   if (const char* e = std::getenv("PMFEM_ROW_SPLIT")) {
     const int v = std::atoi(e);
@@ -1130,6 +1158,9 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
 #define K4_LAUNCH(PP, GG)                                                                               \
   (D.cbox_format == 1                                                                                   \
        ? k4_interp_corr<PP, GG, 1><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
+   : D.k4_vec                                                                                           \
+       ? k4_interp_corr<PP, GG, 2><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
        : k4_interp_corr<PP, GG, 0><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u))

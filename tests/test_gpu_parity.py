@@ -193,11 +193,13 @@ def test_slab_fft_simulated_ranks(key, world, monkeypatch):
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
 
 
-@pytest.mark.parametrize("fmt", ["c4x", "b4"])
+@pytest.mark.parametrize("fmt", ["c4x", "c4x-vec", "b4"])
 @pytest.mark.parametrize("key", ["C2p2", "C3p1", "N1p2"])
 def test_cbox_formats(key, fmt, monkeypatch):
-    """K4 streaming either packed C_box format gives the oracle's field."""
-    monkeypatch.setenv("PMFEM_CBOX_FORMAT", fmt)
+    """K4 streaming either packed C_box format (C4x also with vector gathers of run chunks)
+    gives the oracle's field."""
+    monkeypatch.setenv("PMFEM_CBOX_FORMAT", fmt.split("-")[0])
+    monkeypatch.setenv("PMFEM_K4_VEC", "1" if fmt.endswith("vec") else "0")
     om = oracle_model(key)
     ctx = lib_context(key, device=0)
     ctx.build_pgf()
