@@ -114,8 +114,12 @@ pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_per
  * contiguous, cost-balanced slab ranges and builds halo lists for m (K1 columns), q (C_box
  * columns) and u (ring-1 columns).  m and H passed to the field calls then cover this rank's
  * rows only ([n_parents_local][3], order from pmfem_get_order).  Per evaluation: grouped
- * ncclSend/ncclRecv halo exchanges with every peer that shares a boundary, one ncclAllReduce
- * of the anterpolated grid Q, and a replicated FFT convolution.  nccl_unique_id: 128 bytes
+ * ncclSend/ncclRecv halo exchanges with every peer that shares a boundary, and the
+ * slab-decomposed FFT convolution: ncclReduceScatter of the anterpolated grid Q into z slabs
+ * (n2/world planes), X/Y passes, grouped send/recv all-to-all into k0 slabs (columns
+ * [h_r, h_r + H_r), export "slab_kranges"), Z pass x G_hat, all-to-all back, Y'/X' passes,
+ * ncclAllGather of U.  When n2 % world != 0 or H0 < world (or PMFEM_NO_SLAB is set): one
+ * ncclAllReduce of Q and a replicated FFT instead.  nccl_unique_id: 128 bytes
  * from pmfem_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
  * cuda_device = -1 builds the host-only plan (exportable: dist_bounds, send_/recv_{m,q,u}_{ptr,idx}).
  * world = 1 is identical to pmfem_setup. */

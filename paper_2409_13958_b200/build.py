@@ -50,7 +50,7 @@ def build(force=False, verbose=False):
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc(), "-c", os.path.join(CSRC, src), "-o", obj, "-O3", "-std=c++17", "-lineinfo",
                "-Xcompiler", "-fPIC,-fopenmp,-O3", "-I", os.path.join(HERE, "..", "include"), "-I", nccl_dirs()[0],
-               "--expt-relaxed-constexpr"] + ARCH
+               "--expt-relaxed-constexpr"] + ARCH + os.environ.get("PMFEM_EXTRA_NVCC", "").split()
         if src.endswith(".cpp"):
             cmd += ["-x", "cu"] if False else []
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

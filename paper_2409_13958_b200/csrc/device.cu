@@ -80,6 +80,17 @@ __global__ void k_unpack(const float* __restrict__ buf, const int32_t* __restric
 // 16-byte gather of m (float4 copy); on the ring-1 prefix one more 16-byte load (L, Dx, Dy, Dz).
 __device__ __forceinline__ int colof(float4 v) { return __float_as_int(v.w); }
 
+// operator streams are read once per evaluation; PMFEM_STREAM_CS builds them with the
+// evict-first (cache-streaming) hint so L1/L2 keep the gathered vectors
+template <class T>
+__device__ __forceinline__ T ld_stream(const T* p) {
+#ifdef PMFEM_STREAM_CS
+  return __ldcs(p);
+#else
+  return __ldg(p);
+#endif
+}
+
 __global__ void k_to_m4(RowRange rr, const float* __restrict__ m, float4* __restrict__ m4) {
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= rr.row1) return;
@@ -118,8 +129,8 @@ __global__ void __launch_bounds__(256) k1_local_in(
   int j = part;
 #pragma unroll 4
   for (; j < w1; j += SPLIT, e += 32 * SPLIT, e1 += 32 * SPLIT) {
-    const float4 zc = __ldg(s_zc + e);
-    const float4 LD = __ldg(s_LD + e1);
+    const float4 zc = ld_stream(s_zc + e);
+    const float4 LD = ld_stream(s_LD + e1);
     const float4 mc = m4[colof(zc)];
     const float dx = mc.x - mn.x, dy = mc.y - mn.y, dz = mc.z - mn.z;
     hx = fmaf(LD.x, dx, hx); hy = fmaf(LD.x, dy, hy); hz = fmaf(LD.x, dz, hz);
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(256) k1_local_in(
   }
 #pragma unroll 4
   for (; j < w; j += SPLIT, e += 32 * SPLIT) {
-    const float4 zc = __ldg(s_zc + e);
+    const float4 zc = ld_stream(s_zc + e);
     const float4 mc = m4[colof(zc)];
     ul = fmaf(zc.x, mc.x - mn.x, fmaf(zc.y, mc.y - mn.y, fmaf(zc.z, mc.z - mn.z, ul)));
   }
@@ -161,7 +172,7 @@ __global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float4* __r
   int64_t e = o + l, e1 = o1 + l;
 #pragma unroll 4
   for (int j = 0; j < w1; ++j, e += 32, e1 += 32) {
-    const float4 mc = m4[colof(__ldg(s_zc + e))];
+    const float4 mc = m4[colof(ld_stream(s_zc + e))];
     const float L = __ldg(&s_LD[e1].x);
     hx = fmaf(L, mc.x - mn.x, hx); hy = fmaf(L, mc.y - mn.y, hy); hz = fmaf(L, mc.z - mn.z, hz);
   }
@@ -374,8 +385,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     const float4* q4 = reinterpret_cast<const float4*>(q);
 #pragma unroll 4
     for (int64_t e = b + lane; e < e_end; e += G) {
-      const int bi = __ldg(c_bidx + e);
-      const float4 vv = __ldg(c_val4 + e);
+      const int bi = ld_stream(c_bidx + e);
+      const float4 vv = ld_stream(c_val4 + e);
       const float4 qq = __ldg(q4 + bi);
       acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
     }
@@ -385,8 +396,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     const float4* q4 = reinterpret_cast<const float4*>(q);
 #pragma unroll 2
     for (int64_t e = b + lane; e < e_end; e += G) {
-      const unsigned long long h = __ldg(c_hdr + e);
-      const float4 vv = __ldg(c_val4 + e);
+      const unsigned long long h = ld_stream(c_hdr + e);
+      const float4 vv = ld_stream(c_val4 + e);
       const int k0 = (int)(h & 0xFFFFFFFull);
       float a0, a1, a2, a3;
       if ((h >> 28) == 0x001001001ull) {
@@ -409,8 +420,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   } else
 #pragma unroll 2
   for (int64_t e = b + lane; e < e_end; e += G) {
-    const unsigned long long h = __ldg(c_hdr + e);
-    const float4 vv = __ldg(c_val4 + e);
+    const unsigned long long h = ld_stream(c_hdr + e);
+    const float4 vv = ld_stream(c_val4 + e);
     const int k0 = (int)(h & 0xFFFFFFFull);
     const int k1 = k0 + (int)((h >> 28) & 0xFFF);
     const int k2 = k1 + (int)((h >> 40) & 0xFFF);
@@ -472,7 +483,7 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
   int64_t e1 = o1 + l + 32 * part;
 #pragma unroll 4
   for (int j = part; j < w1; j += SPLIT, e1 += 32 * SPLIT) {
-    const float4 gc = __ldg(s_Gc + e1);
+    const float4 gc = ld_stream(s_Gc + e1);
     const float du = u[colof(gc)] - un;
     gx = fmaf(gc.x, du, gx); gy = fmaf(gc.y, du, gy); gz = fmaf(gc.z, du, gz);
   }
