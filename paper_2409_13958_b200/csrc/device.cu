@@ -80,11 +80,13 @@ __global__ void k_unpack(const float* __restrict__ buf, const int32_t* __restric
 // 16-byte gather of m (float4 copy); on the ring-1 prefix one more 16-byte load (L, Dx, Dy, Dz).
 __device__ __forceinline__ int colof(float4 v) { return __float_as_int(v.w); }
 
-// operator streams are read once per evaluation; PMFEM_STREAM_CS builds them with the
-// evict-first (cache-streaming) hint so L1/L2 keep the gathered vectors
+// operator streams of K1/K5 are read once per evaluation: loaded with the evict-first
+// (cache-streaming) hint so L1/L2 keep the gathered m / u vectors (measured: K1 at C2 0.067 ->
+// 0.059 ms, C5 -5 %; K4's C_box stream measured neutral-to-worse with it (C3 +3 %) and keeps
+// __ldg).  PMFEM_NO_STREAM_CS builds the plain __ldg variant for A/B.
 template <class T>
 __device__ __forceinline__ T ld_stream(const T* p) {
-#ifdef PMFEM_STREAM_CS
+#ifndef PMFEM_NO_STREAM_CS
   return __ldcs(p);
 #else
   return __ldg(p);
@@ -385,8 +387,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     const float4* q4 = reinterpret_cast<const float4*>(q);
 #pragma unroll 4
     for (int64_t e = b + lane; e < e_end; e += G) {
-      const int bi = ld_stream(c_bidx + e);
-      const float4 vv = ld_stream(c_val4 + e);
+      const int bi = __ldg(c_bidx + e);
+      const float4 vv = __ldg(c_val4 + e);
       const float4 qq = __ldg(q4 + bi);
       acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
     }
@@ -396,8 +398,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     const float4* q4 = reinterpret_cast<const float4*>(q);
 #pragma unroll 2
     for (int64_t e = b + lane; e < e_end; e += G) {
-      const unsigned long long h = ld_stream(c_hdr + e);
-      const float4 vv = ld_stream(c_val4 + e);
+      const unsigned long long h = __ldg(c_hdr + e);
+      const float4 vv = __ldg(c_val4 + e);
       const int k0 = (int)(h & 0xFFFFFFFull);
       float a0, a1, a2, a3;
       if ((h >> 28) == 0x001001001ull) {
@@ -420,8 +422,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   } else
 #pragma unroll 2
   for (int64_t e = b + lane; e < e_end; e += G) {
-    const unsigned long long h = ld_stream(c_hdr + e);
-    const float4 vv = ld_stream(c_val4 + e);
+    const unsigned long long h = __ldg(c_hdr + e);
+    const float4 vv = __ldg(c_val4 + e);
     const int k0 = (int)(h & 0xFFFFFFFull);
     const int k1 = k0 + (int)((h >> 28) & 0xFFF);
     const int k2 = k1 + (int)((h >> 40) & 0xFFF);
@@ -640,10 +642,22 @@ __global__ void k_spec_slice(const float* __restrict__ spec, float* __restrict__
 
 void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
   const int tile = D.fused_tile, P1 = D.P[1], P2 = D.P[2];
+  if (D.yz_half) {   // tile 1, zero-padded z: half the shared memory (fft_yz_fused_zhalf)
+    const int n2 = D.n[2], chunk = std::min(32, P1);
+    const size_t smem = ((size_t)n2 * (P1 + 1) + (size_t)2 * chunk * (n2 + 1)) * sizeof(float2);
+    auto kh = fft_yz_fused_zhalf<float>;
+    CK(cudaFuncSetAttribute(kh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kh<<<D.H0, 512, smem, st>>>(D.C, D.n[1], P1, ilog2(P1), n2, ilog2(n2), D.H0, chunk, D.spec, D.tw32[1], D.tw32[2]);
+    CK(cudaGetLastError());
+    return;
+  }
   size_t smem = (size_t)P2 * (P1 * tile + (tile == 1 ? 1 : 0)) * sizeof(float2);   // padded planes
   auto kern = fft_yz_fused<float>;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int threads = std::min(512, std::max(128, P1 * P2 * tile / 4));
+  // up to 1024 threads: at the C3 plane size (129 KB) one CTA fills an SM, and its passes are
+  // latency-bound (measured C3 FFT 0.156 -> 0.151 ms vs 512); PMFEM_YZ_THREADS overrides
+  static const int cap = std::getenv("PMFEM_YZ_THREADS") ? std::atoi(std::getenv("PMFEM_YZ_THREADS")) : 1024;
+  int threads = std::min(cap, std::max(128, P1 * P2 * tile / 4));
   threads = (threads + 31) / 32 * 32;
   kern<<<(D.H0 + tile - 1) / tile, threads, smem, st>>>(D.C, D.n[1], P1, ilog2(P1), D.n[2], P2, ilog2(P2), D.H0,
                                                          tile, D.spec, D.tw32[1], D.tw32[2]);
@@ -817,6 +831,10 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       int tile = 1;
       while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && (D.H0 + 2 * tile - 1) / (2 * tile) >= 148) tile *= 2;
       D.fused_tile = tile;
+      // PMFEM_YZ_HALF=1: the split-z fused kernel for tile-1 columns with a zero-padded z axis
+      // (opt-in: measured slower, C3 FFT 0.156 -> 0.182 ms -- more barriers per column)
+      const char* yh = std::getenv("PMFEM_YZ_HALF");
+      D.yz_half = tile == 1 && D.P[2] == 2 * D.n[2] && D.n[2] >= 2 && yh != nullptr && std::atoi(yh) == 1;
     }
   }
   D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5

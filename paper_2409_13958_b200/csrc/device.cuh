@@ -46,6 +46,7 @@ struct DeviceState {
   int k2_tile[3] = {8, 8, 8}; // K2 grid tile per axis (divides n)
   int box_max = 1;            // largest anchor-box population (K2 fixed-point bound)
   int row_split = 1;          // K1/K5 threads per row (2 for small meshes)
+  bool yz_half = false;       // fused YZ FFT with the z axis split into even/odd halves (PMFEM_YZ_HALF=1)
   bool k4_vec = false;        // C4x: vector q gathers for run chunks (PMFEM_K4_VEC=1)
 
   float4* st_t = nullptr;     // local coordinates t - s

@@ -133,13 +133,25 @@ __global__ void fft_x_forward(const T* __restrict__ in, typename Cx<T>::t* __res
   const int M = P0 >> 1, H0 = M + 1;
   const int r0 = blockIdx.x * nl;
   const int nlines = min(nl, nrows - r0);
-  for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    const int l = idx >> logM, j = idx & (M - 1);
-    const T* row = in + (long long)(r0 + l) * n0;
-    C z;
-    z.x = (2 * j < n0) ? row[2 * j] : T(0);
-    z.y = (2 * j + 1 < n0) ? row[2 * j + 1] : T(0);
-    buf[l * M + bitrev(j, logM)] = z;
+  // global loads issued LB at a time per thread (latency: one pass streams the whole grid)
+  constexpr int LB = 8;
+  for (int i0 = threadIdx.x; i0 < nlines * M; i0 += LB * blockDim.x) {
+    C z[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, l = idx >> logM, j = idx & (M - 1);
+      z[b].x = T(0); z[b].y = T(0);
+      if (idx < nlines * M) {
+        const T* row = in + (long long)(r0 + l) * n0;
+        if (2 * j < n0) z[b].x = row[2 * j];
+        if (2 * j + 1 < n0) z[b].y = row[2 * j + 1];
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, l = idx >> logM, j = idx & (M - 1);
+      if (idx < nlines * M) buf[l * M + bitrev(j, logM)] = z[b];
+    }
   }
   __syncthreads();
   smem_fft<C>(buf, M, logM, nlines, RowBase{M}, 1, tw, 2, false, false);
@@ -170,16 +182,29 @@ __global__ void fft_x_inverse(const typename Cx<T>::t* __restrict__ in, T* __res
   const int r0 = blockIdx.x * nl;
   const int nlines = min(nl, nrows - r0);
   // Z_k = (X_k + conj X_{M-k}) + i W^{-k} (X_k - conj X_{M-k}),  k < M
-  for (int idx = threadIdx.x; idx < nlines * M; idx += blockDim.x) {
-    const int l = idx >> logM, k = idx & (M - 1);
-    const C* row = in + rm.crow(r0 + l) * H0;
-    C xk = row[k];
-    C xm = cconj(row[M - k]);
+  constexpr int LB = 4;
+  for (int i0 = threadIdx.x; i0 < nlines * M; i0 += LB * blockDim.x) {
+    C xa[LB], xb[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, l = idx >> logM, k = idx & (M - 1);
+      if (idx < nlines * M) {
+        const C* row = in + rm.crow(r0 + l) * H0;
+        xa[b] = row[k]; xb[b] = row[M - k];
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+    const int idx = i0 + b * blockDim.x, l = idx >> logM, k = idx & (M - 1);
+    if (idx >= nlines * M) break;
+    C xk = xa[b];
+    C xm = cconj(xb[b]);
     C E; E.x = xk.x + xm.x; E.y = xk.y + xm.y;
     C D; D.x = xk.x - xm.x; D.y = xk.y - xm.y;
     C O = cmul(cconj(tw[k]), D);
     C Z; Z.x = E.x - O.y; Z.y = E.y + O.x;     // E + i O
     buf[l * M + bitrev(k, logM)] = Z;
+    }
   }
   __syncthreads();
   smem_fft<C>(buf, M, logM, nlines, RowBase{M}, 1, tw, 2, true, false);
@@ -210,11 +235,20 @@ __global__ void fft_strided(typename Cx<T>::t* __restrict__ data, int P, int log
   const int c0 = blockIdx.x * TILE;
   const int nc = min(TILE, ncol - c0);
   C* base = data + (long long)blockIdx.y * plane_stride + c0;
-  for (int idx = threadIdx.x; idx < P * TILE; idx += blockDim.x) {
-    const int e = idx / TILE, c = idx - e * TILE;
-    C v; v.x = T(0); v.y = T(0);
-    if (e < nin && c < nc) v = base[e * es + c];
-    buf[bitrev(e, logP) * TILE + c] = v;
+  constexpr int LB = 8;
+  for (int i0 = threadIdx.x; i0 < P * TILE; i0 += LB * blockDim.x) {
+    C v[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, e = idx / TILE, c = idx - e * TILE;
+      v[b].x = T(0); v[b].y = T(0);
+      if (idx < P * TILE && e < nin && c < nc) v[b] = base[e * es + c];
+    }
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, e = idx / TILE, c = idx - e * TILE;
+      if (idx < P * TILE) buf[bitrev(e, logP) * TILE + c] = v[b];
+    }
   }
   __syncthreads();
   smem_fft<C>(buf, P, logP, TILE, TileBase{}, TILE, tw, 1, mode == 1, true);
@@ -261,7 +295,7 @@ struct PlaneBase {   // line l = (plane index l / tile, column l % tile); logP2 
 // smem [P2][P1][tile] (tile columns contiguous).  Planes are stored at bit-reversed z
 // positions so the y transforms of the n2 data planes leave the z lines in DIT input order.
 template <class T>
-__global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P1, int logP1, int n2, int P2,
+__global__ void __launch_bounds__(1024) fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P1, int logP1, int n2, int P2,
                              int logP2, int H0, int tile, const T* __restrict__ spec,
                              const typename Cx<T>::t* __restrict__ tw1, const typename Cx<T>::t* __restrict__ tw2) {
   using C = typename Cx<T>::t;
@@ -281,11 +315,21 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   // data) so consecutive threads store to nearby shared addresses; the global reads of one
   // column are strided either way
   const int sstep = P1 / n1;
-  for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
-    const int c = idx & (tile - 1), r = idx >> ltile, slot = (r & (n1 - 1)) * sstep, i2 = r >> ln1;
-    const int i1 = bitrev(slot, logP1);
-    if (c < nc)
-      buf[bitrev(i2, logP2) * pl + slot * tile + c] = data[((long long)i2 * P1 + i1) * H0 + c0 + c];
+  constexpr int LB = 8;
+  for (int i0 = threadIdx.x; i0 < n2 * n1 * tile; i0 += LB * blockDim.x) {
+    C v[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x;
+      const int c = idx & (tile - 1), r = idx >> ltile, slot = (r & (n1 - 1)) * sstep, i2 = r >> ln1;
+      if (idx < n2 * n1 * tile && c < nc) v[b] = data[((long long)i2 * P1 + bitrev(slot, logP1)) * H0 + c0 + c];
+    }
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x;
+      const int c = idx & (tile - 1), r = idx >> ltile, slot = (r & (n1 - 1)) * sstep, i2 = r >> ln1;
+      if (idx < n2 * n1 * tile && c < nc) buf[bitrev(i2, logP2) * pl + slot * tile + c] = v[b];
+    }
   }
   __syncthreads();
   // forward y on the n2 data planes: line (i2, c) base = bitrev(i2)*pl + c, stride tile
@@ -330,6 +374,101 @@ __global__ void fft_yz_fused(typename Cx<T>::t* __restrict__ data, int n1, int P
   for (int idx = threadIdx.x; idx < n2 * n1 * tile; idx += blockDim.x) {
     const int c = idx & (tile - 1), r = idx >> ltile, i1 = r & (n1 - 1), i2 = r >> ln1;
     if (c < nc) data[((long long)i2 * P1 + i1) * H0 + c0 + c] = buf[i2 * pl + i1 * tile + c];
+  }
+}
+
+// ---------------------------------------------------------------- fused YZ, zero-padded z
+// One column per CTA (tile 1) when z is zero-padded (P2 = 2 n2).  The length-P2 z transform of
+// a line with n2 data values splits into two length-n2 transforms (w = exp(-2 pi i / P2)):
+//   X[2k] = DFT_n2(x)[k],   X[2k+1] = DFT_n2(x_j w^j)[k],
+// and the n2 kept outputs of the (unnormalised) inverse are
+//   y_j = IDFT_n2(Y_even)_j + w^-j IDFT_n2(Y_odd)_j,
+// so shared memory holds only the n2 data planes [n2][P1 + 1] plus scratch for `chunk` z lines
+// (even and odd halves, line stride n2 + 1): about half the footprint of fft_yz_fused, i.e. two
+// CTAs per SM at P1 = P2 = 128 (C3) instead of one.
+template <class T>
+__global__ void __launch_bounds__(512, 2) fft_yz_fused_zhalf(typename Cx<T>::t* __restrict__ data, int n1, int P1,
+                                                             int logP1, int n2, int logn2, int H0, int chunk,
+                                                             const T* __restrict__ spec,
+                                                             const typename Cx<T>::t* __restrict__ tw1,
+                                                             const typename Cx<T>::t* __restrict__ tw2) {
+  using C = typename Cx<T>::t;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* buf = reinterpret_cast<C*>(smem_raw);
+  const int pl = P1 + 1, ls = n2 + 1;
+  C* scr = buf + n2 * pl;
+  const int c0 = blockIdx.x;
+  const int ln1 = __ffs(n1) - 1, lch = __ffs(chunk) - 1;
+  for (int idx = threadIdx.x; idx < n2 * pl; idx += blockDim.x) { C z; z.x = T(0); z.y = T(0); buf[idx] = z; }
+  __syncthreads();
+  // data rows i1 < n1 go to their bit-reversed y slots (every (P1/n1)-th slot)
+  const int sstep = P1 / n1;
+  constexpr int LB = 8;
+  for (int i0 = threadIdx.x; i0 < n2 * n1; i0 += LB * blockDim.x) {
+    C v[LB];
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, slot = (idx & (n1 - 1)) * sstep, i2 = idx >> ln1;
+      if (idx < n2 * n1) v[b] = data[((long long)i2 * P1 + bitrev(slot, logP1)) * H0 + c0];
+    }
+#pragma unroll
+    for (int b = 0; b < LB; ++b) {
+      const int idx = i0 + b * blockDim.x, slot = (idx & (n1 - 1)) * sstep, i2 = idx >> ln1;
+      if (idx < n2 * n1) buf[i2 * pl + slot] = v[b];
+    }
+  }
+  __syncthreads();
+  const PlaneBase yb{1, pl, 0};
+  smem_fft<C>(buf, P1, logP1, n2, yb, 1, tw1, 1, false, false);
+  const RowBase zb{ls};
+  for (int k1a = 0; k1a < P1; k1a += chunk) {
+    // z lines k1a .. k1a+chunk: even half x_j, odd half x_j w^j, both bit-reversed (DIT input)
+    for (int idx = threadIdx.x; idx < chunk * n2; idx += blockDim.x) {
+      const int l = idx & (chunk - 1), j = idx >> lch, r = bitrev(j, logn2);
+      const C x = buf[j * pl + k1a + l];
+      scr[l * ls + r] = x;
+      scr[(chunk + l) * ls + r] = cmul(x, tw2[j]);
+    }
+    __syncthreads();
+    smem_fft<C>(scr, n2, logn2, 2 * chunk, zb, 1, tw2, 2, false, false);
+    // x G_hat[k2][k1]: k2 = 2k (even half), 2k + 1 (odd half); loads batched for latency
+    constexpr int SB = 8;
+    const int tot = 2 * chunk * n2;
+    for (int base = threadIdx.x; base < tot; base += SB * blockDim.x) {
+      T gv[SB];
+#pragma unroll
+      for (int b = 0; b < SB; ++b) {
+        const int idx = base + b * blockDim.x;
+        const int k = idx & (n2 - 1), l = idx >> logn2, half = l >= chunk ? 1 : 0, k1 = k1a + l - half * chunk;
+        gv[b] = idx < tot ? __ldg(spec + ((long long)(2 * k + half) * P1 + k1) * H0 + c0) : T(0);
+      }
+#pragma unroll
+      for (int b = 0; b < SB; ++b) {
+        const int idx = base + b * blockDim.x;
+        if (idx < tot) {
+          C* pv = scr + (idx >> logn2) * ls + (idx & (n2 - 1));
+          C v = *pv;
+          v.x *= gv[b]; v.y *= gv[b];
+          *pv = v;
+        }
+      }
+    }
+    __syncthreads();
+    smem_bitrev<C>(scr, n2, logn2, 2 * chunk, zb, 1);
+    smem_fft<C>(scr, n2, logn2, 2 * chunk, zb, 1, tw2, 2, true, false);
+    for (int idx = threadIdx.x; idx < chunk * n2; idx += blockDim.x) {
+      const int l = idx & (chunk - 1), j = idx >> lch;
+      const C e = scr[l * ls + j], o = cmul(cconj(tw2[j]), scr[(chunk + l) * ls + j]);
+      C y; y.x = e.x + o.x; y.y = e.y + o.y;
+      buf[j * pl + k1a + l] = y;
+    }
+    __syncthreads();
+  }
+  smem_bitrev<C>(buf, P1, logP1, n2, yb, 1);
+  smem_fft<C>(buf, P1, logP1, n2, yb, 1, tw1, 1, true, false);
+  for (int idx = threadIdx.x; idx < n2 * n1; idx += blockDim.x) {
+    const int i1 = idx & (n1 - 1), i2 = idx >> ln1;
+    data[((long long)i2 * P1 + i1) * H0 + c0] = buf[i2 * pl + i1];
   }
 }
 

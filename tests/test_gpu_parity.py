@@ -130,6 +130,20 @@ def test_split_fft_plan(key, monkeypatch):
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
 
 
+@pytest.mark.parametrize("key", ["C2p2", "C3p1", "C5p2", "N1p2"])
+def test_yz_half_fft(key, monkeypatch):
+    """The fused YZ pass with the zero-padded z axis split into even/odd half-length transforms
+    (fft_yz_fused_zhalf, PMFEM_YZ_HALF=1; tile-1 columns with P2 = 2 n2) gives the oracle's field."""
+    monkeypatch.setenv("PMFEM_YZ_HALF", "1")
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    assert ctx.query()["fft_fused"] == 1
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=37)
+    assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
+
+
 def test_kernel_timing_in_graph(pair):
     """Per-kernel timing events inside the captured graph are readable and leave no error."""
     import torch
