@@ -79,7 +79,7 @@ def main():
         for n, t in L:
             agg.setdefault(n, []).append(t)
         def is_eval(k):   # per-evaluation kernels (setup kernels and torch's own are excluded)
-            return not k.startswith(("void at::", "at::", "k_z0", "k_cbox", "k_pgf", "k_spec")) \
+            return not k.startswith(("void at::", "at::", "k_z0", "k_cbox", "k_c4x", "k_b4", "k_pgf", "k_spec")) \
                 and "<double" not in k
         tot = sum(sum(v) for k, v in agg.items() if is_eval(k))
         print("## Launch list (ncu gpu__time_duration.sum, cold-cache, serialised)\n")
