@@ -23,7 +23,9 @@ class OracleModel:
         self.Aex_tet = np.full(T, float(Aex)) if np.isscalar(Aex) else np.asarray(Aex, float)
         self.ops = fem.assemble(self.pm, self.Ms_tet, self.Aex_tet)
         self.rows = rows
-        self.z0 = oz0.assemble_z0(self.pm, self.ops, self.Ms_tet, z0_ring, nquad, rows)
+        # rows = [] defers Z0 to the caller (sampled full-size checks pick their rows later)
+        self.z0 = oz0.assemble_z0(self.pm, self.ops, self.Ms_tet, z0_ring, nquad, rows) \
+            if rows is None or len(rows) else None
         self.xw = self.pm.wrapped_parent_xyz()
         self.periodic = self.pm.periodic
         self.lattice = tuple(float(lattice[a]) if periodic[a] else 0.0 for a in range(3))
@@ -67,9 +69,15 @@ class OracleModel:
         return u
 
     def potential_bf(self, m, chunk=256):
-        """O12: u_n = sum_{k != n} G_p(r_n - r_k) q_k + G_p^reg(0) q_n + (Z0 m)_n."""
+        """O12: u_n = sum_{k != n} G_p(r_n - r_k) q_k + G_p^reg(0) q_n + (Z0 m)_n.
+        Periodic kernels use the C pair sums of oracle/bf.c (pinned to oracle.pgf to 1e-13 in
+        tests/test_oracle_bf.py); free space the NumPy sum."""
         q = self.charges(m)
-        u = pgf_potential(self.xw, self.xw, q, self.spec, chunk)
+        if self.spec.dim > 0:
+            from . import bf
+            u = bf.potential(self.xw, self.xw, q, self.spec)
+        else:
+            u = pgf_potential(self.xw, self.xw, q, self.spec, chunk)
         u += pgf_self(self.spec) * q
         return u + self.u_loc(m)
 
