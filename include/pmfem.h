@@ -35,15 +35,21 @@ typedef struct pmfem_ctx_s* pmfem_ctx;   /* opaque; owns every host and device b
 
 typedef enum {
   PMFEM_OK = 0,
-  PMFEM_E_INVALID_ARG = 1,      /* NULL pointer, bad size, non-positive period, grid not a power of two,
-                                   stencil order not in 1..3, N_i < 2(p+1)                         */
+  PMFEM_E_INVALID_ARG = 1,      /* NULL pointer, bad size, non-positive period, non-diagonal lattice
+                                   vectors, grid not a power of two, stencil order not in 1..3,
+                                   N_i < 2(p+1)                                                    */
   PMFEM_E_MESH = 2,             /* tet index out of range, degenerate tet (|V| < 1e-12 mean |V|),
                                    zero lumped volume                                              */
   PMFEM_E_PBC_AMBIGUOUS = 3,    /* two nodes within match_tol of one periodic image        */
   PMFEM_E_PBC_INCONSISTENT = 4, /* an LCA component whose members are not period translates*/
-  PMFEM_E_OUTSIDE_GRID = 5,     /* reserved (the grid is built to cover the mesh)                  */
+  PMFEM_E_OUTSIDE_GRID = 5,     /* a node's stencil anchor falls outside [0, N_i - 1 - p] on a
+                                   non-periodic axis (fp64 rounding of the grid built from the node
+                                   extent); the grid is built to cover the mesh, so this
+                                   signals corrupted coordinates (NaN / Inf)                        */
   PMFEM_E_RER_TOO_LARGE = 6,    /* r_ER >= L/2 or r_ER/Delta + p + 1 >= N/2 on a periodic axis     */
-  PMFEM_E_PGF_NOT_CONVERGED = 7,/* reserved                                                          */
+  PMFEM_E_PGF_NOT_CONVERGED = 7,/* pmfem_build_pgf: the Ewald truncation error measured with enlarged
+                                   cutoffs stays above target_rel_err after 4 refinements;
+                                   the achieved value is in the message and pmfem_info            */
   PMFEM_E_STATE = 8,            /* call order (field evaluation before pmfem_build_pgf, host-only ctx)*/
   PMFEM_E_CUDA = 9,             /* a CUDA runtime error (message holds cudaGetErrorString)         */
   PMFEM_E_NCCL = 10,            /* a NCCL error (distributed contexts)                              */
@@ -62,10 +68,13 @@ typedef struct {
   const double*  Aex;       /* [n_regions] exchange stiffness, erg/cm                          */
 } pmfem_mesh;
 
-/* Periodicity (P:36-43 Eq. pm_cont; 1D, 2D or 3D along any axes). */
+/* Periodicity (P:36-43 Eq. pm_cont; 1D, 2D or 3D along any axes; P:277 uses z). */
 typedef struct {
-  int32_t periodic[3];      /* 1 = axis is periodic (at least one axis must be)                */
-  double  lattice[3];       /* period L_i along axis i (cm); ignored on non-periodic axes       */
+  int32_t periodic[3];      /* 1 = axis is periodic; none periodic = non-periodic mode (NEXT-3) */
+  double  lattice[3][3];    /* rows = lattice vectors (cm).  P:36-43 writes them L_x x^, L_y y^,
+                               L_z z^: they must be diagonal (|off-diagonal| <= 1e-12 x max |L_i|,
+                               else PMFEM_E_INVALID_ARG); lattice[i][i] = L_i > 0 on periodic axes,
+                               ignored on non-periodic axes                                      */
   double  match_tol;        /* T-PBC pair tolerance (cm); 0 -> 1e-6 x shortest edge */
 } pmfem_periodicity;
 
@@ -98,6 +107,9 @@ typedef struct {
                                                      (4 entries + 64-bit column header), 1 = B4
                                                      (aligned 4-column blocks + 32-bit block id)  */
   int64_t cbox_packed_units;                      /* C4x chunks or B4 blocks                     */
+  double  pgf_achieved_rel_err;                   /* pmfem_build_pgf: max |K(cutoffs) - K(enlarged
+                                                     cutoffs)| / max |K| over probe displacements
+                                                     (0 before build_pgf and in free space)      */
 } pmfem_info;
 
 /* Build a context: validate, orient, detect T-PBC pairs and fold them to LCAs,
@@ -131,10 +143,16 @@ pmfem_status pmfem_nccl_unique_id(void* out128);
 /* Tabulate the periodic Green's function K on the padded grid with Ewald sums in fp64
  * (Eq. 2 with k0 = 0; "exponentially rapidly convergent sums"; normalisation
  * R3), K(0) = G_p^reg(0), and store G_hat = real(FFT(K)) / (#FFT points), G_hat[0] = 0, as fp32
- * (P:204).  On a device context the tabulation and fp64 FFT run on the GPU. */
+ * (P:204).  On a device context the tabulation and fp64 FFT run on the GPU.
+ * target_rel_err (clamped to [1e-16, 1e-2]) sets the Ewald cutoffs (erfc(x_r) and
+ * exp(-k_max^2/4 alpha^2) at 1e-2 x target); the truncation error is then MEASURED as
+ * max |K - K'| / max |K| over 64 probe displacements, K' with enlarged cutoffs, and the cutoffs
+ * are tightened (x 1e-2, up to 4 times) until it is <= target; otherwise
+ * PMFEM_E_PGF_NOT_CONVERGED.  The reported error is at least DBL_EPSILON (2.2e-16): targets
+ * below fp64 resolution cannot be met.  The achieved value is reported in pmfem_info. */
 pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err);
 
-/* Field evaluations.  m: device pointer [N'][3] fp32 (internal node order, unit vectors);
+/* Field evaluations.  m: device pointer [N'_local][3] fp32 (internal node order, unit vectors);
  * H: device pointer [N'][3] fp32, written (not accumulated); must not alias m.
  * cuda_stream: a cudaStream_t or NULL for the legacy default stream.  Asynchronous: nothing
  * synchronises the host; kernel faults surface as PMFEM_E_CUDA on a later call. */

@@ -206,8 +206,8 @@ __device__ __forceinline__ int wrapi(int i, int n, int per) { return per ? (i >=
 // tile's (T2+P) x (T1+P) anchor lines, read through box_ptr.  A warp takes one line at a time,
 // lanes take its nodes.  Shared-memory fp32 atomics are CAS loops on sm_100 (ATOMS.CAST.SPIN),
 // so the tile accumulates in 32-bit fixed point with the native integer ATOMS.ADD: a first
-// sweep finds max|q| and the largest anchor-box population m_b of the tile's halo, which bound
-// every partial sum by 2 m_b (P+1)^3 max|q| (|Lagrange weight| <= 1 on the stencil interval,
+// sweep finds max|q| of the tile's halo; with m_b the largest anchor-box population of the mesh
+// (D.box_max, a global bound) every partial sum is bounded by 2 m_b (P+1)^3 max|q| (|Lagrange weight| <= 1 on the stencil interval,
 // x2 margin); the scale is the power of two that maps that bound to 2^30 (no overflow), so a
 // contribution is rounded to ~1e-7 of max|q| -- the level of fp32 accumulation -- and the sum is
 // order-independent (deterministic).  Each node is read by up to prod_a (T_a+P)/T_a tiles.
@@ -791,10 +791,14 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     int64_t target = 256;
     while (target < 4096 && target * 2 * 600 <= Gb) target *= 2;
     int t[3] = {1, 1, 1};
+    // the kernel's segment scan holds k2_nseg(t1, t2, P) <= 256 threads x 8 segments
+    auto nseg_ok = [&](int a) {
+      return k2_nseg(a == 1 ? 2 * t[1] : t[1], a == 2 ? 2 * t[2] : t[2], D.order) <= 2048;
+    };
     while ((int64_t)t[0] * t[1] * t[2] < target) {
       int best = -1;
       for (int a = 0; a < 3; ++a)
-        if (t[a] < D.n[a] && (best < 0 || t[a] < t[best])) best = a;
+        if (t[a] < D.n[a] && nseg_ok(a) && (best < 0 || t[a] < t[best])) best = a;
       if (best < 0) break;
       t[best] *= 2;
     }
@@ -806,6 +810,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       }
     }
     for (int a = 0; a < 3; ++a) D.k2_tile[a] = t[a];
+    if (k2_nseg(t[1], t[2], D.order) > 2048) throw Error(PMFEM_E_STATE, "K2 tile exceeds the segment scan capacity");
   }
   // ---- C_box: built on the device in internal order, stored in the chunked C4x format
   if (!S.cbox_device) throw Error(PMFEM_E_STATE, "device contexts build C_box on the device");

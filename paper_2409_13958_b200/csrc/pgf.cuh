@@ -20,6 +20,7 @@ struct PgfDev {
   double alpha;
   int nreal[3];       // real-space image range per periodic axis
   int mrec[3];        // reciprocal range per periodic axis
+  double xr;          // real-space cutoff alpha * r_c (erfc(xr) below the truncation target)
   double gl_x[64], gl_w[64];   // Gauss-Legendre on [0,1] for the incomplete Bessel integral
 };
 
@@ -89,7 +90,7 @@ PM_HD inline double pgf_eval(const PgfDev& P, const double r_in[3], bool self) {
   }
   for (int i = P.dim; i < 3; ++i) rf[i - P.dim] = self ? 0.0 : r_in[P.ax[i]];
   const double rf2 = rf[0] * rf[0] + rf[1] * rf[1];
-  const double rc = 6.2 / a;
+  const double rc = P.xr / a;
   // real-space sum over pruned images
   double real = 0.0;
   int n0 = P.nreal[0], n1 = P.dim > 1 ? P.nreal[1] : 0, n2 = P.dim > 2 ? P.nreal[2] : 0;

@@ -31,7 +31,7 @@ void gauss_legendre01(int n, double* x, double* w) {
   }
 }
 
-PgfParams make_pgf_params(const int periodic[3], const double L[3]) {
+PgfParams make_pgf_params(const int periodic[3], const double L[3], double target) {
   PgfParams P{};
   int k = 0;
   for (int a = 0; a < 3; ++a)
@@ -42,10 +42,13 @@ PgfParams make_pgf_params(const int periodic[3], const double L[3]) {
   double Lmin = 1e300;
   for (int i = 0; i < P.dim; ++i) Lmin = std::min(Lmin, P.L[i]);
   P.alpha = P.dim > 0 ? std::sqrt(M_PI) / Lmin : 1.0;   // dim 0: free space, alpha unused
-  const double kmax = 2.0 * P.alpha * std::sqrt(-std::log(1e-15)) * 1.1;
+  const double tol = 1e-2 * std::min(std::max(target, 1e-16), 1e-2);
+  P.xr = 1.0;
+  while (std::erfc(P.xr) > tol && P.xr < 7.0) P.xr += 0.05;
+  const double kmax = 2.0 * P.alpha * std::sqrt(-std::log(tol)) * 1.1;
   for (int i = 0; i < 3; ++i) {
     if (i < P.dim) {
-      P.nreal[i] = (int)std::ceil(6.2 / (P.alpha * P.L[i]) + 1.0);
+      P.nreal[i] = (int)std::ceil(P.xr / (P.alpha * P.L[i]) + 1.0);
       P.mrec[i] = (int)std::ceil(kmax * P.L[i] / (2 * M_PI)) + 1;
     } else {
       P.nreal[i] = 0;
@@ -60,8 +63,38 @@ static PgfDev to_dev(const PgfParams& P) {
   d.dim = P.dim;
   for (int i = 0; i < 3; ++i) { d.ax[i] = P.ax[i]; d.L[i] = P.L[i]; d.nreal[i] = P.nreal[i]; d.mrec[i] = P.mrec[i]; }
   d.alpha = P.alpha;
+  d.xr = P.xr;
   gauss_legendre01(64, d.gl_x, d.gl_w);
   return d;
+}
+
+double pgf_truncation_error(const HostSetup& S, const PgfParams& P) {
+  if (P.dim == 0) return 0.0;
+  PgfParams Q = P;                     // enlarged cutoffs: +1.5 in alpha r_c, +2 shells each way
+  Q.xr = P.xr + 1.5;
+  for (int i = 0; i < P.dim; ++i) {
+    Q.nreal[i] = (int)std::ceil(Q.xr / (Q.alpha * Q.L[i]) + 1.0);
+    Q.mrec[i] = P.mrec[i] + 2 + P.mrec[i] / 2;
+  }
+  const PgfDev a = to_dev(P), b = to_dev(Q);
+  // probes: the self value and 63 grid displacements j = (u_a (N_a - 1)) on a scrambled
+  // lattice of fractions u in (0, 1) (Weyl sequence), covering near and far displacements
+  double dmax = 0.0, kmax = 0.0;
+  for (int t = 0; t < 64; ++t) {
+    double r[3];
+    for (int x = 0; x < 3; ++x) {
+      const double u = std::fmod(0.5 + t * (x == 0 ? 0.7548776662 : x == 1 ? 0.5698402910 : 0.3319573700), 1.0);
+      const int j = (int)std::floor(u * S.grid_n[x]);
+      r[x] = j * S.delta[x];
+    }
+    const bool self = t == 0;
+    if (!self && r[0] == 0 && r[1] == 0 && r[2] == 0) continue;
+    const double ka = pgf_eval(a, r, self), kb = pgf_eval(b, r, self);
+    dmax = std::max(dmax, std::fabs(ka - kb));
+    kmax = std::max(kmax, std::fabs(kb));
+  }
+  // nothing is resolved below the fp64 unit roundoff: report at least DBL_EPSILON
+  return std::max(kmax > 0 ? dmax / kmax : 0.0, 2.220446049250313e-16);
 }
 
 void host_kernel_table(const HostSetup& S, const PgfParams& P, std::vector<double>& K) {

@@ -1,5 +1,6 @@
 // extern "C" entry points of libpmfem (include/pmfem.h).  No exception crosses the ABI.
 #include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -138,10 +139,26 @@ pmfem_status pmfem_nccl_unique_id(void* out128) {
 
 pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err) {
   if (!ctx) return PMFEM_E_INVALID_ARG;
-  (void)target_rel_err;   // the Ewald cutoffs are fixed at the 1e-15 level (reading R5)
   return guard(ctx, [&] {
+    pmfem::require(target_rel_err > 0 && std::isfinite(target_rel_err), PMFEM_E_INVALID_ARG,
+                   "target_rel_err must be positive");
     double t0 = now();
-    pmfem::PgfParams P = pmfem::make_pgf_params(ctx->S.periodic, ctx->S.L);
+    // Ewald cutoffs from the target, then the truncation error measured with enlarged cutoffs;
+    // tightened up to 4 times (report the achieved error, fail if the target is missed)
+    double tgt = target_rel_err;
+    pmfem::PgfParams P = pmfem::make_pgf_params(ctx->S.periodic, ctx->S.L, tgt);
+    double achieved = pmfem::pgf_truncation_error(ctx->S, P);
+    for (int it = 0; it < 4 && achieved > target_rel_err; ++it) {
+      tgt *= 1e-2;
+      P = pmfem::make_pgf_params(ctx->S.periodic, ctx->S.L, tgt);
+      achieved = pmfem::pgf_truncation_error(ctx->S, P);
+    }
+    ctx->S.pgf_achieved_rel_err = achieved;
+    if (achieved > target_rel_err) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "PGF truncation error %.3e above target %.3e", achieved, target_rel_err);
+      throw pmfem::Error(PMFEM_E_PGF_NOT_CONVERGED, buf);
+    }
     if (ctx->host_only) {
       pmfem::host_kernel_table(ctx->S, P, ctx->S.kernel);
       pmfem::host_fft_spectrum(ctx->S, ctx->S.kernel, ctx->S.spectrum);
@@ -304,6 +321,7 @@ pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out) {
   out->slab_world = ctx->D.slab_world;
   out->cbox_format = ctx->D.cbox_format;
   out->cbox_packed_units = ctx->D.cbox_chunks;
+  out->pgf_achieved_rel_err = ctx->S.pgf_achieved_rel_err;
   out->comm_bytes_per_eval = ctx->D.comm_bytes_per_eval;
   out->setup_seconds = S.setup_seconds;
   out->pgf_seconds = S.pgf_seconds;

@@ -98,6 +98,7 @@ struct HostSetup {
   std::vector<double> kernel;       // host-only contexts: K table [fft2][fft1][fft0]
   std::vector<double> spectrum;     // host-only: G_hat half spectrum [fft2][fft1][fft0/2+1]
   double setup_seconds = 0, pgf_seconds = 0;
+  double pgf_achieved_rel_err = 0;
   DistPlan dist;
 };
 
@@ -120,8 +121,14 @@ struct PgfParams {
   double alpha;
   int nreal[3];
   int mrec[3];
+  double xr;              // real-space cutoff alpha * r_c
 };
-PgfParams make_pgf_params(const int periodic[3], const double L[3]);
+// Ewald parameters for a truncation target (clamped to [1e-16, 1e-2]): erfc(xr) and
+// exp(-kmax^2 / 4 alpha^2) at 1e-2 x target
+PgfParams make_pgf_params(const int periodic[3], const double L[3], double target = 1e-15);
+// measured truncation error of P: max |K_P - K_P'| / max |K_P'| over probe displacements of the
+// AIM grid, P' = P with enlarged cutoffs (0 in free space)
+double pgf_truncation_error(const HostSetup& S, const PgfParams& P);
 void gauss_legendre01(int n, double* x, double* w);
 void host_kernel_table(const HostSetup& S, const PgfParams& P, std::vector<double>& K);
 void host_fft_spectrum(const HostSetup& S, const std::vector<double>& K, std::vector<double>& Ghat);

@@ -69,6 +69,11 @@ void setup_aim(HostSetup& S, const pmfem_grid* g) {
     }
     require(is_pow2(S.fft_n[a]), PMFEM_E_INVALID_ARG, "FFT length must be a power of two on every axis");
   }
+  // shared-memory limits of the FFT passes (device.cu): the fp64 PGF transform stages 16 lines of
+  // P complex doubles per CTA along axes 1 and 2 (P <= 512 in 227 KB), the x pass <= 4096
+  // complex per line
+  require(S.fft_n[1] <= 512 && S.fft_n[2] <= 512 && S.fft_n[0] <= 8192, PMFEM_E_INVALID_ARG,
+          "FFT lengths above the shared-memory limits (axis 0 <= 8192, axes 1, 2 <= 512)");
   // r_ER = s * max(Delta) on every axis (R8); validity on periodic axes (K8)
   const double rer = S.rer_scale * std::max(S.delta[0], std::max(S.delta[1], S.delta[2]));
   for (int a = 0; a < 3; ++a)
@@ -83,6 +88,10 @@ void setup_aim(HostSetup& S, const pmfem_grid* g) {
   for (int64_t n = 0; n < Np; ++n)
     for (int a = 0; a < 3; ++a) {
       double t = (S.xw[3 * n + a] - S.origin[a]) / S.delta[a];
+      // the grid spans the node extent, so only corrupted coordinates leave it
+      require(std::isfinite(t) && (S.periodic[a] ? (t >= 0.0 && t < S.grid_n[a] + 1e-9)
+                                                 : (t >= -1e-9 && t <= S.grid_n[a] - 1 + 1e-9)),
+              PMFEM_E_OUTSIDE_GRID, "node outside the AIM grid on axis " + std::to_string(a));
       int64_t s = (p % 2) ? (int64_t)std::floor(t) - (p - 1) / 2 : (int64_t)std::floor(t + 0.5) - p / 2;
       if (!S.periodic[a]) s = std::min<int64_t>(std::max<int64_t>(s, 0), S.grid_n[a] - 1 - p);
       S.st_s[3 * n + a] = (int32_t)s;

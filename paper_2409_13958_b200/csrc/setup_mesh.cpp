@@ -89,9 +89,19 @@ void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* p
   S.xyz.assign(mesh->xyz, mesh->xyz + 3 * S.N);
   S.tets.assign(mesh->tets, mesh->tets + 4 * S.T);
   int nper = 0;
+  // lattice vectors: rows of lattice[3][3]; P:36-43 writes them L_x x^, L_y y^, L_z z^, so they
+  // must be diagonal (the grid, stencils and FFT are axis-aligned)
+  double lmax = 0.0;
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b) lmax = std::max(lmax, std::fabs(per->lattice[a][b]));
+  for (int a = 0; a < 3; ++a)
+    for (int b = 0; b < 3; ++b)
+      if (a != b)
+        require(std::fabs(per->lattice[a][b]) <= 1e-12 * lmax, PMFEM_E_INVALID_ARG,
+                "non-diagonal lattice vectors (P:36 uses L_x x, L_y y, L_z z)");
   for (int a = 0; a < 3; ++a) {
     S.periodic[a] = per->periodic[a] ? 1 : 0;
-    S.L[a] = S.periodic[a] ? per->lattice[a] : 0.0;
+    S.L[a] = S.periodic[a] ? per->lattice[a][a] : 0.0;
     if (S.periodic[a]) require(S.L[a] > 0, PMFEM_E_INVALID_ARG, "non-positive period");
     nper += S.periodic[a];
   }

@@ -41,7 +41,7 @@ class _Mesh(ctypes.Structure):
 
 
 class _Periodicity(ctypes.Structure):
-    _fields_ = [("periodic", ctypes.c_int32 * 3), ("lattice", ctypes.c_double * 3),
+    _fields_ = [("periodic", ctypes.c_int32 * 3), ("lattice", (ctypes.c_double * 3) * 3),
                 ("match_tol", ctypes.c_double)]
 
 
@@ -60,7 +60,7 @@ class _Info(ctypes.Structure):
                 ("launches_per_eval", ctypes.c_int32), ("fft_fused", ctypes.c_int32),
                 ("comm_bytes_per_eval", ctypes.c_double), ("k2_tile", ctypes.c_int32 * 3),
                 ("slab_world", ctypes.c_int32), ("cbox_format", ctypes.c_int32),
-                ("cbox_packed_units", ctypes.c_int64)]
+                ("cbox_packed_units", ctypes.c_int64), ("pgf_achieved_rel_err", ctypes.c_double)]
 
 
 _vp = ctypes.c_void_p
@@ -105,11 +105,27 @@ def _ptr(a, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
 
 
-def _dev_ptr(t):
+def _dev_ptr(t, rows=None, device=None):
+    """Device pointer of a contiguous float32 CUDA tensor [rows, 3] on `device` (the ABI takes
+    no row count: a wrong shape or device would read/write out of bounds, so it is checked here)."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
         raise TypeError("expected a contiguous float32 CUDA tensor")
+    if rows is not None and tuple(t.shape) != (rows, 3):
+        raise ValueError("expected shape (%d, 3), got %s" % (rows, tuple(t.shape)))
+    if device is not None and t.device.index != device:
+        raise ValueError("tensor on cuda:%s, context on cuda:%d" % (t.device.index, device))
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _host_ptr(t, rows):
+    """Host pointer of a contiguous float32 CPU tensor [rows, 3]."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and not t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError("expected a contiguous float32 CPU tensor")
+    if tuple(t.shape) != (rows, 3):
+        raise ValueError("expected shape (%d, 3), got %s" % (rows, tuple(t.shape)))
+    return _vp(t.data_ptr())
 
 
 class Context:
@@ -129,8 +145,14 @@ class Context:
             region = np.ascontiguousarray(region, dtype=np.int32)
             self._keep.append(region)
             m.region = _ptr(region, ctypes.c_int32)
-        p = _Periodicity((ctypes.c_int32 * 3)(*[int(bool(v)) for v in periodic]),
-                         (ctypes.c_double * 3)(*[float(v) for v in lattice]), float(match_tol))
+        # lattice: 3 periods (the diagonal) or 3x3 lattice vectors (rows; must be diagonal)
+        lat = np.asarray(lattice, dtype=np.float64)
+        if lat.shape == (3,):
+            lat = np.diag(lat)
+        if lat.shape != (3, 3):
+            raise ValueError("lattice must be 3 periods or a 3x3 matrix of lattice vectors")
+        latc = ((ctypes.c_double * 3) * 3)(*[(ctypes.c_double * 3)(*[float(v) for v in row]) for row in lat])
+        p = _Periodicity((ctypes.c_int32 * 3)(*[int(bool(v)) for v in periodic]), latc, float(match_tol))
         g = _Grid((ctypes.c_int32 * 3)(*[int(v) for v in grid_n]), int(order), float(rer_scale), int(z0_ring))
         h = _vp()
         if world == 1:
@@ -176,7 +198,8 @@ class Context:
         import torch
         if H is None:
             H = torch.empty_like(m)
-        fn_st = fn(self._h, _dev_ptr(m), _dev_ptr(H), self._stream(stream))
+        n = self.n_parents_local
+        fn_st = fn(self._h, _dev_ptr(m, n, self.device), _dev_ptr(H, n, self.device), self._stream(stream))
         self._check(fn_st)
         return H
 
@@ -196,14 +219,14 @@ class Context:
             m_host = torch.from_numpy(np.ascontiguousarray(m_host, dtype=np.float32))
         if H_host is None:
             H_host = torch.empty_like(m_host)
-        self._check(_lib.pmfem_heff_host(self._h, _vp(m_host.data_ptr()), _vp(H_host.data_ptr()),
-                                         self._stream(stream)))
+        n = self.n_parents_local
+        self._check(_lib.pmfem_heff_host(self._h, _host_ptr(m_host, n), _host_ptr(H_host, n), self._stream(stream)))
         return H_host
 
     def llg_rk4(self, m, steps, dt, alpha, gamma=1.7595e7, H_applied=(0.0, 0.0, 0.0), stream=None):
         """`steps` RK4 steps of the LLG equation on m (float32 CUDA tensor [N'_local, 3], in place)."""
         hap = (ctypes.c_double * 3)(*[float(v) for v in H_applied])
-        self._check(_lib.pmfem_llg_rk4(self._h, _dev_ptr(m), int(steps), float(dt), float(alpha), float(gamma),
+        self._check(_lib.pmfem_llg_rk4(self._h, _dev_ptr(m, self.n_parents_local, self.device), int(steps), float(dt), float(alpha), float(gamma),
                                        ctypes.cast(hap, ctypes.c_void_p), self._stream(stream)))
         return m
 
