@@ -8,7 +8,10 @@
 // Pass 1 counts the near pairs of every row, the host scans, pass 2 writes columns (in
 // increasing order, by construction) and values; the rows are then packed into the C4x
 // chunk format K4 streams (6 bytes per entry instead of 8 for a column + value CSR).
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -104,43 +107,143 @@ __global__ void k_cbox_count(CboxGeom c, long long Np, const double* __restrict_
   cnt[n] = k_cnt;
 }
 
+// C_box entry (K9) of the near pair (n, k, img): G0*(d) - sum_{a,b} w_na w_kb G0*((a - b - img N) o Delta),
+// the double stencil sum regrouped per axis into the (2p+1)-point convolution cw of the two
+// weight vectors (exact algebraic regrouping)
+__device__ __forceinline__ double cbox_entry(const CboxGeom& c, const double (*wn)[4], const double* __restrict__ t_loc,
+                                             const int* __restrict__ s_unw, long long n, int k, const double* d,
+                                             const int* img) {
+  const int p = c.p, p1 = p + 1, W = 2 * p + 1;
+  const double r = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+  const double v = r > 0 ? 1.0 / r : 0.0;
+  double wk[3][4], cw[3][7];
+  int base[3];
+  for (int a = 0; a < 3; ++a) {
+    lagr_d(t_loc[3 * (long long)k + a], p, wk[a]);
+    base[a] = s_unw[3 * n + a] - s_unw[3 * (long long)k + a] - img[a] * c.n[a] - p;
+    for (int e = 0; e < W; ++e) cw[a][e] = 0.0;
+    for (int i = 0; i < p1; ++i)
+      for (int j = 0; j < p1; ++j) cw[a][i - j + p] += wn[a][i] * wk[a][j];
+  }
+  double gm = 0.0;
+  for (int ex = 0; ex < W; ++ex) {
+    const double dx = (base[0] + ex) * c.delta[0];
+    for (int ey = 0; ey < W; ++ey) {
+      const double dy = (base[1] + ey) * c.delta[1];
+      const double wxy = cw[0][ex] * cw[1][ey];
+      for (int ez = 0; ez < W; ++ez) {
+        const double dz = (base[2] + ez) * c.delta[2];
+        const double rr = dx * dx + dy * dy + dz * dz;
+        if (rr > 0) gm += wxy * cw[2][ez] / sqrt(rr);
+      }
+    }
+  }
+  return v - gm;
+}
+
 __global__ void k_cbox_fill(CboxGeom c, long long Np, const double* __restrict__ xw, const int* __restrict__ box_ptr,
                             const int* __restrict__ s_unw, const double* __restrict__ t_loc,
                             const long long* __restrict__ rowptr, int* __restrict__ col, float* __restrict__ val) {
   const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= Np) return;
-  const int p = c.p, p1 = p + 1, W = 2 * p + 1;
   double wn[3][4];
-  for (int a = 0; a < 3; ++a) lagr_d(t_loc[3 * n + a], p, wn[a]);
+  for (int a = 0; a < 3; ++a) lagr_d(t_loc[3 * n + a], c.p, wn[a]);
   long long o = rowptr[n];
   for_near(c, xw, box_ptr, n, [&](int k, const double* d, const int* img) {
-    const double r = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-    double v = r > 0 ? 1.0 / r : 0.0;
-    double wk[3][4], cw[3][7];
-    int base[3];
-    for (int a = 0; a < 3; ++a) {
-      lagr_d(t_loc[3 * (long long)k + a], p, wk[a]);
-      base[a] = s_unw[3 * n + a] - s_unw[3 * (long long)k + a] - img[a] * c.n[a] - p;
-      for (int e = 0; e < W; ++e) cw[a][e] = 0.0;
-      for (int i = 0; i < p1; ++i)
-        for (int j = 0; j < p1; ++j) cw[a][i - j + p] += wn[a][i] * wk[a][j];
-    }
-    double gm = 0.0;
-    for (int ex = 0; ex < W; ++ex) {
-      const double dx = (base[0] + ex) * c.delta[0];
-      for (int ey = 0; ey < W; ++ey) {
-        const double dy = (base[1] + ey) * c.delta[1];
-        const double wxy = cw[0][ex] * cw[1][ey];
-        for (int ez = 0; ez < W; ++ez) {
-          const double dz = (base[2] + ez) * c.delta[2];
-          const double rr = dx * dx + dy * dy + dz * dz;
-          if (rr > 0) gm += wxy * cw[2][ez] / sqrt(rr);
-        }
+    col[o] = k;
+    val[o] = (float)cbox_entry(c, wn, t_loc, s_unw, n, k, d, img);
+    ++o;
+  });
+}
+
+// ---- SEG: candidate enumeration (device.cuh seg_axis) shared by the builder and K4
+template <class F>
+__device__ void for_cand(const SegGeom& G, const int* __restrict__ box_ptr, int4 s, F&& f) {
+  int rz[4], ry[4], rx[4];
+  const int nz = seg_axis(G, 2, s.z, rz), ny = seg_axis(G, 1, s.y, ry), nx = seg_axis(G, 0, s.x, rx);
+  const int lz = seg_len(rz, nz), ly = seg_len(ry, ny);
+  int c = 0;
+  for (int iz = 0; iz < lz; ++iz) {
+    const int z = seg_at(rz, iz);
+    for (int iy = 0; iy < ly; ++iy) {
+      const long long line = ((long long)z * G.n[1] + seg_at(ry, iy)) * G.n[0];
+      for (int ix = 0; ix < nx; ++ix) {
+        const int k0 = box_ptr[line + rx[2 * ix]], k1 = box_ptr[line + rx[2 * ix + 1] + 1];
+        for (int k = k0; k < k1; ++k) f(k, c++);
       }
     }
-    col[o] = k;
-    val[o] = (float)(v - gm);
-    ++o;
+  }
+}
+
+// K8 near test of the candidate pair (n, k) with its minimum image (as for_near)
+__device__ __forceinline__ bool near_pair(const CboxGeom& c, const double* xn, const double* __restrict__ xw, int k,
+                                          double* d, int* img) {
+  bool in = true;
+  for (int a = 0; a < 3; ++a) {
+    d[a] = xn[a] - xw[3 * (long long)k + a];
+    img[a] = 0;
+    if (c.per[a]) { img[a] = (int)rint(d[a] / c.L[a]); d[a] -= img[a] * c.L[a]; }
+    in &= fabs(d[a]) <= c.rer;
+  }
+  return in;
+}
+
+// per row: near pairs among the candidates, candidate count, number of column runs
+__global__ void k_seg_count(CboxGeom c, SegGeom G, long long Np, const double* __restrict__ xw,
+                            const int* __restrict__ box_ptr, const int4* __restrict__ st, int* __restrict__ nnear,
+                            int* __restrict__ ncand, int* __restrict__ nseg) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  const double xn[3] = {xw[3 * n], xw[3 * n + 1], xw[3 * n + 2]};
+  int cnt = 0, cc = 0;
+  for_cand(G, box_ptr, st[n], [&](int k, int) {
+    double d[3];
+    int img[3];
+    cnt += near_pair(c, xn, xw, k, d, img);
+    ++cc;
+  });
+  int rz[4], ry[4], rx[4];
+  const int4 s = st[n];
+  const int nz = seg_axis(G, 2, s.z, rz), ny = seg_axis(G, 1, s.y, ry), nx = seg_axis(G, 0, s.x, rx);
+  nnear[n] = cnt;
+  ncand[n] = cc;
+  nseg[n] = seg_len(rz, nz) * seg_len(ry, ny) * nx;
+}
+
+__global__ void k_seg_fill(CboxGeom c, SegGeom G, long long Np, const double* __restrict__ xw,
+                           const int* __restrict__ box_ptr, const int4* __restrict__ st, const int* __restrict__ s_unw,
+                           const double* __restrict__ t_loc, const long long* __restrict__ moff,
+                           const long long* __restrict__ voff, uint32_t* __restrict__ mask, float* __restrict__ val) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  const double xn[3] = {xw[3 * n], xw[3 * n + 1], xw[3 * n + 2]};
+  double wn[3][4];
+  for (int a = 0; a < 3; ++a) lagr_d(t_loc[3 * n + a], c.p, wn[a]);
+  uint32_t bits = 0;
+  long long o = voff[n];
+  int last = -1;
+  for_cand(G, box_ptr, st[n], [&](int k, int ci) {
+    double d[3];
+    int img[3];
+    if (near_pair(c, xn, xw, k, d, img)) {
+      bits |= 1u << (ci & 31);
+      val[o++] = (float)cbox_entry(c, wn, t_loc, s_unw, n, k, d, img);
+    }
+    if ((ci & 31) == 31) { mask[moff[n] + (ci >> 5)] = bits; bits = 0; }
+    last = ci;
+  });
+  if (last >= 0 && (last & 31) != 31) mask[moff[n] + (last >> 5)] = bits;
+}
+
+// expand SEG rows to (column, value) lists (pmfem_export of the device C_box, tests)
+__global__ void k_seg_decode(SegGeom G, long long Np, const int* __restrict__ box_ptr, const int4* __restrict__ st,
+                             const long long* __restrict__ moff, const long long* __restrict__ voff,
+                             const uint32_t* __restrict__ mask, int* __restrict__ col) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long o = voff[n];
+  for_cand(G, box_ptr, st[n], [&](int k, int ci) {
+    if ((mask[moff[n] + (ci >> 5)] >> (ci & 31)) & 1u) col[o++] = k;
   });
 }
 
@@ -242,6 +345,16 @@ T* dup_c(const std::vector<T>& v) {
 // Builds the C4x arrays D.c_ptr (chunk offsets) / D.c_hdr / D.c_val in internal order on the
 // device.  Needs D.box_ptr (anchor-box row pointers of the internal order).  Returns the number
 // of near pairs.
+// SEG rows expanded to column lists (tests): col[voff[n] + j] for the j-th near pair of row n
+void device_seg_decode(const DeviceState& D, int* d_col) {
+  const unsigned blocks = (unsigned)((D.Np + 127) / 128);
+  k_seg_decode<<<blocks, 128>>>(D.seg, D.Np, D.box_ptr, reinterpret_cast<const int4*>(D.st_s),
+                                reinterpret_cast<const long long*>(D.seg_moff), reinterpret_cast<const long long*>(D.c_ptr),
+                                D.seg_mask, d_col);
+  CKC(cudaGetLastError());
+  CKC(cudaDeviceSynchronize());
+}
+
 int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   CKC(cudaSetDevice(D.device));
   const int64_t Np = S.Np;
@@ -279,6 +392,69 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   std::vector<long long> ptr(Np + 1, 0);
   for (int64_t i = 0; i < Np; ++i) ptr[i + 1] = ptr[i] + cnt[i];
   const int64_t nnz = ptr[Np];
+  // ---- SEG (default): candidate reach R_a = ceil(rho_a + 1) - 1, rho_a = r_ER / Delta_a; usable
+  // when every row's near set (the for_near count above) is found among its candidates
+  const char* fmt_env = std::getenv("PMFEM_CBOX_FORMAT");
+  const std::string fmt = fmt_env ? std::string(fmt_env) : std::string("seg");
+  if (fmt == "seg") {
+    SegGeom G{};
+    for (int a = 0; a < 3; ++a) {
+      const double rho = c.rer / c.delta[a];
+      G.R[a] = (int)std::ceil(rho + 1.0) - 1;
+      G.n[a] = c.n[a];
+      G.per[a] = c.per[a];
+      G.lim[a] = c.per[a] ? c.n[a] - 1 : c.n[a] - 1 - p;
+    }
+    int* d_near = dalloc_c<int>(Np);
+    int* d_cand = dalloc_c<int>(Np);
+    int* d_nseg = dalloc_c<int>(Np);
+    const int4* d_st = reinterpret_cast<const int4*>(D.st_s);
+    k_seg_count<<<blocks, 128>>>(c, G, Np, d_xw, D.box_ptr, d_st, d_near, d_cand, d_nseg);
+    CKC(cudaGetLastError());
+    std::vector<int> nnear(Np), ncand(Np), nseg(Np);
+    CKC(cudaMemcpy(nnear.data(), d_near, sizeof(int) * Np, cudaMemcpyDeviceToHost));
+    CKC(cudaMemcpy(ncand.data(), d_cand, sizeof(int) * Np, cudaMemcpyDeviceToHost));
+    CKC(cudaMemcpy(nseg.data(), d_nseg, sizeof(int) * Np, cudaMemcpyDeviceToHost));
+    bool ok = true;
+    int maxseg = 0;
+    for (int64_t i = 0; i < Np && ok; ++i) {
+      ok = nnear[i] == cnt[i];
+      maxseg = std::max(maxseg, nseg[i]);
+    }
+    if (ok && maxseg <= SEG_MAXSEG) {
+      std::vector<long long> moff(Np + 1, 0), voff(Np + 1, 0);
+      for (int64_t i = 0; i < Np; ++i) {
+        moff[i + 1] = moff[i] + (ncand[i] + 31) / 32;
+        voff[i + 1] = voff[i] + nnear[i];
+      }
+      long long* d_moff = dup_c(moff);
+      long long* d_voff = dup_c(voff);
+      uint32_t* d_mask = dalloc_c<uint32_t>(moff[Np]);
+      float* d_val = dalloc_c<float>(voff[Np] + 4);
+      CKC(cudaMemset(d_mask, 0, sizeof(uint32_t) * std::max<long long>(moff[Np], 1)));
+      CKC(cudaMemset(d_val, 0, sizeof(float) * (voff[Np] + 4)));
+      k_seg_fill<<<blocks, 128>>>(c, G, Np, d_xw, D.box_ptr, d_st, d_su, d_tl, d_moff, d_voff, d_mask, d_val);
+      CKC(cudaGetLastError());
+      CKC(cudaDeviceSynchronize());
+      D.c_ptr = reinterpret_cast<int64_t*>(d_voff);
+      D.seg_moff = reinterpret_cast<int64_t*>(d_moff);
+      D.seg_mask = d_mask;
+      D.c_val = d_val;
+      D.seg = G;
+      D.seg_maxseg = maxseg;
+      D.seg_mask_words = moff[Np];
+      D.cbox_chunks = moff[Np];
+      D.cbox_format = 2;
+      D.cbox_nnz = nnz;
+      cudaFree(d_near); cudaFree(d_cand); cudaFree(d_nseg);
+      cudaFree(d_xw); cudaFree(d_tl); cudaFree(d_su); cudaFree(d_cnt);
+      return nnz;
+    }
+    cudaFree(d_near); cudaFree(d_cand); cudaFree(d_nseg);
+    if (std::getenv("PMFEM_VERBOSE"))
+      std::fprintf(stderr, "[pmfem] SEG C_box not usable (near sets %s, max runs %d): packed format\n",
+                   ok ? "covered" : "NOT covered", maxseg);
+  }
   long long* d_ptr = dup_c(ptr);
   int* d_col = dalloc_c<int>(nnz);
   float* d_val = dalloc_c<float>(nnz);
@@ -298,10 +474,8 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   // measured C2 +11 % bytes -> K4 4 % faster, C3 +33 % bytes -> 46 % slower);
   // PMFEM_CBOX_FORMAT=c4x|b4 forces one (tests)
   bool use_b4 = 20.0 * bptr[Np] <= 1.15 * 24.0 * cptr[Np];
-  if (const char* e = std::getenv("PMFEM_CBOX_FORMAT")) {
-    if (std::string(e) == "c4x") use_b4 = false;
-    else if (std::string(e) == "b4") use_b4 = true;
-  }
+  if (fmt == "c4x") use_b4 = false;
+  else if (fmt == "b4") use_b4 = true;
   if (use_b4) {
     long long* d_bptr = dup_c(bptr);
     int* d_bidx = dalloc_c<int>(bptr[Np]);

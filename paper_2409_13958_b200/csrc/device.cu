@@ -464,6 +464,110 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   if (valid && lane == 0) u[n] = acc + uloc[n];
 }
 
+// K4 over the SEG C_box (cbox_format 2, device.cuh): G lanes per row.  The lanes first build the
+// row's table of column runs in shared memory -- one run per (z, y) candidate anchor line and x
+// subrange, [box_ptr(line + xa), box_ptr(line + xb + 1)) -- with an exclusive scan of the run
+// lengths; then per 32-candidate mask word each lane takes candidates sub * G + lane: a set bit
+// selects the next stored value (rank = popcount of the lower bits) and q at the candidate's
+// column, found by a per-lane cursor over the runs (candidates are visited in increasing order).
+// No column indices are streamed and the q reads walk contiguous runs.
+template <int P, int G>
+__global__ void __launch_bounds__(256) k4_seg(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
+                                              const float4* __restrict__ st_t, GridDims g, SegGeom sg, int maxseg,
+                                              const int* __restrict__ box_ptr, const int64_t* __restrict__ moff,
+                                              const int64_t* __restrict__ voff, const uint32_t* __restrict__ mask,
+                                              const float* __restrict__ val, const float* __restrict__ q,
+                                              const float* __restrict__ uloc, float* __restrict__ u) {
+  extern __shared__ int k4s_smem[];
+  const int lane = threadIdx.x & (G - 1);
+  const int grp = threadIdx.x / G;
+  int* beg = k4s_smem + grp * (2 * maxseg + 2);
+  int* cum = beg + maxseg;                    // maxseg + 1 entries
+  const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x / G) + grp;
+  const bool valid = n < rr.row1;
+  const unsigned gmask = G == 32 ? 0xffffffffu : (((1u << G) - 1) << ((threadIdx.x & 31) & ~(G - 1)));
+  float acc = 0.f;
+  int4 s = make_int4(0, 0, 0, 0);
+  if (valid) s = st_s[n];
+  // ---- runs of candidate columns
+  int rz[4], ry[4], rx[4];
+  const int nz = seg_axis(sg, 2, s.z, rz), ny = seg_axis(sg, 1, s.y, ry), nx = seg_axis(sg, 0, s.x, rx);
+  const int lz = seg_len(rz, nz), ly = seg_len(ry, ny);
+  const int nseg = valid ? lz * ly * nx : 0;
+  int carry = 0;
+  for (int b0 = 0; b0 < nseg; b0 += G) {
+    const int sgi = b0 + lane;
+    int len = 0;
+    if (sgi < nseg) {
+      const int xi = sgi % nx, li = sgi / nx;
+      const int z = seg_at(rz, li / ly), y = seg_at(ry, li - (li / ly) * ly);
+      const int64_t line = ((int64_t)z * g.n1 + y) * g.n0;
+      const int k0 = __ldg(box_ptr + line + rx[2 * xi]), k1 = __ldg(box_ptr + line + rx[2 * xi + 1] + 1);
+      beg[sgi] = k0;
+      len = k1 - k0;
+    }
+    int incl = len;
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) {
+      const int v = __shfl_up_sync(gmask, incl, o, G);
+      if (lane >= o) incl += v;
+    }
+    if (sgi < nseg) cum[sgi] = carry + incl - len;
+    carry += __shfl_sync(gmask, incl, G - 1, G);
+  }
+  if (lane == 0) cum[nseg] = carry;
+  __syncwarp();
+  const int ncand = carry;
+  // ---- masked candidate loop
+  if (valid && ncand > 0) {
+    const uint32_t* M = mask + moff[n];
+    const float* V = val + voff[n];
+    const int nwords = (ncand + 31) >> 5;
+    int base = 0, sidx = 0;
+    for (int w = 0; w < nwords; ++w) {
+      const uint32_t word = __ldg(M + w);
+#pragma unroll
+      for (int sub = 0; sub < 32 / G; ++sub) {
+        const int bp = sub * G + lane;
+        if ((word >> bp) & 1u) {
+          const int c = (w << 5) + bp;
+          while (cum[sidx + 1] <= c) ++sidx;
+          const int k = beg[sidx] + (c - cum[sidx]);
+          acc = fmaf(__ldg(V + base + __popc(word & ((1u << bp) - 1u))), __ldg(q + k), acc);
+        }
+      }
+      base += __popc(word);
+    }
+  }
+  // ---- interpolation P^T U (as k4_interp_corr)
+  constexpr int NR = (P + 1) * (P + 1);
+  if (valid) {
+    const float4 t = st_t[n];
+    float wx[P + 1], wy[P + 1], wz[P + 1];
+    lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+    int ix[P + 1];
+#pragma unroll
+    for (int i = 0; i <= P; ++i) ix[i] = wrapi(s.x + i, g.n0, g.per0);
+    for (int r = lane; r < NR; r += G) {
+      const int jy = r % (P + 1), jz = r / (P + 1);
+      float wyz = 0.f;
+#pragma unroll
+      for (int a = 0; a <= P; ++a)
+#pragma unroll
+        for (int b = 0; b <= P; ++b)
+          if (a == jy && b == jz) wyz = wy[a] * wz[b];
+      const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+      float v = 0.f;
+#pragma unroll
+      for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(row + ix[i]), v);
+      acc = fmaf(wyz, v, acc);
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (valid && lane == 0) u[n] = acc + uloc[n];
+}
+
 // ------------------------------------------------------------------ K5 gradient + sum
 template <int SPLIT>
 __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __restrict__ u, const int64_t* __restrict__ sl1_off,
@@ -835,6 +939,13 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     if (plane_bytes <= 200 * 1024 && std::getenv("PMFEM_FFT_SPLIT") == nullptr) {
       int tile = 1;
       while (tile < 4 && plane_bytes * tile * 2 <= 96 * 1024 && (D.H0 + 2 * tile - 1) / (2 * tile) >= 148) tile *= 2;
+      // PMFEM_YZ_TILE=1|2|4|8 forces the column tile when its planes fit (tests run tile > 1 on
+      // small grids: the production tile-4 plan of C5 has H0 = 1025)
+      if (const char* e = std::getenv("PMFEM_YZ_TILE")) {
+        const int tv = std::atoi(e);
+        if ((tv == 1 || tv == 2 || tv == 4 || tv == 8) && (size_t)D.P[1] * D.P[2] * tv * sizeof(float2) <= 200 * 1024)
+          tile = tv;
+      }
       D.fused_tile = tile;
       // PMFEM_YZ_HALF=1: the split-z fused kernel for tile-1 columns with a zero-padded z axis
       // (opt-in: measured slower, C3 FFT 0.156 -> 0.182 ms -- more barriers per column)
@@ -896,6 +1007,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     // K4 group size: ~4+ chunks per lane; PMFEM_K4_GROUP overrides (tests)
     const double row4 = (double)D.cbox_chunks / std::max<int64_t>(Np, 1);
     D.k4_group = row4 >= 96 ? 32 : (row4 >= 40 ? 16 : 8);
+    if (D.cbox_format == 2) D.k4_group = 16;   // SEG: mask words per row (A/B: PMFEM_K4_GROUP)
     if (const char* e = std::getenv("PMFEM_K4_GROUP")) {
       const int gsel = std::atoi(e);
       if (gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
@@ -903,7 +1015,11 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   }
   // C_box per near pair: C4x 4-byte value + 2 bytes of chunk header, B4 4-byte value + 1 byte
   // of block index (chunk padding / empty block slots are format overhead, not counted)
-  D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + G * 4.0;
+  // SEG: 4-byte value per near pair + the candidate bitmask words + two 8-byte row offsets
+  if (D.cbox_format == 2)
+    D.kernel_bytes[3] = Np * (16.0 + 16 + 16 + 4 + 4 + 4) + (double)cnnz * 4 + (double)D.seg_mask_words * 4 + G * 4.0;
+  else
+    D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + G * 4.0;
   D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
 
@@ -952,6 +1068,7 @@ void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
   void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_bidx, D.c_val,
+                  D.seg_moff, D.seg_mask,
                   D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
                   D.send_buf, D.recv_buf, D.slab_cx, D.slab_buf, D.slab_spec, D.send_idx[0], D.send_idx[1], D.send_idx[2],
@@ -1188,6 +1305,26 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   halo(D, 1, D.q, 1, st);
   mark(3);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
+  if (D.cbox_format == 2) {
+    const int G = D.k4_group;
+    const size_t smem = sizeof(int) * (size_t)(256 / G) * (2 * D.seg_maxseg + 2);
+    const unsigned blocks = (unsigned)((nrows * G + 255) / 256);
+#define K4S_LAUNCH(PP, GG)                                                                                 \
+  do {                                                                                                     \
+    CK(cudaFuncSetAttribute(k4_seg<PP, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
+    k4_seg<PP, GG><<<blocks, 256, smem, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.seg, D.seg_maxseg, D.box_ptr,    \
+                                              D.seg_moff, D.c_ptr, D.seg_mask, D.c_val, D.q, D.uloc, D.u); \
+  } while (0)
+#define K4S_BY_G(PP) \
+  if (G == 8) K4S_LAUNCH(PP, 8); else if (G == 16) K4S_LAUNCH(PP, 16); else K4S_LAUNCH(PP, 32)
+    switch (D.order) {
+      case 1: K4S_BY_G(1); break;
+      case 2: K4S_BY_G(2); break;
+      default: K4S_BY_G(3); break;
+    }
+#undef K4S_BY_G
+#undef K4S_LAUNCH
+  } else
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
   (D.cbox_format == 1                                                                                   \

@@ -13,6 +13,45 @@ namespace pmfem {
 __host__ __device__ __forceinline__ int slab_h0(int p, int H0, int W) { return p * (H0 / W) + (p < H0 % W ? p : H0 % W); }
 __host__ __device__ __forceinline__ int slab_hn(int p, int H0, int W) { return H0 / W + (p < H0 % W ? 1 : 0); }
 
+// ---- SEG C_box format (cbox_format 2): per row, the candidate columns are every node of the
+// anchor boxes within +-R_a anchors of the row's own stored anchor on each axis (wrapped on
+// periodic axes, clamped to [0, N-1-p] on non-periodic ones) -- a superset of the K8 near set,
+// proven per row at build time.  Candidates are enumerated z-major, then y, then the x
+// subranges of each (z, y) anchor line; rows are box-sorted, so each line contributes one or two
+// CONTIGUOUS runs of columns [box_ptr(line + xa), box_ptr(line + xb + 1)).  A per-row bitmask over
+// the candidates marks the near pairs; their values are stored contiguously in candidate order.
+// No column indices are stored: K4 reads q along contiguous runs.
+constexpr int SEG_MAXSEG = 512;
+struct SegGeom {
+  int R[3];      // candidate reach in anchors per axis
+  int n[3];      // grid points per axis
+  int per[3];    // periodic flags
+  int lim[3];    // largest stored anchor per axis (N-1 periodic, N-1-p non-periodic)
+};
+// candidate anchor subranges of axis a for stored anchor s, in enumeration order: up to two
+// [lo, hi] pairs in r (returns their number, >= 1)
+__host__ __device__ __forceinline__ int seg_axis(const SegGeom& G, int a, int s, int* r) {
+  const int N = G.n[a], R = G.R[a];
+  if (G.per[a]) {
+    if (2 * R + 1 >= N) { r[0] = 0; r[1] = N - 1; return 1; }
+    const int lo = s - R, hi = s + R;
+    if (lo < 0) { r[0] = lo + N; r[1] = N - 1; r[2] = 0; r[3] = hi; return 2; }
+    if (hi >= N) { r[0] = lo; r[1] = N - 1; r[2] = 0; r[3] = hi - N; return 2; }
+    r[0] = lo; r[1] = hi; return 1;
+  }
+  r[0] = s - R < 0 ? 0 : s - R;
+  r[1] = s + R > G.lim[a] ? G.lim[a] : s + R;
+  return 1;
+}
+__host__ __device__ __forceinline__ int seg_len(const int* r, int nr) {
+  return (r[1] - r[0] + 1) + (nr == 2 ? r[3] - r[2] + 1 : 0);
+}
+// i-th anchor of the subranges r (i < seg_len)
+__host__ __device__ __forceinline__ int seg_at(const int* r, int i) {
+  const int l0 = r[1] - r[0] + 1;
+  return i < l0 ? r[0] + i : r[2] + (i - l0);
+}
+
 struct DeviceState {
   int device = -1;
   int64_t Np = 0;
@@ -37,7 +76,12 @@ struct DeviceState {
   float* c_val = nullptr;             // [chunks][4]
   int64_t cbox_nnz = 0;               // near pairs (entries without chunk padding)
   int64_t cbox_chunks = 0;             // C4x chunks or B4 blocks
-  int cbox_format = 0;                // 0: C4x, 1: B4 (aligned 4-column blocks, c_bidx + c_val)
+  int cbox_format = 0;                // 0: C4x, 1: B4 (aligned 4-column blocks, c_bidx + c_val), 2: SEG
+  SegGeom seg{};                      // SEG: candidate geometry
+  int seg_maxseg = 0;                 // SEG: largest number of column runs of a row
+  int64_t* seg_moff = nullptr;        // SEG: [N'+1] mask word offsets (c_ptr holds the value offsets)
+  uint32_t* seg_mask = nullptr;       // SEG: candidate bitmasks
+  int64_t seg_mask_words = 0;
   int* c_bidx = nullptr;              // B4 block index (column >> 2) per block
   int k4_group = 32;          // lanes per row in K4 (8/16/32 from the mean padded row length)
   // stencils
@@ -115,6 +159,7 @@ void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, d
 
 void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id);
 int64_t device_build_cbox(DeviceState& D, const HostSetup& S);
+void device_seg_decode(const DeviceState& D, int* d_col);
 
 void device_upload(DeviceState& D, const HostSetup& S);
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& P);

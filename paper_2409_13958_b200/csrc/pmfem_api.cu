@@ -384,7 +384,25 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
       cudaMemcpy(ptr.data(), D.c_ptr, sizeof(int64_t) * (S.Np + 1), cudaMemcpyDeviceToHost);
       const std::string tail = n.substr(12);
       const int64_t nch = ptr[S.Np];
-      if (tail == "rowptr") {
+      if (D.cbox_format == 2 && (tail == "rowptr" || tail == "col" || tail == "val")) {
+        // SEG: value offsets, the near columns decoded from the candidate bitmasks, the values
+        if (tail == "rowptr") put(ptr.data(), S.Np + 1, 8);
+        else {
+          *count = nch;
+          if (dst && nch) {
+            if (tail == "val") {
+              cudaMemcpy(dst, D.c_val, sizeof(float) * (size_t)nch, cudaMemcpyDeviceToHost);
+            } else {
+              int* d_col = nullptr;
+              if (cudaMalloc(&d_col, sizeof(int) * (size_t)nch) != cudaSuccess)
+                throw pmfem::Error(PMFEM_E_OOM, "cudaMalloc (SEG decode)");
+              pmfem::device_seg_decode(D, d_col);
+              cudaMemcpy(dst, d_col, sizeof(int) * (size_t)nch, cudaMemcpyDeviceToHost);
+              cudaFree(d_col);
+            }
+          }
+        }
+      } else if (tail == "rowptr") {
         for (auto& v : ptr) v *= 4;
         put(ptr.data(), S.Np + 1, 8);
       } else if (tail == "val") {
@@ -430,6 +448,18 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
         const auto& v = snd ? S.dist.send_idx[k] : S.dist.recv_idx[k];
         put(v.data(), (int64_t)v.size(), 4);
       } else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
+    }
+    else if (n == "spectrum_device") {
+      // the fp32 spectrum the device evaluation multiplies by ([P2][P1][H0], / #FFT points)
+      pmfem::require(!ctx->host_only && ctx->D.pgf_ready, PMFEM_E_STATE, "no device spectrum (build_pgf first)");
+      const int64_t cnt = (int64_t)ctx->D.H0 * ctx->D.P[1] * ctx->D.P[2];
+      *count = cnt;
+      if (dst) {
+        std::vector<float> f(cnt);
+        cudaMemcpy(f.data(), ctx->D.spec, sizeof(float) * cnt, cudaMemcpyDeviceToHost);
+        double* o = static_cast<double*>(dst);
+        for (int64_t i = 0; i < cnt; ++i) o[i] = f[i];
+      }
     }
     else if (n == "kernel") put(S.kernel.data(), (int64_t)S.kernel.size(), 8);
     else if (n == "spectrum") put(S.spectrum.data(), (int64_t)S.spectrum.size(), 8);

@@ -1,6 +1,17 @@
-// GPU integration of the Z0 element integrals: one thread per (row, element
-// image) task enumerated by setup_z0.cpp; the same ConeIntegrator (z0_cone.cuh) as the host
-// path, in fp64; contributions are accumulated with fp64 atomics into the row's value slots.
+// GPU integration of the Z0 element integrals: the (row, element image) tasks
+// enumerated by setup_z0.cpp, the same signed-cone quadrature (z0_cone.cuh: the same adaptive
+// face subdivision, the same collapsed Gauss rules) as the host path, in fp64; contributions are
+// accumulated with fp64 atomics into the row's value slots.
+//
+// k_z0_warp (default): ONE WARP PER TASK.  Lane 0 runs the adaptive subdivision of a face on a
+// shared-memory stack and emits leaf triangles into a shared-memory buffer; all 32 lanes then
+// share the leaves' quadrature points (flattened over the batch), each lane accumulating the 34
+// moments (A[4], B[10][3]) in registers; a butterfly reduction at the end of the task gives every
+// lane the totals and lanes scatter the 48 (k, m, axis) contributions.  No divergence inside
+// the point loop and no per-thread local-memory stack (the thread-per-task kernel k_z0_items,
+// PMFEM_Z0_THREAD=1, spilled its 24-triangle stack and diverged on the adaptive depth).
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -58,6 +69,184 @@ __global__ void k_z0_items(const Z0Item* __restrict__ items, int64_t nitems, con
   }
 }
 
+// ---- one warp per task
+constexpr int Z0W_WARPS = 4;           // warps per CTA
+constexpr int Z0W_LEAVES = 48;         // leaf buffer per warp (flushed when full)
+constexpr int Z0W_STACK = 24;          // subdivision stack per warp (as ConeIntegrator::face)
+
+struct Z0Leaf { double v[9]; double wf; int rule; };
+struct Z0Tri { double v[9]; int depth; };
+struct Z0Warp {
+  Z0Leaf leaf[Z0W_LEAVES];
+  Z0Tri stack[Z0W_STACK];
+  double g[4][3], c[4], a[4], o[3];
+  int start[Z0W_LEAVES + 1];
+};
+
+__global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
+    const Z0Item* __restrict__ items, int64_t nitems, const double* __restrict__ xyz, const int32_t* __restrict__ tets,
+    const int64_t* __restrict__ parent, const double* __restrict__ Ms_tet, Lat lat, const TriRules* __restrict__ rules,
+    const int64_t* __restrict__ rowbase, int64_t r0, double* __restrict__ vals) {
+  extern __shared__ __align__(16) unsigned char z0w_smem[];
+  TriRules& R = *reinterpret_cast<TriRules*>(z0w_smem);
+  Z0Warp* W = reinterpret_cast<Z0Warp*>(z0w_smem + ((sizeof(TriRules) + 15) / 16) * 16);
+  for (int i = threadIdx.x; i < (int)(sizeof(TriRules) / sizeof(double)); i += blockDim.x)
+    reinterpret_cast<double*>(&R)[i] = reinterpret_cast<const double*>(rules)[i];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Z0Warp& w = W[wid];
+  for (int64_t it_i = (int64_t)blockIdx.x * Z0W_WARPS + wid; it_i < nitems; it_i += (int64_t)gridDim.x * Z0W_WARPS) {
+    const Z0Item it = items[it_i];
+    int code = it.code;
+    int sh[3];
+    sh[2] = code % 17 - 8; code /= 17;
+    sh[1] = code % 17 - 8; code /= 17;
+    sh[0] = code - 8;
+    const int32_t* tv = tets + 4 * (int64_t)it.tet;
+    double P[4][3];
+    for (int j = 0; j < 4; ++j)
+      for (int x = 0; x < 3; ++x) P[j][x] = xyz[3 * (int64_t)tv[j] + x] + sh[x] * lat.L[x];
+    const int64_t pn = parent[it.row];
+    if (lane == 0) {
+      double g[4][3];
+      tet_grads(P, g);
+      for (int i = 0; i < 4; ++i) {
+        for (int x = 0; x < 3; ++x) w.g[i][x] = g[i][x];
+        w.c[i] = 1.0 - zc_dot(g[i], P[i]);
+      }
+      for (int x = 0; x < 3; ++x) w.o[x] = xyz[3 * pn + x];
+      for (int i = 0; i < 4; ++i)
+        w.a[i] = (it.va >= 0) ? (i == it.va ? 1.0 : 0.0) : w.c[i] + zc_dot(w.g[i], w.o);
+    }
+    __syncwarp();
+    double A[4] = {0, 0, 0, 0}, B[10][3];
+    for (int i = 0; i < 10; ++i) B[i][0] = B[i][1] = B[i][2] = 0.0;
+    for (int j = 0; j < 4; ++j) {
+      if (it.va >= 0 && j != it.va) continue;                 // warp-uniform
+      const double gn = sqrt(zc_dot(w.g[j], w.g[j]));
+      const double h = w.a[j] / gn;                            // phi_j(o) = |g_j| h_j
+      if (fabs(h) * gn < 1e-14) continue;
+      int top = 0;
+      if (lane == 0) {
+        const int f[3] = {(j + 1) % 4, (j + 2) % 4, (j + 3) % 4};
+        for (int k = 0; k < 3; ++k)
+          for (int x = 0; x < 3; ++x) w.stack[0].v[3 * k + x] = P[f[k]][x];
+        w.stack[0].depth = 0;
+        top = 1;
+      }
+      while (true) {
+        int nleaf = 0;
+        if (lane == 0) {          // adaptive subdivision (ConeIntegrator::face) until empty or full
+          while (top > 0 && nleaf < Z0W_LEAVES) {
+            const Z0Tri T = w.stack[--top];
+            const double* V0 = T.v;
+            const double* V1 = T.v + 3;
+            const double* V2 = T.v + 6;
+            double cen[3], e01[3], e02[3], e12[3];
+            for (int x = 0; x < 3; ++x) {
+              cen[x] = (V0[x] + V1[x] + V2[x]) / 3.0;
+              e01[x] = V1[x] - V0[x]; e02[x] = V2[x] - V0[x]; e12[x] = V2[x] - V1[x];
+            }
+            const double size = sqrt(fmax(zc_dot(e01, e01), fmax(zc_dot(e02, e02), zc_dot(e12, e12))));
+            double rc = 0;
+            for (int k = 0; k < 3; ++k) {
+              const double d[3] = {T.v[3 * k] - cen[0], T.v[3 * k + 1] - cen[1], T.v[3 * k + 2] - cen[2]};
+              rc = fmax(rc, sqrt(zc_dot(d, d)));
+            }
+            const double dc[3] = {cen[0] - w.o[0], cen[1] - w.o[1], cen[2] - w.o[2]};
+            const double dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
+            if (size > dest && T.depth < 7 && top + 4 <= Z0W_STACK) {
+              double m01[3], m02[3], m12[3];
+              for (int x = 0; x < 3; ++x) {
+                m01[x] = 0.5 * (V0[x] + V1[x]); m02[x] = 0.5 * (V0[x] + V2[x]); m12[x] = 0.5 * (V1[x] + V2[x]);
+              }
+              const double* kids[4][3] = {{V0, m01, m02}, {m01, V1, m12}, {m02, m12, V2}, {m12, m02, m01}};
+              for (int c4 = 0; c4 < 4; ++c4) {
+                Z0Tri& N = w.stack[top++];
+                for (int k = 0; k < 3; ++k)
+                  for (int x = 0; x < 3; ++x) N.v[3 * k + x] = kids[c4][k][x];
+                N.depth = T.depth + 1;
+              }
+              continue;
+            }
+            // leaf: the rule by size / distance (ConeIntegrator::quad), weight area2 * h
+            const double cr[3] = {e01[1] * e02[2] - e01[2] * e02[1], e01[2] * e02[0] - e01[0] * e02[2],
+                                  e01[0] * e02[1] - e01[1] * e02[0]};
+            const double ratio = size / dest;
+            Z0Leaf& L = w.leaf[nleaf];
+            for (int k = 0; k < 9; ++k) L.v[k] = T.v[k];
+            L.wf = sqrt(zc_dot(cr, cr)) * h;
+            L.rule = ratio <= 0.3 ? 0 : (ratio <= 0.6 ? 1 : 2);
+            w.start[nleaf + 1] = 0;
+            ++nleaf;
+          }
+          int acc = 0;
+          for (int l = 0; l < nleaf; ++l) { w.start[l] = acc; acc += R.cnt[w.leaf[l].rule]; }
+          w.start[nleaf] = acc;
+        }
+        __syncwarp();
+        nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
+        const int more = __shfl_sync(0xffffffffu, top, 0);
+        const int npts = w.start[nleaf];
+        int l = 0;
+        for (int gq = lane; gq < npts; gq += 32) {
+          while (gq >= w.start[l + 1]) ++l;
+          const Z0Leaf& L = w.leaf[l];
+          const int q = R.off[L.rule] + (gq - w.start[l]);
+          double y[3], Rv[3];
+          for (int x = 0; x < 3; ++x) {
+            y[x] = R.l0[q] * L.v[x] + R.l1[q] * L.v[3 + x] + R.l2[q] * L.v[6 + x];
+            Rv[x] = y[x] - w.o[x];
+          }
+          const double inv = rsqrt(zc_dot(Rv, Rv));
+          const double inv3 = inv * inv * inv;
+          const double wt = R.w[q] * L.wf;
+          double ak[4], bk[4];
+          for (int i = 0; i < 4; ++i) {
+            ak[i] = w.a[i];
+            const double py = w.c[i] + zc_dot(w.g[i], y);
+            bk[i] = py - ak[i];
+            A[i] += wt * (ak[i] / 6.0 + py / 3.0) * inv;
+          }
+          int pi = 0;
+          for (int k = 0; k < 4; ++k)
+            for (int m = k; m < 4; ++m, ++pi) {
+              const double sv = -wt * (ak[k] * ak[m] + 0.5 * (ak[k] * bk[m] + ak[m] * bk[k]) + bk[k] * bk[m] / 3.0) * inv3;
+              B[pi][0] += sv * Rv[0]; B[pi][1] += sv * Rv[1]; B[pi][2] += sv * Rv[2];
+            }
+        }
+        __syncwarp();
+        if (!more) break;
+        top = more;
+      }
+    }
+    // butterfly: every lane gets the task totals
+    for (int o = 16; o > 0; o >>= 1) {
+      for (int i = 0; i < 4; ++i) A[i] += __shfl_xor_sync(0xffffffffu, A[i], o);
+      for (int i = 0; i < 10; ++i)
+        for (int x = 0; x < 3; ++x) B[i][x] += __shfl_xor_sync(0xffffffffu, B[i][x], o);
+    }
+    const double Ms = Ms_tet[it.tet];
+    double* v = vals + rowbase[it.row - r0];
+    for (int t = lane; t < 48; t += 32) {
+      const int k = t / 12, m = (t / 3) % 4, x = t % 3;
+      if (!(it.flags & (1u << k))) continue;
+      const int lo = k < m ? k : m, hi = k < m ? m : k;
+      const int pi = lo * 4 - lo * (lo - 1) / 2 + (hi - lo);
+      // select B[pi][x] without dynamic register indexing
+      double bv = 0.0;
+      for (int i = 0; i < 10; ++i)
+        for (int y = 0; y < 3; ++y)
+          if (i == pi && y == x) bv = B[i][y];
+      double av = 0.0;
+      for (int i = 0; i < 4; ++i)
+        if (i == m) av = A[i];
+      atomicAdd(v + 3 * it.pos[m] + x, Ms * (bv + w.g[k][x] * av));
+    }
+    __syncwarp();
+  }
+}
+
 }  // namespace
 
 void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& titems,
@@ -84,9 +273,22 @@ void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& t
   CKZ(cudaMemset(d_vals, 0, std::max<int64_t>(nvals, 1) * sizeof(double)));
   Lat lat{{S.L[0], S.L[1], S.L[2]}};
   const int64_t n = (int64_t)items.size();
-  if (n) {
+  static const bool thread_per_task = std::getenv("PMFEM_Z0_THREAD") != nullptr;
+  if (n && thread_per_task) {
     k_z0_items<<<(unsigned)((n + 127) / 128), 128>>>(d_items, n, d_xyz, d_tets, d_parent, d_ms, lat, d_rules, d_base,
                                                      r0, d_vals);
+    CKZ(cudaGetLastError());
+    CKZ(cudaDeviceSynchronize());
+  } else if (n) {
+    const size_t smem = ((sizeof(TriRules) + 15) / 16) * 16 + Z0W_WARPS * sizeof(Z0Warp);
+    CKZ(cudaFuncSetAttribute(k_z0_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int dev = 0, nsm = 148;
+    CKZ(cudaGetDevice(&dev));
+    CKZ(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    const int64_t want = (n + Z0W_WARPS - 1) / Z0W_WARPS;
+    const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)nsm * 32);
+    k_z0_warp<<<blocks, 32 * Z0W_WARPS, smem>>>(d_items, n, d_xyz, d_tets, d_parent, d_ms, lat, d_rules, d_base, r0,
+                                                d_vals);
     CKZ(cudaGetLastError());
     CKZ(cudaDeviceSynchronize());
   }

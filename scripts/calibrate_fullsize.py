@@ -45,7 +45,7 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--coarsen", type=float, default=1.0)
     ap.add_argument("--samples", type=int, default=12)
-    ap.add_argument("--settings", default="1,3;1,4;2,3;2,4;3,3;3,4")
+    ap.add_argument("--settings", default="2,3;2,4;3,3;3,4")
     ap.add_argument("--ring", type=int, default=1)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -78,13 +78,14 @@ def main():
                          np.sin(th) * np.sin(k * xw[:, ax])], axis=1)
     fields = {"random": m_random(pm.n_parents, seed=77), "smooth": m_smooth}
     # brute force at the rows (C pair sums) -> H at the samples
-    ref = {}
+    ref, hex_ = {}, {}
     t0 = time.time()
     for name, m in fields.items():
         q = om.charges(m)
         u = np.zeros(pm.n_parents)
         u[rows] = bf.potential(xw[rows], xw, q, om.spec) + bf.pgf_self(om.spec) * q[rows] + om.u_loc(m)[rows]
-        ref[name] = (fem.gradient_field(ops, u) + om.exchange(m))[samples]
+        ref[name] = fem.gradient_field(ops, u)[samples]
+        hex_[name] = om.exchange(m)[samples]
     t_bf = time.time() - t0
     print("brute force: %.1f s" % t_bf, flush=True)
     grid = aim.Grid(cfg["grid"], om.periodic, om.lattice, xw)
@@ -105,18 +106,20 @@ def main():
         rec = {"p": p, "s": s, "nnz_cbox_per_row": float(om.C.nnz / rows.size)}
         for name, m in fields.items():
             u = om.potential_aim(m)
-            H = (fem.gradient_field(ops, u) + om.exchange(m))[samples]
+            H = fem.gradient_field(ops, u)[samples]
             Hb = ref[name]
-            rec["rel_l2_%s" % name] = float(np.linalg.norm(H - Hb) / np.linalg.norm(Hb))
-            rec["max_node_rel_%s" % name] = float(np.max(np.linalg.norm(H - Hb, axis=1) /
-                                                       np.mean(np.linalg.norm(Hb, axis=1))))
+            dn = np.linalg.norm(H - Hb, axis=1)
+            # H_ms (the field the AIM approximates) and H_eff = H_ms + H_ex (exact exchange)
+            rec["rel_l2_Hms_%s" % name] = float(np.linalg.norm(H - Hb) / np.linalg.norm(Hb))
+            rec["max_node_rel_Hms_%s" % name] = float(np.max(dn) / np.mean(np.linalg.norm(Hb, axis=1)))
+            rec["rel_l2_Heff_%s" % name] = float(np.linalg.norm(H - Hb) / np.linalg.norm(Hb + hex_[name]))
         rec["seconds"] = time.time() - t0
         print(json.dumps(rec), flush=True)
         results.append(rec)
     out = {"config": a.config, "coarsen": a.coarsen, "n_parents": int(pm.n_parents), "grid": list(cfg["grid"]),
            "z0_ring": a.ring, "samples": int(samples.size), "rows": int(rows.size),
-           "metric": "relative L2 of H_eff (H_ms + H_ex) over the samples, oracle AIM vs oracle brute force; "
-                     "max_node_rel = max_n |dH_n| / mean_n |H_n|",
+           "metric": "relative L2 over the samples of H_ms (and of H_eff = H_ms + H_ex, exchange exact), "
+                     "oracle AIM vs oracle brute force; max_node_rel = max_n |dH_n| / mean_n |H_ms,n|",
            "oracle_setup_s": t_setup, "bruteforce_s": t_bf, "results": results}
     print(json.dumps(out))
     if a.out:

@@ -22,6 +22,9 @@ CONFIGS = {
     # non-periodic mode: not a BASELINE.json workload
     "N1": "non-periodic isolated cube, ~1k nodes, 16^3 AIM grid (32^3 FFT)",
     "N2": "non-periodic isolated sphere, ~30k nodes, 32^3 AIM grid (64^3 FFT)",
+    # other periodic axes (parity coverage, not BASELINE workloads)
+    "R1": "1D-periodic rod along z (PAPER.md:277: R = 20 nm, cell height 2R, touching), 16x16x16 AIM grid",
+    "Y1": "1D-periodic strip along y with a slot (touching), 8x64x4 AIM grid",
 }
 
 
@@ -32,7 +35,7 @@ def _round_cells(length, h):
 def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
     """Return dict(mesh, periodic, L, grid, Ms, Aex, name, desc)."""
     if seed is None:
-        seed = (1000 if name[0] == "C" else 2000) + int(name[1:])
+        seed = {"C": 1000, "N": 2000, "R": 3000, "Y": 4000}[name[0]] + int(name[1:])
     c = float(coarsen)
     if name == "C1":
         L = 100 * NM
@@ -115,6 +118,37 @@ def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
                                jitter=jitter, seed=seed, name=name)
         periodic = (0, 0, 0); lattice = (0.0, 0.0, 0.0)
         g = grid or (max(8, int(32 // c)),) * 3
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "R1":
+        # infinitely long cylindrical rod, unit cell height 2R, T-NP-PBC along z;
+        # A = 9.604e-7 erg/cm, Ms = 490 emu/cm^3
+        R = 20 * NM; Lz = 2 * R; h = 2.5 * NM * c
+        n = int(math.ceil(R / h))
+        nz = _round_cells(Lz, h); h_z = Lz / nz
+        h = h_z
+        n = int(math.ceil(R / h))
+        cc = (np.arange(-n, n) + 0.5) * h
+        X, Y = np.meshgrid(cc, cc, indexing="ij")
+        disk = X ** 2 + Y ** 2 <= R * R
+        mask = np.repeat(disk[:, :, None], nz, axis=2)
+        mesh = kuhn_voxel_mesh(mask, h, origin=(-n * h, -n * h, 0.0), wrap=(False, False, True),
+                               jitter=jitter, seed=seed, name=name)
+        periodic = (0, 0, 1); lattice = (0.0, 0.0, Lz)
+        g = grid or (max(8, int(16 // c)),) * 3
+        Ms, Aex = 490.0, 9.604e-7
+    elif name == "Y1":
+        # strip along y (touching), 100 nm period, 40 nm wide, 6 nm thick, a 20 nm slot
+        Ly = 100 * NM; h = 2 * NM * c
+        ny = _round_cells(Ly, h); h = Ly / ny
+        nx = _round_cells(40 * NM, h); nz = max(1, _round_cells(6 * NM, h))
+        xc = (np.arange(nx) + 0.5) * h
+        yc = (np.arange(ny) + 0.5) * h
+        X, Y = np.meshgrid(xc, yc, indexing="ij")
+        keep = ~((np.abs(X - 20 * NM) < 8 * NM) & (np.abs(Y - 50 * NM) < 10 * NM))
+        mask = np.repeat(keep[:, :, None], nz, axis=2)
+        mesh = kuhn_voxel_mesh(mask, h, wrap=(False, True, False), jitter=jitter, seed=seed, name=name)
+        periodic = (0, 1, 0); lattice = (0.0, Ly, 0.0)
+        g = grid or (max(4, int(8 // c)), max(16, int(64 // c)), 4)
         Ms, Aex = 637.0, 1.4e-6
     else:
         raise KeyError(name)

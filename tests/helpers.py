@@ -1,4 +1,6 @@
 """Test helpers: build the oracle and the library context on the same seeded inputs."""
+import functools
+
 import numpy as np
 
 from oracle.heff import OracleModel
@@ -15,6 +17,9 @@ SMALL = {
     "C5p2": dict(cfg=("C5", 16), grid=(128, 8, 4), order=2, s=2.0, ring=0),
     # non-periodic mode (NEXT-3): isolated cube, free-space kernel, 2N padding on every axis
     "N1p2": dict(cfg=("N1", 2), grid=(16, 16, 16), order=2, s=2.0, ring=1),
+    # other periodic axes: the z-periodic rod of P:277 and a y-periodic strip
+    "R1p2": dict(cfg=("R1", 2), grid=(8, 8, 16), order=2, s=1.5, ring=1),
+    "Y1p2": dict(cfg=("Y1", 2), grid=(8, 32, 4), order=2, s=2.0, ring=0),
 }
 
 
@@ -25,7 +30,9 @@ def config(key):
     return cfg, spec
 
 
+@functools.lru_cache(maxsize=None)
 def oracle_model(key):
+    """The oracle for a SMALL config (cached: the model is read-only for the tests)."""
     cfg, spec = config(key)
     m = cfg["mesh"]
     return OracleModel(m.xyz, m.tets, cfg["periodic"], cfg["lattice"], spec["grid"], Ms=cfg["Ms"],
@@ -53,3 +60,10 @@ def dense(ctx, prefix, nv, n):
 
 def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def max_node_rel(a, b):
+    """Per-node bound: max_n |a_n - b_n| / rms_n |b_n| (rows = nodes)."""
+    a = np.asarray(a).reshape(len(a), -1)
+    b = np.asarray(b).reshape(len(b), -1)
+    return float(np.max(np.linalg.norm(a - b, axis=1)) / np.sqrt(np.mean(np.sum(b * b, axis=1))))
