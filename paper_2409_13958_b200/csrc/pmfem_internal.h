@@ -109,6 +109,8 @@ void setup_aim(HostSetup& S, const pmfem_grid* g);
 void setup_order(HostSetup& S);
 void setup_dist(HostSetup& S, int rank, int world);
 struct TriRules;
+void z0_device_begin(const HostSetup& S, const TriRules& rules);
+void z0_device_end(std::vector<std::vector<double>>& rval);
 void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& items,
                          const std::vector<std::vector<int32_t>>& rcol, std::vector<std::vector<double>>& rval,
                          const TriRules& rules, int64_t r0, int64_t r1);

@@ -24,11 +24,18 @@
 namespace pmfem {
 
 void build_tri_rules(TriRules& R) {
+  // subdivision / rule-selection parameters (PMFEM_Z0_SPLIT, PMFEM_Z0_THR0/1/2 for
+  // accuracy-vs-cost studies; defaults measured against the oracle in DESIGN.md)
+  auto envd = [](const char* k, double d) { return std::getenv(k) ? std::atof(std::getenv(k)) : d; };
+  R.split = envd("PMFEM_Z0_SPLIT", 1.0);
+  R.thr0 = envd("PMFEM_Z0_THR0", 0.3);
+  R.thr1 = envd("PMFEM_Z0_THR1", 0.6);
+  R.thr2 = envd("PMFEM_Z0_THR2", 1e30);
   int off = 0;
-  const int ns[3] = {4, 6, 8};
-  for (int r = 0; r < 3; ++r) {
+  const int ns[4] = {4, 6, 8, 12};
+  for (int r = 0; r < 4; ++r) {
     const int n = ns[r];
-    double x[8], w[8];
+    double x[12], w[12];
     gauss_legendre01(n, x, w);
     R.off[r] = off;
     R.cnt[r] = n * n;
@@ -66,20 +73,26 @@ void setup_z0(HostSetup& S) {
   const int64_t Np = S.Np;
   const int NC = 17 * 17 * 17;
   static TriRules rules;
-  static bool rules_ready = false;
-  if (!rules_ready) { build_tri_rules(rules); rules_ready = true; }
+  build_tri_rules(rules);
   std::vector<std::vector<int32_t>> rcol(Np);
   std::vector<std::vector<double>> rval(Np);
   S.rowsumZ.assign(3 * Np, 0.0);
   const bool on_device = S.z0_device >= 0;
-  const int64_t chunk = on_device ? 400000 : Np;
+  const int64_t chunk = on_device ? 250000 : Np;
   std::string err;
   const bool verbose = std::getenv("PMFEM_VERBOSE") != nullptr;
+  if (on_device) z0_device_begin(S, rules);
+  // on an exception the device pipeline is released (z0_device_end) before it propagates
+  struct PipeGuard {
+    bool on; std::vector<std::vector<double>>* rv;
+    ~PipeGuard() { if (on) { try { z0_device_end(*rv); } catch (...) {} } }
+  } guard_pipe{on_device, &rval};
   for (int64_t c0 = 0; c0 < Np && err.empty(); c0 += chunk) {
     const double t_chunk = omp_get_wtime();
     const int64_t c1 = std::min(Np, c0 + chunk);
+    long long host_pts = 0;
     std::vector<std::vector<Z0Item>> titems(omp_get_max_threads());
-#pragma omp parallel
+#pragma omp parallel reduction(+ : host_pts)
     {
       ConeIntegrator I;
       I.R = &rules;
@@ -220,13 +233,15 @@ void setup_z0(HostSetup& S) {
           err = e.what();
         }
       }
+      host_pts += I.npts;
     }
     const double t_enum = omp_get_wtime();
     if (on_device && err.empty()) z0_device_integrate(S, titems, rcol, rval, rules, c0, c1);
     if (verbose)
-      std::fprintf(stderr, "[pmfem]   z0 rows %lld-%lld: enumerate %.2f s, integrate %.2f s\n", (long long)c0,
-                   (long long)c1, t_enum - t_chunk, omp_get_wtime() - t_enum);
+      std::fprintf(stderr, "[pmfem]   z0 rows %lld-%lld: enumerate %.2f s, integrate %.2f s (host quadrature points %lld)\n",
+                   (long long)c0, (long long)c1, t_enum - t_chunk, omp_get_wtime() - t_enum, host_pts);
   }
+  if (on_device) { guard_pipe.on = false; z0_device_end(rval); }   // the last chunks' values
   require(err.empty(), PMFEM_E_MESH, err);
   // split diagonal (kept only in the row sum) from the off-diagonal entries
 #pragma omp parallel for schedule(dynamic, 1024)

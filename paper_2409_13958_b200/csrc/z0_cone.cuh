@@ -22,10 +22,16 @@
 
 namespace pmfem {
 
-struct TriRules {              // collapsed n x n Gauss on the reference triangle, n = 4, 6, 8
-  double l0[116], l1[116], l2[116], w[116];
-  int off[3], cnt[3];
+struct TriRules {              // collapsed n x n Gauss on the reference triangle, n = 4, 6, 8, 12
+  double l0[260], l1[260], l2[260], w[260];
+  double split;                // a face piece is subdivided while size > split * distance bound
+  double thr0, thr1, thr2;     // rule by size / distance: <= thr0 -> 4x4, <= thr1 -> 6x6,
+                               // <= thr2 -> 8x8, else 12x12
+  int off[4], cnt[4];
 };
+ZC_HD inline int tri_rule(const TriRules& R, double ratio) {
+  return ratio <= R.thr0 ? 0 : (ratio <= R.thr1 ? 1 : (ratio <= R.thr2 ? 2 : 3));
+}
 
 // host: fill the three rules (Gauss-Legendre nodes on [0,1] by Newton iteration)
 void build_tri_rules(TriRules& R);
@@ -37,6 +43,7 @@ struct ConeIntegrator {
   double o[3], a[4];
   double A[4], B[4][4][3];
   const TriRules* R;
+  long long npts = 0;                // quadrature points evaluated (cost diagnostics)
 
   ZC_HD double phi(int i, const double* r) const { return c[i] + zc_dot(g[i], r); }
 
@@ -47,7 +54,8 @@ struct ConeIntegrator {
                           e01[0] * e02[1] - e01[1] * e02[0]};
     const double area2 = sqrt(zc_dot(cr, cr));
     const double ratio = size / dest;
-    const int r = ratio <= 0.3 ? 0 : (ratio <= 0.6 ? 1 : 2);
+    const int r = tri_rule(*R, ratio);
+    npts += R->cnt[r];
     for (int q = R->off[r]; q < R->off[r] + R->cnt[r]; ++q) {
       double y[3];
       for (int x = 0; x < 3; ++x) y[x] = R->l0[q] * V0[x] + R->l1[q] * V1[x] + R->l2[q] * V2[x];
@@ -92,7 +100,7 @@ struct ConeIntegrator {
       }
       const double dc[3] = {cen[0] - o[0], cen[1] - o[1], cen[2] - o[2]};
       const double dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
-      if (size > dest && T.depth < 7 && top + 4 <= 24) {
+      if (size > R->split * dest && T.depth < 7 && top + 4 <= 24) {
         double m01[3], m02[3], m12[3];
         for (int x = 0; x < 3; ++x) {
           m01[x] = 0.5 * (V0[x] + V1[x]); m02[x] = 0.5 * (V0[x] + V2[x]); m12[x] = 0.5 * (V1[x] + V2[x]);

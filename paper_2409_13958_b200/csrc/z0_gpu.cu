@@ -119,8 +119,12 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
         w.a[i] = (it.va >= 0) ? (i == it.va ? 1.0 : 0.0) : w.c[i] + zc_dot(w.g[i], w.o);
     }
     __syncwarp();
-    double A[4] = {0, 0, 0, 0}, B[10][3];
-    for (int i = 0; i < 10; ++i) B[i][0] = B[i][1] = B[i][2] = 0.0;
+    // 23 face moments summed over the task's faces (the per-task coefficients a, g are common to
+    // all of them): S0 = sum w/R, S1 = sum w Rv/R, T1 = sum w Rv/R^3, T2 = sum w Rv Rv/R^3 (6),
+    // T3 = sum w Rv Rv Rv/R^3 (10), Rv = y - o, w = rule weight * area2 * h
+    double Mo[23];
+#pragma unroll
+    for (int i = 0; i < 23; ++i) Mo[i] = 0.0;
     for (int j = 0; j < 4; ++j) {
       if (it.va >= 0 && j != it.va) continue;                 // warp-uniform
       const double gn = sqrt(zc_dot(w.g[j], w.g[j]));
@@ -155,7 +159,7 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
             }
             const double dc[3] = {cen[0] - w.o[0], cen[1] - w.o[1], cen[2] - w.o[2]};
             const double dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
-            if (size > dest && T.depth < 7 && top + 4 <= Z0W_STACK) {
+            if (size > R.split * dest && T.depth < 7 && top + 4 <= Z0W_STACK) {
               double m01[3], m02[3], m12[3];
               for (int x = 0; x < 3; ++x) {
                 m01[x] = 0.5 * (V0[x] + V1[x]); m02[x] = 0.5 * (V0[x] + V2[x]); m12[x] = 0.5 * (V1[x] + V2[x]);
@@ -176,7 +180,7 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
             Z0Leaf& L = w.leaf[nleaf];
             for (int k = 0; k < 9; ++k) L.v[k] = T.v[k];
             L.wf = sqrt(zc_dot(cr, cr)) * h;
-            L.rule = ratio <= 0.3 ? 0 : (ratio <= 0.6 ? 1 : 2);
+            L.rule = tri_rule(R, ratio);
             w.start[nleaf + 1] = 0;
             ++nleaf;
           }
@@ -199,49 +203,64 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
             Rv[x] = y[x] - w.o[x];
           }
           const double inv = rsqrt(zc_dot(Rv, Rv));
-          const double inv3 = inv * inv * inv;
           const double wt = R.w[q] * L.wf;
-          double ak[4], bk[4];
-          for (int i = 0; i < 4; ++i) {
-            ak[i] = w.a[i];
-            const double py = w.c[i] + zc_dot(w.g[i], y);
-            bk[i] = py - ak[i];
-            A[i] += wt * (ak[i] / 6.0 + py / 3.0) * inv;
-          }
-          int pi = 0;
-          for (int k = 0; k < 4; ++k)
-            for (int m = k; m < 4; ++m, ++pi) {
-              const double sv = -wt * (ak[k] * ak[m] + 0.5 * (ak[k] * bk[m] + ak[m] * bk[k]) + bk[k] * bk[m] / 3.0) * inv3;
-              B[pi][0] += sv * Rv[0]; B[pi][1] += sv * Rv[1]; B[pi][2] += sv * Rv[2];
-            }
+          const double wi = wt * inv, w3 = wi * inv * inv;
+          const double x = Rv[0], yy = Rv[1], z = Rv[2];
+          Mo[0] += wi;
+          Mo[1] += wi * x; Mo[2] += wi * yy; Mo[3] += wi * z;
+          Mo[4] += w3 * x; Mo[5] += w3 * yy; Mo[6] += w3 * z;
+          const double xx = w3 * x * x, xy = w3 * x * yy, xz = w3 * x * z, yv = w3 * yy * yy, yz = w3 * yy * z,
+                       zz = w3 * z * z;
+          Mo[7] += xx; Mo[8] += xy; Mo[9] += xz; Mo[10] += yv; Mo[11] += yz; Mo[12] += zz;
+          Mo[13] += xx * x; Mo[14] += xx * yy; Mo[15] += xx * z; Mo[16] += xy * yy; Mo[17] += xy * z;
+          Mo[18] += xz * z; Mo[19] += yv * yy; Mo[20] += yv * z; Mo[21] += yz * z; Mo[22] += zz * z;
         }
         __syncwarp();
         if (!more) break;
         top = more;
       }
     }
-    // butterfly: every lane gets the task totals
-    for (int o = 16; o > 0; o >>= 1) {
-      for (int i = 0; i < 4; ++i) A[i] += __shfl_xor_sync(0xffffffffu, A[i], o);
-      for (int i = 0; i < 10; ++i)
-        for (int x = 0; x < 3; ++x) B[i][x] += __shfl_xor_sync(0xffffffffu, B[i][x], o);
-    }
+    // butterfly: every lane gets the task's moments
+#pragma unroll
+    for (int i = 0; i < 23; ++i)
+      for (int o = 16; o > 0; o >>= 1) Mo[i] += __shfl_xor_sync(0xffffffffu, Mo[i], o);
+    // A_m = a_m S0 / 2 + g_m . S1 / 3;
+    // B_km,x = -(a_k a_m T1_x + (a_k g_m + a_m g_k) . T2_(.x) / 2 + g_k^T T3_(..x) g_m / 3)
+    // (the per-point formulas of ConeIntegrator::quad with phi(y) = a + g . (y - o), regrouped)
     const double Ms = Ms_tet[it.tet];
     double* v = vals + rowbase[it.row - r0];
     for (int t = lane; t < 48; t += 32) {
       const int k = t / 12, m = (t / 3) % 4, x = t % 3;
       if (!(it.flags & (1u << k))) continue;
-      const int lo = k < m ? k : m, hi = k < m ? m : k;
-      const int pi = lo * 4 - lo * (lo - 1) / 2 + (hi - lo);
-      // select B[pi][x] without dynamic register indexing
-      double bv = 0.0;
-      for (int i = 0; i < 10; ++i)
-        for (int y = 0; y < 3; ++y)
-          if (i == pi && y == x) bv = B[i][y];
-      double av = 0.0;
-      for (int i = 0; i < 4; ++i)
-        if (i == m) av = A[i];
-      atomicAdd(v + 3 * it.pos[m] + x, Ms * (bv + w.g[k][x] * av));
+      const double* gk = w.g[k];
+      const double* gm = w.g[m];
+      const double ak = w.a[k], am = w.a[m];
+      const double Am = 0.5 * am * Mo[0] + (gm[0] * Mo[1] + gm[1] * Mo[2] + gm[2] * Mo[3]) / 3.0;
+      // T2 column x, T3 slice x as 3x3 (symmetric index maps)
+      double t2[3], t3[3][3];
+      const int i2[3][3] = {{7, 8, 9}, {8, 10, 11}, {9, 11, 12}};
+      const int i3[3][3][3] = {{{13, 14, 15}, {14, 16, 17}, {15, 17, 18}},
+                               {{14, 16, 17}, {16, 19, 20}, {17, 20, 21}},
+                               {{15, 17, 18}, {17, 20, 21}, {18, 21, 22}}};
+      double bv = ak * am * (x == 0 ? Mo[4] : x == 1 ? Mo[5] : Mo[6]);
+      for (int i = 0; i < 3; ++i) {
+        double c2 = 0.0;
+        for (int j = 0; j < 23; ++j)
+          if (j == i2[i][x]) c2 = Mo[j];
+        t2[i] = c2;
+        for (int l = 0; l < 3; ++l) {
+          double c3 = 0.0;
+          for (int j = 0; j < 23; ++j)
+            if (j == i3[i][l][x]) c3 = Mo[j];
+          t3[i][l] = c3;
+        }
+      }
+      for (int i = 0; i < 3; ++i) bv += 0.5 * (ak * gm[i] + am * gk[i]) * t2[i];
+      double q3 = 0.0;
+      for (int i = 0; i < 3; ++i)
+        for (int l = 0; l < 3; ++l) q3 += gk[i] * gm[l] * t3[i][l];
+      bv = -(bv + q3 / 3.0);
+      atomicAdd(v + 3 * it.pos[m] + x, Ms * (bv + gk[x] * Am));
     }
     __syncwarp();
   }
@@ -249,58 +268,124 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
 
 }  // namespace
 
+// Chunked, pipelined driver: the mesh arrays are uploaded once (z0_device_begin); each chunk's
+// tasks are uploaded and integrated asynchronously on a private stream and its values copied
+// back into pinned memory, while the host enumerates the next chunk; a chunk's values are
+// accumulated into rval when the NEXT chunk has been launched (or at z0_device_end).
+struct Z0Pipe {
+  int dev = -1;
+  cudaStream_t st = nullptr;
+  double* xyz = nullptr;
+  int32_t* tets = nullptr;
+  int64_t* parent = nullptr;
+  double* ms = nullptr;
+  TriRules* rules = nullptr;
+  struct Chunk {
+    bool busy = false;
+    int64_t r0 = 0, r1 = 0;
+    std::vector<int64_t> rowbase;
+    Z0Item* items = nullptr;
+    int64_t* base = nullptr;
+    double* vals = nullptr;
+    double* hvals = nullptr;       // pinned
+    size_t hcap = 0;
+    cudaEvent_t done = nullptr;
+  } ch[2];
+  int cur = 0;
+};
+
+static Z0Pipe g_z0;
+
+void z0_device_begin(const HostSetup& S, const TriRules& rules) {
+  Z0Pipe& P = g_z0;
+  P.dev = S.z0_device;
+  CKZ(cudaSetDevice(P.dev));
+  CKZ(cudaStreamCreateWithFlags(&P.st, cudaStreamNonBlocking));
+  P.xyz = up(S.xyz.data(), S.xyz.size());
+  P.tets = up(S.tets.data(), S.tets.size());
+  P.parent = up(S.parent.data(), S.parent.size());
+  P.ms = up(S.Ms_tet.data(), S.Ms_tet.size());
+  P.rules = up(&rules, 1);
+  for (auto& c : P.ch) CKZ(cudaEventCreateWithFlags(&c.done, cudaEventDisableTiming));
+  P.cur = 0;
+}
+
+static void z0_finish_chunk(Z0Pipe::Chunk& c, std::vector<std::vector<double>>& rval) {
+  if (!c.busy) return;
+  CKZ(cudaEventSynchronize(c.done));
+  for (int64_t r = c.r0; r < c.r1; ++r) {
+    const double* src = c.hvals + c.rowbase[r - c.r0];
+    std::vector<double>& dst = rval[r];
+    for (size_t j = 0; j < dst.size(); ++j) dst[j] += src[j];
+  }
+  cudaFree(c.items); cudaFree(c.base); cudaFree(c.vals);
+  c.items = nullptr; c.base = nullptr; c.vals = nullptr;
+  c.busy = false;
+}
+
 void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& titems,
                          const std::vector<std::vector<int32_t>>& rcol, std::vector<std::vector<double>>& rval,
                          const TriRules& rules, int64_t r0, int64_t r1) {
-  CKZ(cudaSetDevice(S.z0_device));
+  (void)rules;
+  Z0Pipe& P = g_z0;
+  CKZ(cudaSetDevice(P.dev));
+  Z0Pipe::Chunk& c = P.ch[P.cur];
+  z0_finish_chunk(c, rval);                       // the chunk two launches ago (normally done)
   std::vector<Z0Item> items;
   size_t tot = 0;
   for (auto& v : titems) tot += v.size();
   items.reserve(tot);
   for (auto& v : titems) { items.insert(items.end(), v.begin(), v.end()); std::vector<Z0Item>().swap(v); }
-  std::vector<int64_t> rowbase(r1 - r0 + 1, 0);
-  for (int64_t n = r0; n < r1; ++n) rowbase[n - r0 + 1] = rowbase[n - r0] + 3 * (int64_t)rcol[n].size();
-  const int64_t nvals = rowbase[r1 - r0];
-  Z0Item* d_items = up(items.data(), items.size());
-  double* d_xyz = up(S.xyz.data(), S.xyz.size());
-  int32_t* d_tets = up(S.tets.data(), S.tets.size());
-  int64_t* d_parent = up(S.parent.data(), S.parent.size());
-  double* d_ms = up(S.Ms_tet.data(), S.Ms_tet.size());
-  TriRules* d_rules = up(&rules, 1);
-  int64_t* d_base = up(rowbase.data(), rowbase.size());
-  double* d_vals = nullptr;
-  CKZ(cudaMalloc(&d_vals, std::max<int64_t>(nvals, 1) * sizeof(double)));
-  CKZ(cudaMemset(d_vals, 0, std::max<int64_t>(nvals, 1) * sizeof(double)));
+  c.r0 = r0; c.r1 = r1;
+  c.rowbase.assign(r1 - r0 + 1, 0);
+  for (int64_t n = r0; n < r1; ++n) c.rowbase[n - r0 + 1] = c.rowbase[n - r0] + 3 * (int64_t)rcol[n].size();
+  const int64_t nvals = c.rowbase[r1 - r0];
+  c.items = up(items.data(), items.size());
+  c.base = up(c.rowbase.data(), c.rowbase.size());
+  CKZ(cudaMalloc(&c.vals, std::max<int64_t>(nvals, 1) * sizeof(double)));
+  CKZ(cudaMemsetAsync(c.vals, 0, std::max<int64_t>(nvals, 1) * sizeof(double), P.st));
+  if ((size_t)nvals > c.hcap) {
+    if (c.hvals) cudaFreeHost(c.hvals);
+    c.hcap = (size_t)std::max<int64_t>(nvals, 1);
+    CKZ(cudaMallocHost(&c.hvals, c.hcap * sizeof(double)));
+  }
   Lat lat{{S.L[0], S.L[1], S.L[2]}};
   const int64_t n = (int64_t)items.size();
   static const bool thread_per_task = std::getenv("PMFEM_Z0_THREAD") != nullptr;
   if (n && thread_per_task) {
-    k_z0_items<<<(unsigned)((n + 127) / 128), 128>>>(d_items, n, d_xyz, d_tets, d_parent, d_ms, lat, d_rules, d_base,
-                                                     r0, d_vals);
+    k_z0_items<<<(unsigned)((n + 127) / 128), 128, 0, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules,
+                                                               c.base, r0, c.vals);
     CKZ(cudaGetLastError());
-    CKZ(cudaDeviceSynchronize());
   } else if (n) {
     const size_t smem = ((sizeof(TriRules) + 15) / 16) * 16 + Z0W_WARPS * sizeof(Z0Warp);
     CKZ(cudaFuncSetAttribute(k_z0_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int dev = 0, nsm = 148;
-    CKZ(cudaGetDevice(&dev));
-    CKZ(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    int nsm = 148;
+    CKZ(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.dev));
     const int64_t want = (n + Z0W_WARPS - 1) / Z0W_WARPS;
     const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)nsm * 32);
-    k_z0_warp<<<blocks, 32 * Z0W_WARPS, smem>>>(d_items, n, d_xyz, d_tets, d_parent, d_ms, lat, d_rules, d_base, r0,
-                                                d_vals);
+    k_z0_warp<<<blocks, 32 * Z0W_WARPS, smem, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules, c.base,
+                                                       r0, c.vals);
     CKZ(cudaGetLastError());
-    CKZ(cudaDeviceSynchronize());
   }
-  std::vector<double> vals(nvals);
-  if (nvals) CKZ(cudaMemcpy(vals.data(), d_vals, nvals * sizeof(double), cudaMemcpyDeviceToHost));
-  for (int64_t r = r0; r < r1; ++r) {
-    const double* src = &vals[rowbase[r - r0]];
-    std::vector<double>& dst = rval[r];
-    for (size_t j = 0; j < dst.size(); ++j) dst[j] += src[j];
+  if (nvals) CKZ(cudaMemcpyAsync(c.hvals, c.vals, nvals * sizeof(double), cudaMemcpyDeviceToHost, P.st));
+  CKZ(cudaEventRecord(c.done, P.st));
+  c.busy = true;
+  P.cur ^= 1;
+}
+
+void z0_device_end(std::vector<std::vector<double>>& rval) {
+  Z0Pipe& P = g_z0;
+  if (P.dev < 0) return;
+  CKZ(cudaSetDevice(P.dev));
+  for (int k = 0; k < 2; ++k) z0_finish_chunk(P.ch[(P.cur + k) & 1], rval);
+  for (auto& c : P.ch) {
+    if (c.hvals) cudaFreeHost(c.hvals);
+    c.hvals = nullptr; c.hcap = 0;
+    cudaEventDestroy(c.done);
   }
-  cudaFree(d_items); cudaFree(d_xyz); cudaFree(d_tets); cudaFree(d_parent); cudaFree(d_ms);
-  cudaFree(d_rules); cudaFree(d_base); cudaFree(d_vals);
+  cudaFree(P.xyz); cudaFree(P.tets); cudaFree(P.parent); cudaFree(P.ms); cudaFree(P.rules);
+  cudaStreamDestroy(P.st);
+  P = Z0Pipe();
 }
 
 }  // namespace pmfem
