@@ -1030,6 +1030,7 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
   pd.dim = Pp.dim;
   for (int i = 0; i < 3; ++i) { pd.ax[i] = Pp.ax[i]; pd.L[i] = Pp.L[i]; pd.nreal[i] = Pp.nreal[i]; pd.mrec[i] = Pp.mrec[i]; }
   pd.alpha = Pp.alpha;
+  pd.xr = Pp.xr;
   gauss_legendre01(64, pd.gl_x, pd.gl_w);
   const int P0 = D.P[0], P1 = D.P[1], P2 = D.P[2];
   const int64_t tot = (int64_t)P0 * P1 * P2;
