@@ -22,8 +22,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "periodic H_eff evals/s and mesh nodes/s at 1/2/4/8 B200; % HBM roofline"
-DEFAULTS = {"C2": dict(order=2, rer_scale=3.0, z0_ring=1), "C3": dict(order=2, rer_scale=3.0, z0_ring=1),
-            "C5": dict(order=2, rer_scale=3.0, z0_ring=1), "C4": dict(order=2, rer_scale=3.0, z0_ring=1),
+# AIM settings per workload: the cheapest (p, s) whose oracle AIM meets the paper's 1e-3 level
+# (reading R19: relative L2 of H_ms vs the oracle's brute force) at full size for both the
+# random and the smooth m field (scripts/calibrate_fullsize.py -> profiles/calib_*.json)
+DEFAULTS = {"C2": dict(order=3, rer_scale=4.0, z0_ring=1), "C3": dict(order=3, rer_scale=4.0, z0_ring=1),
+            "C5": dict(order=3, rer_scale=4.0, z0_ring=1), "C4": dict(order=3, rer_scale=4.0, z0_ring=1),
             "C1": dict(order=1, rer_scale=2.0, z0_ring=1)}
 CPU_SAMPLE = {"C1": 1, "C2": 8, "C3": 12, "C4": 24, "C5": 16}
 
@@ -348,7 +351,7 @@ def main():
                         "slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + all-reduce of the "
                         "anterpolated grid, replicated FFT" % world), "n_parents_local": Nloc,
                        "k2_tile": info["k2_tile"],
-                       "cbox_format": ["C4x", "B4", "SEG"][info["cbox_format"]],
+                       "cbox_format": ["C4x", "B4", "SEG", "U4"][info["cbox_format"]],
                        "cbox_packed_units": info["cbox_packed_units"]},
             "nodes_per_s": value * Np, "setup_s": t_setup, "build_pgf_s": t_pgf,
             "bytes_per_eval_algorithmic": alg_total,

@@ -325,6 +325,44 @@ __global__ void k_b4_fill(long long Np, const long long* __restrict__ rowptr, co
   }
 }
 
+// ---- U4: blocks of 4 consecutive columns [c, c+4) starting at ANY column c (greedy from the
+// first uncovered entry of a column-sorted row: the fewest length-4 windows covering the row),
+// per block a float4 of values (0 for columns outside the near set) and the int32 start c.  K4
+// gathers q for a block with one 16-byte load of the per-evaluation array q4[c] = (q[c..c+3]),
+// so blocks need no alignment and only run ends leave empty slots (B4 also wastes the slots
+// before a run's first aligned boundary).
+__global__ void k_u4_count(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                           long long* __restrict__ nb) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long blocks = 0;
+  long long end = -1;                 // last column covered by the current block
+  for (long long e = rowptr[n]; e < rowptr[n + 1]; ++e) {
+    if (col[e] > end) { ++blocks; end = (long long)col[e] + 3; }
+  }
+  nb[n] = blocks;
+}
+
+__global__ void k_u4_fill(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                          const float* __restrict__ val, const long long* __restrict__ bptr,
+                          int* __restrict__ bstart, float* __restrict__ bval) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  long long o = bptr[n] - 1;
+  long long end = -1;
+  int start = 0;
+  for (long long e = rowptr[n]; e < rowptr[n + 1]; ++e) {
+    if (col[e] > end) {
+      ++o;
+      start = col[e];
+      end = (long long)start + 3;
+      bstart[o] = start;
+      for (int j = 0; j < 4; ++j) bval[4 * o + j] = 0.f;
+    }
+    bval[4 * o + (col[e] - start)] = val[e];
+  }
+}
+
 template <class T>
 T* dalloc_c(size_t n) {
   T* p = nullptr;
@@ -392,10 +430,11 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   std::vector<long long> ptr(Np + 1, 0);
   for (int64_t i = 0; i < Np; ++i) ptr[i + 1] = ptr[i] + cnt[i];
   const int64_t nnz = ptr[Np];
-  // ---- SEG (default): candidate reach R_a = ceil(rho_a + 1) - 1, rho_a = r_ER / Delta_a; usable
+  // ---- SEG (opt-in, PMFEM_CBOX_FORMAT=seg; measured slower: per-row run tables and a serial
+  // mask walk are latency-bound, profiles/ab/r02_*): candidate reach R_a = ceil(rho_a + 1) - 1, rho_a = r_ER / Delta_a; usable
   // when every row's near set (the for_near count above) is found among its candidates
   const char* fmt_env = std::getenv("PMFEM_CBOX_FORMAT");
-  const std::string fmt = fmt_env ? std::string(fmt_env) : std::string("seg");
+  const std::string fmt = fmt_env ? std::string(fmt_env) : std::string("u4");
   if (fmt == "seg") {
     SegGeom G{};
     for (int a = 0; a < 3; ++a) {
@@ -473,10 +512,27 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   // B4 unless it streams > 15 % more bytes than C4x (its gathers are 4x fewer L1 requests:
   // measured C2 +11 % bytes -> K4 4 % faster, C3 +33 % bytes -> 46 % slower);
   // PMFEM_CBOX_FORMAT=c4x|b4 forces one (tests)
-  bool use_b4 = 20.0 * bptr[Np] <= 1.15 * 24.0 * cptr[Np];
-  if (fmt == "c4x") use_b4 = false;
-  else if (fmt == "b4") use_b4 = true;
-  if (use_b4) {
+  // U4 (default): never more blocks than B4 (greedy unaligned covering), one 16-byte q4 gather
+  // per block; PMFEM_CBOX_FORMAT=c4x|b4|u4|seg forces a format (tests, A/B)
+  bool use_b4 = fmt == "b4";
+  const bool use_c4x = fmt == "c4x";
+  if (!use_b4 && !use_c4x) {
+    std::vector<long long> nu(Np), uptr(Np + 1, 0);
+    k_u4_count<<<blocks, 128>>>(Np, d_ptr, d_col, d_nch);
+    CKC(cudaGetLastError());
+    CKC(cudaMemcpy(nu.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < Np; ++i) uptr[i + 1] = uptr[i] + nu[i];
+    long long* d_uptr = dup_c(uptr);
+    int* d_ustart = dalloc_c<int>(uptr[Np]);
+    float* d_uval = dalloc_c<float>(4 * uptr[Np]);
+    k_u4_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_uptr, d_ustart, d_uval);
+    CKC(cudaGetLastError());
+    D.c_ptr = reinterpret_cast<int64_t*>(d_uptr);
+    D.c_bidx = d_ustart;
+    D.c_val = d_uval;
+    D.cbox_chunks = uptr[Np];
+    D.cbox_format = 3;
+  } else if (use_b4) {
     long long* d_bptr = dup_c(bptr);
     int* d_bidx = dalloc_c<int>(bptr[Np]);
     float* d_bval = dalloc_c<float>(4 * bptr[Np]);

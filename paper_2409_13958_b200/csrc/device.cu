@@ -383,7 +383,9 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
   const int64_t b = valid ? c_ptr[n] : 0, e_end = valid ? c_ptr[n + 1] : 0;
-  if (F == 1) {
+  if (F == 1 || F == 3) {
+    // B4: block index b, q4 = q viewed as float4 (aligned [4b, 4b+4)); U4: start column c,
+    // q4 = the per-evaluation shifted copy (q[c..c+3]) passed in place of q
     const float4* q4 = reinterpret_cast<const float4*>(q);
 #pragma unroll 4
     for (int64_t e = b + lane; e < e_end; e += G) {
@@ -566,6 +568,13 @@ __global__ void __launch_bounds__(256) k4_seg(RowRange rr, const float* __restri
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
   if (valid && lane == 0) u[n] = acc + uloc[n];
+}
+
+// U4 C_box: q4[i] = (q[i], q[i+1], q[i+2], q[i+3]) (q carries 4 trailing zeros)
+__global__ void k_q4(int64_t n, const float* __restrict__ q, float4* __restrict__ q4) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  q4[i] = make_float4(q[i], q[i + 1], q[i + 2], q[i + 3]);
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
@@ -926,6 +935,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   }
   // q: + 4 zero floats so B4's aligned 4-column gathers stay in bounds
   D.q = dalloc<float>(Np + 4); D.uloc = dalloc<float>(Np); D.u = dalloc<float>(Np);
+  if (D.cbox_format == 3) D.q4 = dalloc<float4>(Np);
   CK(cudaMemset(D.q, 0, sizeof(float) * (size_t)(Np + 4)));
   D.Q = dalloc<float>((size_t)D.n[0] * D.n[1] * D.n[2]);
   D.C = dalloc<float2>((size_t)D.H0 * D.P[1] * D.P[2]);
@@ -953,7 +963,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       D.yz_half = tile == 1 && D.P[2] == 2 * D.n[2] && D.n[2] >= 2 && yh != nullptr && std::atoi(yh) == 1;
     }
   }
-  D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5);       // m4, K1, K2, FFT passes, K4, K5
+  D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5) + (D.cbox_format == 3 ? 1 : 0);   // m4, K1, K2, FFT, (q4), K4, K5
   D.k4_vec = std::getenv("PMFEM_K4_VEC") != nullptr && std::atoi(std::getenv("PMFEM_K4_VEC")) == 1;
   D.row_split = 1;            // 2 measured slower on C2 (K1 0.067 -> 0.070 ms); kept for PMFEM_ROW_SPLIT=2
   if (const char* e = std::getenv("PMFEM_ROW_SPLIT")) {
@@ -978,7 +988,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
       D.slab_buf = dalloc<float2>((size_t)(D.world > 1 ? nzl : D.n[2]) * plane * D.H0);
       D.fused_tile = 0;
       // per rank: X, Y, pack, Z, unpack, Y', X' (+ W-1 sends/receives and the copies in NCCL)
-      D.launches_per_eval = 5 + 7 * (D.world > 1 ? 1 : W);
+      D.launches_per_eval = 5 + 7 * (D.world > 1 ? 1 : W) + (D.cbox_format == 3 ? 1 : 0);
     }
   }
   // compulsory bytes per launch: every array read or written once (gathered m, q, u once),
@@ -1018,6 +1028,8 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   // SEG: 4-byte value per near pair + the candidate bitmask words + two 8-byte row offsets
   if (D.cbox_format == 2)
     D.kernel_bytes[3] = Np * (16.0 + 16 + 16 + 4 + 4 + 4) + (double)cnnz * 4 + (double)D.seg_mask_words * 4 + G * 4.0;
+  else if (D.cbox_format == 3)   // + the q4 copy (4-byte read, 16-byte write per row)
+    D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4 + 20) + (double)cnnz * 5 + G * 4.0;
   else
     D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + G * 4.0;
   D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
@@ -1069,7 +1081,7 @@ void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
   void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_bidx, D.c_val,
-                  D.seg_moff, D.seg_mask,
+                  D.seg_moff, D.seg_mask, D.q4,
                   D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
                   D.send_buf, D.recv_buf, D.slab_cx, D.slab_buf, D.slab_spec, D.send_idx[0], D.send_idx[1], D.send_idx[2],
@@ -1306,6 +1318,10 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   halo(D, 1, D.q, 1, st);
   mark(3);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
+  if (D.cbox_format == 3) {
+    k_q4<<<(unsigned)((D.Np + 255) / 256), 256, 0, st>>>(D.Np, D.q, D.q4);
+    CK(cudaGetLastError());
+  }
   if (D.cbox_format == 2) {
     const int G = D.k4_group;
     const size_t smem = sizeof(int) * (size_t)(256 / G) * (2 * D.seg_maxseg + 2);
@@ -1328,7 +1344,11 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   } else
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
-  (D.cbox_format == 1                                                                                   \
+  (D.cbox_format == 3                                                                                   \
+       ? k4_interp_corr<PP, GG, 3><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4,                                \
+             reinterpret_cast<const float*>(D.q4), D.uloc, D.u)                                         \
+   : D.cbox_format == 1                                                                                 \
        ? k4_interp_corr<PP, GG, 1><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
    : D.k4_vec                                                                                           \

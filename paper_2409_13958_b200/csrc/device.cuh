@@ -76,7 +76,9 @@ struct DeviceState {
   float* c_val = nullptr;             // [chunks][4]
   int64_t cbox_nnz = 0;               // near pairs (entries without chunk padding)
   int64_t cbox_chunks = 0;             // C4x chunks or B4 blocks
-  int cbox_format = 0;                // 0: C4x, 1: B4 (aligned 4-column blocks, c_bidx + c_val), 2: SEG
+  int cbox_format = 0;                // 0: C4x, 1: B4 (aligned 4-column blocks, c_bidx + c_val), 2: SEG,
+                                      // 3: U4 (unaligned 4-column blocks, start in c_bidx, q4 gathers)
+  float4* q4 = nullptr;               // U4: per evaluation q4[i] = (q[i], q[i+1], q[i+2], q[i+3])
   SegGeom seg{};                      // SEG: candidate geometry
   int seg_maxseg = 0;                 // SEG: largest number of column runs of a row
   int64_t* seg_moff = nullptr;        // SEG: [N'+1] mask word offsets (c_ptr holds the value offsets)

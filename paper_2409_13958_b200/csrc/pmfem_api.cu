@@ -408,14 +408,16 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
       } else if (tail == "val") {
         *count = 4 * nch;
         if (dst && nch) cudaMemcpy(dst, D.c_val, sizeof(float) * 4 * (size_t)nch, cudaMemcpyDeviceToHost);
-      } else if (tail == "col" && D.cbox_format == 1) {
+      } else if (tail == "col" && (D.cbox_format == 1 || D.cbox_format == 3)) {
+        // B4: aligned block index b -> columns 4b..4b+3; U4: start column c -> c..c+3
         *count = 4 * nch;
         if (dst && nch) {
           std::vector<int32_t> b(nch);
           cudaMemcpy(b.data(), D.c_bidx, sizeof(int32_t) * (size_t)nch, cudaMemcpyDeviceToHost);
           int32_t* c = static_cast<int32_t*>(dst);
+          const int32_t mul = D.cbox_format == 1 ? 4 : 1;
           for (int64_t i = 0; i < nch; ++i)
-            for (int j = 0; j < 4; ++j) c[4 * i + j] = 4 * b[i] + j;
+            for (int j = 0; j < 4; ++j) c[4 * i + j] = mul * b[i] + j;
         }
       } else if (tail == "col") {
         *count = 4 * nch;
