@@ -98,13 +98,14 @@ __device__ void for_near(const CboxGeom& c, const double* __restrict__ xw, const
         }
 }
 
-__global__ void k_cbox_count(CboxGeom c, long long Np, const double* __restrict__ xw, const int* __restrict__ box_ptr,
-                             int* __restrict__ cnt) {
-  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= Np) return;
+// rows r0 + [0, Np) (a rank's own rows); per-row outputs are indexed locally
+__global__ void k_cbox_count(CboxGeom c, long long Np, long long r0, const double* __restrict__ xw,
+                             const int* __restrict__ box_ptr, int* __restrict__ cnt) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Np) return;
   int k_cnt = 0;
-  for_near(c, xw, box_ptr, n, [&](int, const double*, const int*) { ++k_cnt; });
-  cnt[n] = k_cnt;
+  for_near(c, xw, box_ptr, r0 + i, [&](int, const double*, const int*) { ++k_cnt; });
+  cnt[i] = k_cnt;
 }
 
 // C_box entry (K9) of the near pair (n, k, img): G0*(d) - sum_{a,b} w_na w_kb G0*((a - b - img N) o Delta),
@@ -141,14 +142,16 @@ __device__ __forceinline__ double cbox_entry(const CboxGeom& c, const double (*w
   return v - gm;
 }
 
-__global__ void k_cbox_fill(CboxGeom c, long long Np, const double* __restrict__ xw, const int* __restrict__ box_ptr,
-                            const int* __restrict__ s_unw, const double* __restrict__ t_loc,
-                            const long long* __restrict__ rowptr, int* __restrict__ col, float* __restrict__ val) {
-  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= Np) return;
+__global__ void k_cbox_fill(CboxGeom c, long long Np, long long r0, const double* __restrict__ xw,
+                            const int* __restrict__ box_ptr, const int* __restrict__ s_unw,
+                            const double* __restrict__ t_loc, const long long* __restrict__ rowptr,
+                            int* __restrict__ col, float* __restrict__ val) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Np) return;
+  const long long n = r0 + i;
   double wn[3][4];
   for (int a = 0; a < 3; ++a) lagr_d(t_loc[3 * n + a], c.p, wn[a]);
-  long long o = rowptr[n];
+  long long o = rowptr[i];
   for_near(c, xw, box_ptr, n, [&](int k, const double* d, const int* img) {
     col[o] = k;
     val[o] = (float)cbox_entry(c, wn, t_loc, s_unw, n, k, d, img);
@@ -395,15 +398,16 @@ void device_seg_decode(const DeviceState& D, int* d_col) {
 
 int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   CKC(cudaSetDevice(D.device));
-  const int64_t Np = S.Np;
-  if (Np >= (int64_t(1) << 28)) throw Error(PMFEM_E_INVALID_ARG, "C4x column base holds 28 bits: N' < 2^28 required");
+  const int64_t Nall = S.Np;
+  const int64_t r0 = D.lo, Np = D.hi - D.lo;          // this rank's own rows
+  if (Nall >= (int64_t(1) << 28)) throw Error(PMFEM_E_INVALID_ARG, "C4x column base holds 28 bits: N' < 2^28 required");
   const int p = S.order;
   CboxGeom c{};
   c.p = p;
   c.rer = S.rer_scale * std::max(S.delta[0], std::max(S.delta[1], S.delta[2]));
-  std::vector<double> xw(3 * Np), tl(3 * Np);
-  std::vector<int> su(3 * Np);
-  for (int64_t i = 0; i < Np; ++i) {
+  std::vector<double> xw(3 * Nall), tl(3 * Nall);
+  std::vector<int> su(3 * Nall);
+  for (int64_t i = 0; i < Nall; ++i) {
     const int64_t r = S.perm[i];
     for (int a = 0; a < 3; ++a) {
       xw[3 * i + a] = S.xw[3 * r + a];
@@ -423,7 +427,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   int* d_su = dup_c(su);
   int* d_cnt = dalloc_c<int>(Np);
   const unsigned blocks = (unsigned)((Np + 127) / 128);
-  k_cbox_count<<<blocks, 128>>>(c, Np, d_xw, D.box_ptr, d_cnt);
+  k_cbox_count<<<blocks, 128>>>(c, Np, r0, d_xw, D.box_ptr, d_cnt);
   CKC(cudaGetLastError());
   std::vector<int> cnt(Np);
   CKC(cudaMemcpy(cnt.data(), d_cnt, sizeof(int) * Np, cudaMemcpyDeviceToHost));
@@ -435,7 +439,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   // when every row's near set (the for_near count above) is found among its candidates
   const char* fmt_env = std::getenv("PMFEM_CBOX_FORMAT");
   const std::string fmt = fmt_env ? std::string(fmt_env) : std::string("u4");
-  if (fmt == "seg") {
+  if (fmt == "seg" && D.world == 1) {
     SegGeom G{};
     for (int a = 0; a < 3; ++a) {
       const double rho = c.rer / c.delta[a];
@@ -497,7 +501,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   long long* d_ptr = dup_c(ptr);
   int* d_col = dalloc_c<int>(nnz);
   float* d_val = dalloc_c<float>(nnz);
-  k_cbox_fill<<<blocks, 128>>>(c, Np, d_xw, D.box_ptr, d_su, d_tl, d_ptr, d_col, d_val);
+  k_cbox_fill<<<blocks, 128>>>(c, Np, r0, d_xw, D.box_ptr, d_su, d_tl, d_ptr, d_col, d_val);
   CKC(cudaGetLastError());
   // sizes of both packed formats: C4x chunks (24 B) and B4 blocks (20 B)
   long long* d_nch = dalloc_c<long long>(Np);

@@ -57,6 +57,7 @@ float __int_as_float_host(int32_t c) { float f; std::memcpy(&f, &c, 4); return f
 // n - hoff (hoff = row0 for the rank-local H of a distributed context, 0 otherwise).
 struct RowRange {
   int64_t row0, row1, hoff;
+  int c0, c1, c2;          // user component of internal axis 0, 1, 2 (axis permutation of m, H)
 };
 
 // halo pack / unpack: buf[i*w + c] <-> v[idx[i]*w + c]
@@ -97,7 +98,7 @@ __global__ void k_to_m4(RowRange rr, const float* __restrict__ m, float4* __rest
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= rr.row1) return;
   const int64_t h = n - rr.hoff;
-  m4[n] = make_float4(m[3 * h], m[3 * h + 1], m[3 * h + 2], 0.f);
+  m4[n] = make_float4(m[3 * h + rr.c0], m[3 * h + rr.c1], m[3 * h + rr.c2], 0.f);
 }
 
 // SPLIT = 2 (small meshes, < ~1M rows): two threads per row, lanes 0-15 of a warp take the
@@ -116,8 +117,8 @@ __global__ void __launch_bounds__(256) k1_local_in(
   else { n = rr.row0 + (gid >> 6) * 32 + ((gid >> 5) & 1) * 16 + (threadIdx.x & 15); part = (threadIdx.x >> 4) & 1; }
   const bool valid = n < rr.row1;
   if (SPLIT == 1 && !valid) return;
-  const int64_t s = n >> 5;
-  const int l = (int)(n & 31);
+  const int64_t s = (n - rr.row0) >> 5;                 // slices are relative to the own rows
+  const int l = (int)((n - rr.row0) & 31);
   int64_t o = 0, o1 = 0;
   int w = 0, w1 = 0;
   float4 mn = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(256) k1_local_in(
   const float4 rd = rowsum[2 * n], rz = rowsum[2 * n + 1];
   q[n] = qq + rd.x * mn.x + rd.y * mn.y + rd.z * mn.z;
   uloc[n] = ul + rz.x * mn.x + rz.y * mn.y + rz.z * mn.z;
-  if (write_hex) { H[3 * (n - rr.hoff)] = hx; H[3 * (n - rr.hoff) + 1] = hy; H[3 * (n - rr.hoff) + 2] = hz; }
+  if (write_hex) { H[3 * (n - rr.hoff) + rr.c0] = hx; H[3 * (n - rr.hoff) + rr.c1] = hy; H[3 * (n - rr.hoff) + rr.c2] = hz; }
 }
 
 // exchange only: H = L m
@@ -165,8 +166,8 @@ __global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float4* __r
                                                   float* __restrict__ H) {
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= rr.row1) return;
-  const int64_t s = n >> 5;
-  const int l = (int)(n & 31);
+  const int64_t s = (n - rr.row0) >> 5;
+  const int l = (int)((n - rr.row0) & 31);
   const int64_t o = sl_off[s], o1 = sl1_off[s];
   const int w1 = (int)((sl1_off[s + 1] - o1) >> 5);
   const float4 mn = m4[n];
@@ -178,7 +179,7 @@ __global__ void __launch_bounds__(256) k_exchange(RowRange rr, const float4* __r
     const float L = __ldg(&s_LD[e1].x);
     hx = fmaf(L, mc.x - mn.x, hx); hy = fmaf(L, mc.y - mn.y, hy); hz = fmaf(L, mc.z - mn.z, hz);
   }
-  H[3 * (n - rr.hoff)] = hx; H[3 * (n - rr.hoff) + 1] = hy; H[3 * (n - rr.hoff) + 2] = hz;
+  H[3 * (n - rr.hoff) + rr.c0] = hx; H[3 * (n - rr.hoff) + rr.c1] = hy; H[3 * (n - rr.hoff) + rr.c2] = hz;
 }
 
 // Lagrange weights on nodes 0..P at local coordinate t
@@ -234,7 +235,7 @@ template <int P>
 __global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const int32_t* __restrict__ box_ptr,
                                                const int4* __restrict__ st_s, const float4* __restrict__ st_t,
                                                const float* __restrict__ q, int64_t lo, int64_t hi, int box_max,
-                                               float* __restrict__ Q) {
+                                               int bz0, float* __restrict__ Q) {
   extern __shared__ int tile[];
   __shared__ int red_q;
   __shared__ int wsum[8];
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const in
   int* seg_beg = tile + vol;
   int* seg_cum = seg_beg + k2_nseg(T1, T2, P);
   const int nt0 = g.n0 / T0, nt1 = g.n1 / T1;
-  const int bx = blockIdx.x % nt0, by = (blockIdx.x / nt0) % nt1, bz = blockIdx.x / (nt0 * nt1);
+  const int bx = blockIdx.x % nt0, by = (blockIdx.x / nt0) % nt1, bz = bz0 + blockIdx.x / (nt0 * nt1);
   const int x0 = bx * T0, y0 = by * T1, z0 = bz * T2;
   for (int i = threadIdx.x; i < vol; i += blockDim.x) tile[i] = 0;
   if (threadIdx.x == 0) red_q = 0;
@@ -382,7 +383,7 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
-  const int64_t b = valid ? c_ptr[n] : 0, e_end = valid ? c_ptr[n + 1] : 0;
+  const int64_t b = valid ? c_ptr[n - rr.row0] : 0, e_end = valid ? c_ptr[n - rr.row0 + 1] : 0;
   if (F == 1 || F == 3) {
     // B4: block index b, q4 = q viewed as float4 (aligned [4b, 4b+4)); U4: start column c,
     // q4 = the per-evaluation shifted copy (q[c..c+3]) passed in place of q
@@ -522,8 +523,8 @@ __global__ void __launch_bounds__(256) k4_seg(RowRange rr, const float* __restri
   const int ncand = carry;
   // ---- masked candidate loop
   if (valid && ncand > 0) {
-    const uint32_t* M = mask + moff[n];
-    const float* V = val + voff[n];
+    const uint32_t* M = mask + moff[n - rr.row0];
+    const float* V = val + voff[n - rr.row0];
     const int nwords = (ncand + 31) >> 5;
     int base = 0, sidx = 0;
     for (int w = 0; w < nwords; ++w) {
@@ -588,8 +589,8 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
   else { n = rr.row0 + (gid >> 6) * 32 + ((gid >> 5) & 1) * 16 + (threadIdx.x & 15); part = (threadIdx.x >> 4) & 1; }
   const bool valid = n < rr.row1;
   if (SPLIT == 1 && !valid) return;
-  const int64_t s = n >> 5;
-  const int l = (int)(n & 31);
+  const int64_t s = (n - rr.row0) >> 5;
+  const int l = (int)((n - rr.row0) & 31);
   int64_t o1 = 0;
   int w1 = 0;
   float un = 0.f;
@@ -608,8 +609,11 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
     if (part) return;
   }
   if (!valid) return;
-  if (accumulate) { H[3 * (n - rr.hoff)] -= gx; H[3 * (n - rr.hoff) + 1] -= gy; H[3 * (n - rr.hoff) + 2] -= gz; }
-  else { H[3 * (n - rr.hoff)] = -gx; H[3 * (n - rr.hoff) + 1] = -gy; H[3 * (n - rr.hoff) + 2] = -gz; }
+  if (accumulate) {
+    H[3 * (n - rr.hoff) + rr.c0] -= gx; H[3 * (n - rr.hoff) + rr.c1] -= gy; H[3 * (n - rr.hoff) + rr.c2] -= gz;
+  } else {
+    H[3 * (n - rr.hoff) + rr.c0] = -gx; H[3 * (n - rr.hoff) + rr.c1] = -gy; H[3 * (n - rr.hoff) + rr.c2] = -gz;
+  }
 }
 
 // ------------------------------------------------------------------ LLG RK4 stage (NEXT-2)
@@ -788,20 +792,23 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.H0 = D.P[0] / 2 + 1;
   D.rank = S.dist.rank;
   D.world = S.dist.world;
+  for (int a = 0; a < 3; ++a) D.axperm[a] = S.axperm[a];
   D.lo = S.dist.lo();
   D.hi = S.dist.hi();
 
-  // ---- shared local operator in SELL-32, internal order
-  const int64_t ns = (Np + 31) / 32;
+  // ---- shared local operator in SELL-32, internal order; a rank stores its own rows [lo, hi)
+  // only (slices relative to lo)
+  const int64_t lo = D.lo, nloc = D.hi - D.lo;
+  const int64_t ns = (nloc + 31) / 32;
   D.nslices = ns;
   std::vector<int64_t> sl_off(ns + 1, 0), sl1_off(ns + 1, 0);
-  // per internal row: ring-1 cols (user ids) + Z0-only cols, with values
-  std::vector<int> len1(Np), lenz(Np);
-  std::vector<std::vector<int32_t>> rcols(Np);
-  std::vector<std::vector<float>> rz(Np), rld(Np), rg(Np);
+  // per own internal row: ring-1 cols (user ids) + Z0-only cols, with values
+  std::vector<int> len1(nloc), lenz(nloc);
+  std::vector<std::vector<int32_t>> rcols(nloc);
+  std::vector<std::vector<float>> rz(nloc), rld(nloc), rg(nloc);
 #pragma omp parallel for schedule(dynamic, 1024)
-  for (int64_t i = 0; i < Np; ++i) {
-    const int64_t r = S.perm[i];
+  for (int64_t i = 0; i < nloc; ++i) {
+    const int64_t r = S.perm[lo + i];
     std::vector<std::pair<int32_t, int64_t>> r1, rzl;
     for (int64_t e = S.ring1.rowptr[r]; e < S.ring1.rowptr[r + 1]; ++e) r1.push_back({(int32_t)S.iperm[S.ring1.col[e]], e});
     for (int64_t e = S.z0.rowptr[r]; e < S.z0.rowptr[r + 1]; ++e) rzl.push_back({(int32_t)S.iperm[S.z0.col[e]], e});
@@ -830,7 +837,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   }
   for (int64_t s = 0; s < ns; ++s) {
     int w = 0, w1 = 0;
-    for (int64_t i = 32 * s; i < std::min(Np, 32 * s + 32); ++i) { w = std::max(w, lenz[i]); w1 = std::max(w1, len1[i]); }
+    for (int64_t i = 32 * s; i < std::min(nloc, 32 * s + 32); ++i) { w = std::max(w, lenz[i]); w1 = std::max(w1, len1[i]); }
     sl_off[s + 1] = sl_off[s] + 32 * (int64_t)w;
     sl1_off[s + 1] = sl1_off[s] + 32 * (int64_t)w1;
   }
@@ -843,16 +850,16 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   for (int64_t s = 0; s < ns; ++s) {
     const int w = (int)((sl_off[s + 1] - sl_off[s]) / 32), w1 = (int)((sl1_off[s + 1] - sl1_off[s]) / 32);
     for (int l = 0; l < 32; ++l) {
-      const int64_t i = 32 * s + l;
-      const int32_t self = (int32_t)std::min<int64_t>(i, Np - 1);   // padding: the row itself, weight 0
+      const int64_t i = 32 * s + l;                                      // local row
+      const int32_t self = (int32_t)(lo + std::min<int64_t>(i, nloc - 1));   // padding: the row itself, weight 0
       for (int j = 0; j < w; ++j) {
         const int64_t e = sl_off[s] + 32 * j + l;
-        if (i < Np && j < lenz[i]) s_zc[e] = pack(rz[i][3 * j], rz[i][3 * j + 1], rz[i][3 * j + 2], rcols[i][j]);
+        if (i < nloc && j < lenz[i]) s_zc[e] = pack(rz[i][3 * j], rz[i][3 * j + 1], rz[i][3 * j + 2], rcols[i][j]);
         else s_zc[e] = pack(0.f, 0.f, 0.f, self);
       }
       for (int j = 0; j < w1; ++j) {
         const int64_t e1 = sl1_off[s] + 32 * j + l;
-        if (i < Np && j < len1[i]) {
+        if (i < nloc && j < len1[i]) {
           s_LD[e1] = make_float4(rld[i][4 * j], rld[i][4 * j + 1], rld[i][4 * j + 2], rld[i][4 * j + 3]);
           s_Gc[e1] = pack(rg[i][3 * j], rg[i][3 * j + 1], rg[i][3 * j + 2], rcols[i][j]);
         } else {
@@ -970,35 +977,54 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     const int v = std::atoi(e);
     if (v == 1 || v == 2) D.row_split = v;
   }
-  // slab-decomposed convolution: NCCL ranks, or simulated ranks on one device (tests)
+  // slab-decomposed convolution: NCCL ranks (z slabs = the row partition's planes), or simulated
+  // ranks on one device (tests, PMFEM_SLAB_SIM=W: the same plane rule for W ranks)
   {
     int W = 1;
     if (D.world > 1) {
-      if (D.n[2] % D.world == 0 && D.H0 >= D.world && std::getenv("PMFEM_NO_SLAB") == nullptr) W = D.world;
+      if (D.H0 >= D.world && std::getenv("PMFEM_NO_SLAB") == nullptr) W = D.world;
     } else if (const char* e = std::getenv("PMFEM_SLAB_SIM")) {
       const int w = std::atoi(e);
-      if (w > 1 && D.n[2] % w == 0 && D.H0 >= w) W = w;
+      if (w > 1 && D.H0 >= w && D.n[2] >= w) W = w;
     }
     D.slab_world = W;
     if (W > 1) {
-      const int64_t plane = (int64_t)D.P[1], nzl = D.n[2] / W;
+      if (D.world > 1) {
+        D.zpl.assign(S.dist.planes.begin(), S.dist.planes.end());
+        for (int k = 0; k < 2; ++k) { D.gsend[k] = S.dist.gsend[k]; D.grecv[k] = S.dist.grecv[k]; }
+      } else {
+        const std::vector<int32_t> z = slab_planes(S, W, slab_granularity(S, W));
+        D.zpl.assign(z.begin(), z.end());
+      }
+      int nzmax = 0;
+      for (int r = 0; r < W; ++r) nzmax = std::max(nzmax, D.zpl[r + 1] - D.zpl[r]);
+      const int64_t plane = (int64_t)D.P[1];
       const int64_t Hr = D.world > 1 ? slab_hn(D.rank, D.H0, W) : D.H0;
       D.slab_cx = dalloc<float2>((size_t)D.P[2] * plane * Hr);
       D.slab_spec = dalloc<float>((size_t)D.P[2] * plane * Hr);
-      D.slab_buf = dalloc<float2>((size_t)(D.world > 1 ? nzl : D.n[2]) * plane * D.H0);
+      D.slab_buf = dalloc<float2>((size_t)(D.world > 1 ? nzmax : D.n[2]) * plane * D.H0);
       D.fused_tile = 0;
       // per rank: X, Y, pack, Z, unpack, Y', X' (+ W-1 sends/receives and the copies in NCCL)
       D.launches_per_eval = 5 + 7 * (D.world > 1 ? 1 : W) + (D.cbox_format == 3 ? 1 : 0);
     }
   }
+  // K2 tiles must not straddle a z-slab boundary: the z tile divides every slab's planes
+  if (D.slab_world > 1) {
+    int t2 = D.k2_tile[2];
+    auto ok = [&](int t) { for (int b : D.zpl) if (b % t) return false; return true; };
+    while (t2 > 1 && !ok(t2)) t2 >>= 1;
+    D.k2_tile[2] = t2;
+  }
   // compulsory bytes per launch: every array read or written once (gathered m, q, u once),
   // actual entries only (SELL padding is overhead, not algorithmic traffic)
   const double G = (double)D.n[0] * D.n[1] * D.n[2];
   double nsh = 0, n1e = 0;
-  for (int64_t i = 0; i < Np; ++i) { nsh += lenz[i]; n1e += len1[i]; }
+  for (int64_t i = 0; i < nloc; ++i) { nsh += lenz[i]; n1e += len1[i]; }
   // K1 window = m -> float4 copy (12 + 16) + K1 (m4 16, row sums 32, slice offsets ~0, q, u_loc, H_ex)
-  D.kernel_bytes[0] = Np * (12.0 + 16 + 16 + 32 + 4 + 4 + 12) + nsh * 16 + n1e * 16;
-  D.kernel_bytes[1] = Np * (4.0 + 16 + 16) + G * 4.0 * 2;     // q + anchors + local t, box_ptr, Q write
+  D.kernel_bytes[0] = nloc * (12.0 + 16 + 16 + 32 + 4 + 4 + 12) + nsh * 16 + n1e * 16;
+  // q + anchors + local t of the rows read (own + halo band), box_ptr, Q write of the own planes
+  const double Gl = G * (double)(S.dist.planes[S.dist.rank + 1] - S.dist.planes[S.dist.rank]) / D.n[2];
+  D.kernel_bytes[1] = (double)std::min<int64_t>(Np, nloc + (int64_t)S.dist.recv_idx[1].size()) * (4.0 + 16 + 16) + Gl * 4.0 * 2;
   {
     const double Hc = (double)D.H0;
     const double spec_b = Hc * D.P[1] * D.P[2] * 4;
@@ -1027,12 +1053,12 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   // of block index (chunk padding / empty block slots are format overhead, not counted)
   // SEG: 4-byte value per near pair + the candidate bitmask words + two 8-byte row offsets
   if (D.cbox_format == 2)
-    D.kernel_bytes[3] = Np * (16.0 + 16 + 16 + 4 + 4 + 4) + (double)cnnz * 4 + (double)D.seg_mask_words * 4 + G * 4.0;
+    D.kernel_bytes[3] = nloc * (16.0 + 16 + 16 + 4 + 4 + 4) + (double)cnnz * 4 + (double)D.seg_mask_words * 4 + Gl * 4.0;
   else if (D.cbox_format == 3)   // + the q4 copy (4-byte read, 16-byte write per row)
-    D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4 + 20) + (double)cnnz * 5 + G * 4.0;
+    D.kernel_bytes[3] = nloc * (16.0 + 16 + 8 + 4 + 4 + 4) + Np * 20.0 + (double)cnnz * 5 + Gl * 4.0;
   else
-    D.kernel_bytes[3] = Np * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + G * 4.0;
-  D.kernel_bytes[4] = Np * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
+    D.kernel_bytes[3] = nloc * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + Gl * 4.0;
+  D.kernel_bytes[4] = nloc * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
 
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
@@ -1114,12 +1140,20 @@ void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id) {
   D.comm = comm;
   int64_t sbuf = 0, rbuf = 0;
   const int width[3] = {4, 1, 1};   // m travels as the float4 copy
-  // grid traffic sent per rank: ring all-reduce of Q (replicated FFT), or reduce-scatter +
-  // all-gather of Q plus the two spectrum transposes (slab FFT)
-  const double Gq = 4.0 * (double)D.n[0] * D.n[1] * D.n[2] * (P.world - 1) / P.world;
-  D.comm_bytes_per_eval = 2.0 * Gq;
-  if (D.slab_world > 1)
-    D.comm_bytes_per_eval += 2.0 * 8.0 * (double)(D.n[2] / P.world) * D.P[1] * (D.H0 - slab_hn(P.rank, D.H0, P.world));
+  // grid traffic per rank: the two spectrum transposes and the U ghost planes (slab FFT), or a
+  // ring all-reduce of Q (replicated FFT)
+  const double plane_b = 4.0 * (double)D.n[0] * D.n[1];
+  if (D.slab_world > 1) {
+    const int nz = D.zpl[P.rank + 1] - D.zpl[P.rank];
+    const int hn = slab_hn(P.rank, D.H0, P.world);
+    D.comm_bytes_per_eval = 2.0 * 8.0 * (double)nz * D.P[1] * (D.H0 - hn) +
+                            2.0 * 8.0 * (double)(D.n[2] - nz) * D.P[1] * hn;
+    for (int p = 0; p < P.world; ++p)
+      for (int k = 0; k < 2; ++k)
+        D.comm_bytes_per_eval += plane_b * (P.gsend[k][2 * p + 1] + P.grecv[k][2 * p + 1]);
+  } else {
+    D.comm_bytes_per_eval = 2.0 * 4.0 * (double)D.n[0] * D.n[1] * D.n[2] * (P.world - 1) / P.world;
+  }
   for (int k = 0; k < 3; ++k) {
     D.send_ptr[k] = P.send_ptr[k];
     D.recv_ptr[k] = P.recv_ptr[k];
@@ -1159,13 +1193,18 @@ void halo(DeviceState& D, int k, float* v, int w, cudaStream_t st) {
   }
 }
 
-// ---- slab-decomposed FFT convolution; D.slab_world > 1
+// ---- slab-decomposed FFT convolution; D.slab_world > 1.  Rank r owns the z planes
+// [Z_r, Z_r+1) (D.zpl, variable thickness) for the X and Y passes and the k0 columns
+// [h_r, h_r + H_r) for the Z pass; block (r -> p) = Cz_r[:, :, h_p : h_p + H_p] packed as
+// [nz_r][P1][H_p] lands in Cx_p at plane offset Z_r (contiguous).
 // per-rank phases, shared by the NCCL path and the single-device simulation (PMFEM_SLAB_SIM)
-void slab_phase_fwd(const DeviceState& D, const float* Qs, float2* Cz, float2* sbuf, int W, cudaStream_t st) {
-  const int n0 = D.n[0], n1 = D.n[1], nzl = D.n[2] / W, P0 = D.P[0], P1 = D.P[1], H0 = D.H0;
-  launch_x<float>(true, Qs, Cz, nullptr, nzl * n1, n0, P0, n1, P1, D.tw32[0], st);
-  launch_strided<float>(Cz, P1, H0, H0, nzl, (long long)P1 * H0, n1, P1, 0, nullptr, 0, 0, D.tw32[1], st);
-  const int64_t rows = (int64_t)nzl * P1;
+void slab_phase_fwd(const DeviceState& D, int r, const float* Qs, float2* Cz, float2* sbuf, cudaStream_t st) {
+  const int W = D.slab_world, n0 = D.n[0], n1 = D.n[1], nz = D.zpl[r + 1] - D.zpl[r], P0 = D.P[0], P1 = D.P[1],
+            H0 = D.H0;
+  if (nz == 0) return;
+  launch_x<float>(true, Qs, Cz, nullptr, nz * n1, n0, P0, n1, P1, D.tw32[0], st);
+  launch_strided<float>(Cz, P1, H0, H0, nz, (long long)P1 * H0, n1, P1, 0, nullptr, 0, 0, D.tw32[1], st);
+  const int64_t rows = (int64_t)nz * P1;
   k_slab_pack<<<dim3((unsigned)std::min<int64_t>(1024, (rows * (H0 / W + 1) + 255) / 256), W), 256, 0, st>>>(Cz, sbuf, rows, H0, W, 0);
   CK(cudaGetLastError());
 }
@@ -1174,65 +1213,81 @@ void slab_phase_z(const DeviceState& D, float2* Cx, const float* spec_r, int Hr,
   launch_strided<float>(Cx, D.P[2], (long long)P1 * Hr, Hr, P1, Hr, D.n[2], D.n[2], 2, spec_r, (long long)P1 * Hr, Hr,
                         D.tw32[2], st);
 }
-void slab_phase_inv(const DeviceState& D, float2* rbuf, float2* Cz, float* Us, int W, cudaStream_t st) {
-  const int n0 = D.n[0], n1 = D.n[1], nzl = D.n[2] / W, P0 = D.P[0], P1 = D.P[1], H0 = D.H0;
-  const int64_t rows = (int64_t)nzl * P1;
+void slab_phase_inv(const DeviceState& D, int r, float2* rbuf, float2* Cz, float* Us, cudaStream_t st) {
+  const int W = D.slab_world, n0 = D.n[0], n1 = D.n[1], nz = D.zpl[r + 1] - D.zpl[r], P0 = D.P[0], P1 = D.P[1],
+            H0 = D.H0;
+  if (nz == 0) return;
+  const int64_t rows = (int64_t)nz * P1;
   k_slab_pack<<<dim3((unsigned)std::min<int64_t>(1024, (rows * (H0 / W + 1) + 255) / 256), W), 256, 0, st>>>(Cz, rbuf, rows, H0, W, 1);
   CK(cudaGetLastError());
-  launch_strided<float>(Cz, P1, H0, H0, nzl, (long long)P1 * H0, P1, n1, 1, nullptr, 0, 0, D.tw32[1], st);
-  launch_x<float>(false, nullptr, Cz, Us, nzl * n1, n0, P0, n1, P1, D.tw32[0], st);
+  launch_strided<float>(Cz, P1, H0, H0, nz, (long long)P1 * H0, P1, n1, 1, nullptr, 0, 0, D.tw32[1], st);
+  launch_x<float>(false, nullptr, Cz, Us, nz * n1, n0, P0, n1, P1, D.tw32[0], st);
 }
 
-// NCCL path: Q holds this rank's partial anterpolation on the full grid; on return Q holds
-// the full U on every rank.  reduce-scatter (z slabs) -> X, Y -> all-to-all -> Z*G -> all-to-all
-// -> Y', X' -> all-gather.
+// NCCL path: Q holds this rank's z planes [Z_r, Z_r+1) of the anterpolated grid (K2 computed
+// them completely from own + halo rows: no reduction); on return Q holds U on those planes.
+// X, Y -> all-to-all -> Z*G -> all-to-all -> Y', X'.
 void slab_conv_nccl(DeviceState& D, cudaStream_t st) {
   const int W = D.world, r = D.rank, H0 = D.H0, P1 = D.P[1];
-  const int nzl = D.n[2] / W;
-  const size_t slab = (size_t)nzl * D.n[1] * D.n[0];
+  const size_t plane = (size_t)D.n[1] * D.n[0];
   ncclComm_t comm = (ncclComm_t)D.comm;
-  NCK(ncclReduceScatter(D.Q, D.Q + r * slab, slab, ncclFloat, ncclSum, comm, st));
-  slab_phase_fwd(D, D.Q + r * slab, D.C, D.slab_buf, W, st);
+  float* Qr = D.Q + (size_t)D.zpl[r] * plane;
+  slab_phase_fwd(D, r, Qr, D.C, D.slab_buf, st);
   const int Hr = slab_hn(r, H0, W);
-  const int64_t rows = (int64_t)nzl * P1;
+  const int64_t rows_r = (int64_t)(D.zpl[r + 1] - D.zpl[r]) * P1;
   NCK(ncclGroupStart());
   for (int p = 0; p < W; ++p) {
     if (p == r) continue;
-    NCK(ncclSend(D.slab_buf + rows * slab_h0(p, H0, W), (size_t)(rows * slab_hn(p, H0, W) * 2), ncclFloat, p, comm, st));
-    NCK(ncclRecv(D.slab_cx + (int64_t)p * rows * Hr, (size_t)(rows * Hr * 2), ncclFloat, p, comm, st));
+    const int64_t rows_p = (int64_t)(D.zpl[p + 1] - D.zpl[p]) * P1;
+    if (rows_r) NCK(ncclSend(D.slab_buf + rows_r * slab_h0(p, H0, W), (size_t)(rows_r * slab_hn(p, H0, W) * 2), ncclFloat, p, comm, st));
+    if (rows_p) NCK(ncclRecv(D.slab_cx + (int64_t)D.zpl[p] * P1 * Hr, (size_t)(rows_p * Hr * 2), ncclFloat, p, comm, st));
   }
   NCK(ncclGroupEnd());
-  CK(cudaMemcpyAsync(D.slab_cx + (int64_t)r * rows * Hr, D.slab_buf + rows * slab_h0(r, H0, W),
-                     sizeof(float2) * rows * Hr, cudaMemcpyDeviceToDevice, st));
+  if (rows_r)
+    CK(cudaMemcpyAsync(D.slab_cx + (int64_t)D.zpl[r] * P1 * Hr, D.slab_buf + rows_r * slab_h0(r, H0, W),
+                       sizeof(float2) * rows_r * Hr, cudaMemcpyDeviceToDevice, st));
   slab_phase_z(D, D.slab_cx, D.slab_spec, Hr, st);
   NCK(ncclGroupStart());
   for (int p = 0; p < W; ++p) {
     if (p == r) continue;
-    NCK(ncclSend(D.slab_cx + (int64_t)p * rows * Hr, (size_t)(rows * Hr * 2), ncclFloat, p, comm, st));
-    NCK(ncclRecv(D.slab_buf + rows * slab_h0(p, H0, W), (size_t)(rows * slab_hn(p, H0, W) * 2), ncclFloat, p, comm, st));
+    const int64_t rows_p = (int64_t)(D.zpl[p + 1] - D.zpl[p]) * P1;
+    if (rows_p) NCK(ncclSend(D.slab_cx + (int64_t)D.zpl[p] * P1 * Hr, (size_t)(rows_p * Hr * 2), ncclFloat, p, comm, st));
+    if (rows_r) NCK(ncclRecv(D.slab_buf + rows_r * slab_h0(p, H0, W), (size_t)(rows_r * slab_hn(p, H0, W) * 2), ncclFloat, p, comm, st));
   }
   NCK(ncclGroupEnd());
-  CK(cudaMemcpyAsync(D.slab_buf + rows * slab_h0(r, H0, W), D.slab_cx + (int64_t)r * rows * Hr,
-                     sizeof(float2) * rows * Hr, cudaMemcpyDeviceToDevice, st));
-  slab_phase_inv(D, D.slab_buf, D.C, D.Q + r * slab, W, st);
-  NCK(ncclAllGather(D.Q + r * slab, D.Q, slab, ncclFloat, comm, st));
+  if (rows_r)
+    CK(cudaMemcpyAsync(D.slab_buf + rows_r * slab_h0(r, H0, W), D.slab_cx + (int64_t)D.zpl[r] * P1 * Hr,
+                       sizeof(float2) * rows_r * Hr, cudaMemcpyDeviceToDevice, st));
+  slab_phase_inv(D, r, D.slab_buf, D.C, Qr, st);
+  // U ghost planes: K4's stencils read p planes above the slab (DistPlan gsend / grecv)
+  NCK(ncclGroupStart());
+  for (int p = 0; p < W; ++p)
+    for (int k = 0; k < 2; ++k) {
+      const int sz0 = D.gsend[k][2 * p], sn = D.gsend[k][2 * p + 1];
+      const int rz0 = D.grecv[k][2 * p], rn = D.grecv[k][2 * p + 1];
+      if (sn) NCK(ncclSend(D.Q + (size_t)sz0 * plane, (size_t)sn * plane, ncclFloat, p, comm, st));
+      if (rn) NCK(ncclRecv(D.Q + (size_t)rz0 * plane, (size_t)rn * plane, ncclFloat, p, comm, st));
+    }
+  NCK(ncclGroupEnd());
 }
 
 // The same decomposition with W simulated ranks on this device (test mode, PMFEM_SLAB_SIM=W):
-// every rank's phase runs in turn and the transposes are device copies of exactly the blocks
-// the NCCL path sends.  Q holds the full anterpolated grid (= the reduce-scatter result of
-// every rank); each rank's U slab lands in place (= the all-gather result).
+// every rank's phase runs in turn and the transposes are device copies of exactly the blocks the
+// NCCL path sends.  Q holds the full anterpolated grid; each rank's U planes land in place.
 void slab_conv_sim(DeviceState& D, cudaStream_t st) {
   const int W = D.slab_world, H0 = D.H0, P1 = D.P[1], P2 = D.P[2];
-  const int nzl = D.n[2] / W;
-  const size_t slab = (size_t)nzl * D.n[1] * D.n[0];
-  const int64_t rows = (int64_t)nzl * P1;
-  for (int r = 0; r < W; ++r) slab_phase_fwd(D, D.Q + r * slab, D.C + (int64_t)r * rows * H0, D.slab_buf + (int64_t)r * rows * H0, W, st);
+  const size_t plane = (size_t)D.n[1] * D.n[0];
+  // rank r's z-slab blocks live at plane offset Z_r of C / slab_buf ([n2][P1][H0] in total)
+  auto rows_of = [&](int r) { return (int64_t)(D.zpl[r + 1] - D.zpl[r]) * P1; };
+  auto off = [&](int r) { return (int64_t)D.zpl[r] * P1 * H0; };
+  for (int r = 0; r < W; ++r) slab_phase_fwd(D, r, D.Q + D.zpl[r] * plane, D.C + off(r), D.slab_buf + off(r), st);
   for (int r = 0; r < W; ++r)
     for (int p = 0; p < W; ++p) {
       const int64_t hp = slab_h0(p, H0, W), np = slab_hn(p, H0, W);
-      CK(cudaMemcpyAsync(D.slab_cx + (int64_t)P2 * P1 * hp + r * rows * np, D.slab_buf + (int64_t)r * rows * H0 + rows * hp,
-                         sizeof(float2) * rows * np, cudaMemcpyDeviceToDevice, st));
+      if (rows_of(r))
+        CK(cudaMemcpyAsync(D.slab_cx + (int64_t)P2 * P1 * hp + (int64_t)D.zpl[r] * P1 * np,
+                           D.slab_buf + off(r) + rows_of(r) * hp, sizeof(float2) * rows_of(r) * np,
+                           cudaMemcpyDeviceToDevice, st));
     }
   for (int p = 0; p < W; ++p) {
     const int64_t hp = slab_h0(p, H0, W);
@@ -1241,19 +1296,23 @@ void slab_conv_sim(DeviceState& D, cudaStream_t st) {
   for (int r = 0; r < W; ++r)
     for (int p = 0; p < W; ++p) {
       const int64_t hp = slab_h0(p, H0, W), np = slab_hn(p, H0, W);
-      CK(cudaMemcpyAsync(D.slab_buf + (int64_t)r * rows * H0 + rows * hp, D.slab_cx + (int64_t)P2 * P1 * hp + r * rows * np,
-                         sizeof(float2) * rows * np, cudaMemcpyDeviceToDevice, st));
+      if (rows_of(r))
+        CK(cudaMemcpyAsync(D.slab_buf + off(r) + rows_of(r) * hp,
+                           D.slab_cx + (int64_t)P2 * P1 * hp + (int64_t)D.zpl[r] * P1 * np,
+                           sizeof(float2) * rows_of(r) * np, cudaMemcpyDeviceToDevice, st));
     }
-  for (int r = 0; r < W; ++r) slab_phase_inv(D, D.slab_buf + (int64_t)r * rows * H0, D.C + (int64_t)r * rows * H0, D.Q + r * slab, W, st);
+  for (int r = 0; r < W; ++r) slab_phase_inv(D, r, D.slab_buf + off(r), D.C + off(r), D.Q + D.zpl[r] * plane, st);
 }
 }  // namespace
 
 // m, H: [hi-lo][3] rank-local rows (the full [N'][3] on a single GPU)
 void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, EvalMode mode) {
-  const RowRange rr{D.lo, D.hi, D.lo};
+  const RowRange rr{D.lo, D.hi, D.lo, D.axperm[0], D.axperm[1], D.axperm[2]};
   const int64_t nrows = D.hi - D.lo;
-  if (nrows <= 0) return;
-  const unsigned thr_blocks = (unsigned)((nrows + 255) / 256);   // thread per row
+  // a rank without rows (thin slab) still takes part in every collective: only its row kernels
+  // are skipped (launch grids of zero blocks are invalid)
+  if (nrows <= 0 && D.world == 1) return;
+  const unsigned thr_blocks = (unsigned)std::max<int64_t>(1, (nrows + 255) / 256);   // thread per row
   // external records: inside a captured graph a plain cudaEventRecord would only become an
   // internal dependency, not a timestamp readable with cudaEventElapsedTime
   auto mark = [&](int i) { if (D.timing) CK(cudaEventRecordWithFlags(D.ev[i], st, cudaEventRecordExternal)); };
@@ -1270,7 +1329,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   GridDims g{D.n[0], D.n[1], D.n[2], D.periodic[0], D.periodic[1], D.periodic[2]};
   // two threads per row when the rows alone cannot fill the GPU (PMFEM_ROW_SPLIT=1|2 overrides)
   const bool split = D.row_split == 2;
-  const unsigned split_blocks = (unsigned)((2 * ((nrows + 31) / 32 * 32) + 255) / 256);
+  const unsigned split_blocks = (unsigned)std::max<int64_t>(1, (2 * ((nrows + 31) / 32 * 32) + 255) / 256);
   if (split)
     k1_local_in<2><<<split_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.rowsum, D.q, D.uloc, H,
                                                  mode == EVAL_HEFF ? 1 : 0);
@@ -1278,16 +1337,24 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     k1_local_in<1><<<thr_blocks, 256, 0, st>>>(rr, D.m4, D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.rowsum, D.q, D.uloc, H,
                                                mode == EVAL_HEFF ? 1 : 0);
   CK(cudaGetLastError());
+  // q of the rows anchored in the planes bordering the own slab (K2's stencils, C_box columns)
+  halo(D, 1, D.q, 1, st);
   mark(1);
   const size_t G = (size_t)D.n[0] * D.n[1] * D.n[2];
   {
+    // slab NCCL path: tiles of the own z planes only, reading own + halo rows (no row clip, no
+    // reduction); otherwise tiles of the whole grid over the rows [lo, hi)
+    const bool own_planes = D.world > 1 && D.slab_world > 1;
     const TileDims td{D.k2_tile[0], D.k2_tile[1], D.k2_tile[2]};
-    const unsigned nt = (unsigned)(G / ((size_t)td.t0 * td.t1 * td.t2));
+    const int z0p = own_planes ? D.zpl[D.rank] : 0, z1p = own_planes ? D.zpl[D.rank + 1] : D.n[2];
+    const unsigned nt = (unsigned)(((size_t)D.n[0] / td.t0) * (D.n[1] / td.t1) * ((z1p - z0p) / td.t2));
+    const int64_t klo = own_planes ? 0 : D.lo, khi = own_planes ? D.Np : D.hi;
     const size_t smem = sizeof(int) * ((size_t)3 * td.t0 * td.t1 * td.t2 + 2 * k2_nseg(td.t1, td.t2, D.order) + 1);
 #define K2_LAUNCH(PP)                                                                                 \
   do {                                                                                                \
     CK(cudaFuncSetAttribute(k2_tile<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
-    k2_tile<PP><<<nt, 256, smem, st>>>(g, td, D.box_ptr, D.st_s, D.st_t, D.q, D.lo, D.hi, D.box_max, D.Q); \
+    if (nt) k2_tile<PP><<<nt, 256, smem, st>>>(g, td, D.box_ptr, D.st_s, D.st_t, D.q, klo, khi, D.box_max, \
+                                               z0p / td.t2, D.Q);                                    \
   } while (0)
     switch (D.order) {
       case 1: K2_LAUNCH(1); break;
@@ -1315,7 +1382,6 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     }
     launch_x<float>(false, nullptr, D.C, D.Q, n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
   }
-  halo(D, 1, D.q, 1, st);
   mark(3);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   if (D.cbox_format == 3) {
@@ -1325,7 +1391,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   if (D.cbox_format == 2) {
     const int G = D.k4_group;
     const size_t smem = sizeof(int) * (size_t)(256 / G) * (2 * D.seg_maxseg + 2);
-    const unsigned blocks = (unsigned)((nrows * G + 255) / 256);
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, (nrows * G + 255) / 256);
 #define K4S_LAUNCH(PP, GG)                                                                                 \
   do {                                                                                                     \
     CK(cudaFuncSetAttribute(k4_seg<PP, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
@@ -1345,16 +1411,16 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
   (D.cbox_format == 3                                                                                   \
-       ? k4_interp_corr<PP, GG, 3><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+       ? k4_interp_corr<PP, GG, 3><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4,                                \
              reinterpret_cast<const float*>(D.q4), D.uloc, D.u)                                         \
    : D.cbox_format == 1                                                                                 \
-       ? k4_interp_corr<PP, GG, 1><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+       ? k4_interp_corr<PP, GG, 1><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
    : D.k4_vec                                                                                           \
-       ? k4_interp_corr<PP, GG, 2><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+       ? k4_interp_corr<PP, GG, 2><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
-       : k4_interp_corr<PP, GG, 0><<<(unsigned)((nrows * GG + 255) / 256), 256, 0, st>>>(                \
+       : k4_interp_corr<PP, GG, 0><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u))
 #define K4_BY_G(PP)                                                                                     \
   (D.k4_group == 8 ? K4_LAUNCH(PP, 8) : D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
@@ -1382,11 +1448,11 @@ namespace pmfem {
 void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
                          const double Hap[3]) {
   const int64_t n = D.hi - D.lo;
-  if (n <= 0) return;
+  if (n <= 0 && D.world == 1) return;     // a row-less rank still joins the evaluations' collectives
   if (!D.llg_ms) {
-    D.llg_ms = dalloc<float>(3 * (size_t)n);
-    D.llg_H = dalloc<float>(3 * (size_t)n);
-    D.llg_acc = dalloc<float>(3 * (size_t)n);
+    D.llg_ms = dalloc<float>(3 * (size_t)std::max<int64_t>(n, 1));
+    D.llg_H = dalloc<float>(3 * (size_t)std::max<int64_t>(n, 1));
+    D.llg_acc = dalloc<float>(3 * (size_t)std::max<int64_t>(n, 1));
   }
   const float g = (float)(gamma / (1.0 + alpha * alpha));
   const unsigned blocks = (unsigned)((n + 255) / 256);
@@ -1395,6 +1461,7 @@ void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, d
   for (int s = 0; s < 4; ++s) {
     const float* ms = (s == 0) ? m : D.llg_ms;
     device_eval(D, ms, D.llg_H, st, EVAL_HEFF);
+    if (n > 0)
     k_llg_stage<<<blocks, 256, 0, st>>>(n, m, ms, D.llg_H, (float)Hap[0], (float)Hap[1], (float)Hap[2], g,
                                         (float)alpha, w[s], c[s], D.llg_acc, D.llg_ms, s == 0, s == 3);
     CK(cudaGetLastError());

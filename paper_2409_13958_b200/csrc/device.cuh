@@ -112,6 +112,9 @@ struct DeviceState {
   float* m_stage = nullptr;   // pmfem_heff_host staging
   // slab-decomposed convolution (world > 1, or PMFEM_SLAB_SIM=W simulated ranks on one device)
   int slab_world = 1;
+  std::vector<int> zpl;       // [slab_world+1] z-slab plane boundaries (variable thickness; the
+                              // row partition's planes on N > 1, the same rule for the simulation)
+  std::vector<int32_t> gsend[2], grecv[2];   // U ghost planes per peer (DistPlan)
   float2* slab_cx = nullptr;  // x-slab spectrum [P2][P1][H_r] (simulation: all ranks back to back)
   float2* slab_buf = nullptr; // transpose send / receive blocks [nzl][P1][H0]
   float* slab_spec = nullptr; // spectrum slice [P2][P1][H_r]
@@ -127,6 +130,7 @@ struct DeviceState {
   // full length (global column indices) and filled at owned + halo rows; the anterpolated
   // grid is all-reduced and the FFT convolution is replicated on every rank.
   int rank = 0, world = 1;
+  int axperm[3] = {0, 1, 2};  // user axis of internal axis i (m / H components are permuted)
   int64_t lo = 0, hi = 0;
   void* comm = nullptr;                         // ncclComm_t
   std::vector<int64_t> send_ptr[3], recv_ptr[3];

@@ -79,6 +79,41 @@ static pmfem_status setup_impl(pmfem_ctx* out, const pmfem_mesh* mesh, const pmf
       }
     };
     pmfem::HostSetup& S = ctx->S;
+    pmfem::require(grid != nullptr && mesh != nullptr && per != nullptr, PMFEM_E_INVALID_ARG, "NULL argument");
+    // axis permutation: on N > 1 the slab axis -- the longest grid axis, z on ties --
+    // becomes the internal z (slowest) axis, so thin films and wires split along their length;
+    // PMFEM_AXIS_PERM=a,b,c forces one (tests run permuted frames on one GPU).  The setup then
+    // runs on permuted copies of the coordinates, periodicity and grid.
+    int ap[3] = {0, 1, 2};
+    if (world > 1) {
+      int sa = 2;
+      for (int a = 1; a >= 0; --a)
+        if (grid->n[a] > grid->n[sa]) sa = a;
+      if (sa != 2) { ap[sa] = 2; ap[2] = sa; }
+    }
+    if (const char* e = std::getenv("PMFEM_AXIS_PERM")) {
+      int a0, a1, a2;
+      if (std::sscanf(e, "%d,%d,%d", &a0, &a1, &a2) == 3 && a0 + a1 + a2 == 3 && a0 != a1 && a1 != a2 && a0 != a2 &&
+          a0 >= 0 && a1 >= 0 && a2 >= 0 && a0 < 3 && a1 < 3 && a2 < 3) { ap[0] = a0; ap[1] = a1; ap[2] = a2; }
+    }
+    std::vector<double> xyz_p;
+    pmfem_mesh mesh_p = *mesh;
+    pmfem_periodicity per_p = *per;
+    pmfem_grid grid_p = *grid;
+    if (!(ap[0] == 0 && ap[1] == 1 && ap[2] == 2)) {
+      pmfem::require(mesh->xyz != nullptr && mesh->n_nodes >= 0, PMFEM_E_INVALID_ARG, "NULL coordinates");
+      xyz_p.resize(3 * (size_t)mesh->n_nodes);
+      for (int64_t i = 0; i < mesh->n_nodes; ++i)
+        for (int a = 0; a < 3; ++a) xyz_p[3 * i + a] = mesh->xyz[3 * i + ap[a]];
+      mesh_p.xyz = xyz_p.data();
+      for (int a = 0; a < 3; ++a) {
+        per_p.periodic[a] = per->periodic[ap[a]];
+        grid_p.n[a] = grid->n[ap[a]];
+        for (int b = 0; b < 3; ++b) per_p.lattice[a][b] = per->lattice[ap[a]][ap[b]];
+      }
+      mesh = &mesh_p; per = &per_p; grid = &grid_p;
+    }
+    for (int a = 0; a < 3; ++a) S.axperm[a] = ap[a];
     pmfem::setup_mesh(S, mesh, per);
     stage("mesh/pbc");
     pmfem::setup_operators(S);
@@ -87,14 +122,16 @@ static pmfem_status setup_impl(pmfem_ctx* out, const pmfem_mesh* mesh, const pmf
     pmfem::require(grid != nullptr, PMFEM_E_INVALID_ARG, "NULL grid");
     pmfem::require(grid->z0_ring == 0 || grid->z0_ring == 1, PMFEM_E_INVALID_ARG, "z0_ring must be 0 or 1");
     S.z0_device = cuda_device;            // device contexts integrate Z0 on the GPU
-    pmfem::setup_z0(S);
-    stage("z0");
     S.cbox_device = cuda_device >= 0;     // device contexts build C_box on the GPU
     pmfem::setup_aim(S, grid);
     stage("aim");
     pmfem::setup_order(S);
-    pmfem::setup_dist(S, rank, world);
+    pmfem::setup_dist(S, rank, world);    // slab partition; a rank builds Z0 for its own rows
     stage("order/dist");
+    pmfem::setup_z0(S);
+    stage("z0");
+    pmfem::setup_dist_halos(S);
+    stage("halos");
     S.setup_seconds = now() - t0;
     if (cuda_device >= 0) {
       ctx->host_only = false;
@@ -366,6 +403,27 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     else if (n == "grid_origin") put(S.origin, 3, 8);
     else if (n == "perm") put(S.perm.data(), S.Np, 8);
     else if (n == "dist_bounds") put(S.dist.bounds.data(), (int64_t)S.dist.bounds.size(), 8);
+    else if (n == "axis_perm") {
+      const int64_t a[3] = {S.axperm[0], S.axperm[1], S.axperm[2]};
+      put(a, 3, 8);
+    }
+    else if (n == "dist_planes") {
+      // z-slab plane boundaries [world+1] of the row partition = the FFT's z slabs
+      std::vector<int64_t> z(S.dist.planes.begin(), S.dist.planes.end());
+      put(z.data(), (int64_t)z.size(), 8);
+    }
+    else if (n == "dist_ghost") {
+      // U ghost planes per peer: [world][send r0 (z0, n), send r1, recv r0, recv r1] (8 values)
+      const int W = S.dist.world;
+      std::vector<int64_t> g(8 * W, 0);
+      if (W > 1)
+        for (int p = 0; p < W; ++p)
+          for (int k = 0; k < 2; ++k) {
+            g[8 * p + 2 * k] = S.dist.gsend[k][2 * p]; g[8 * p + 2 * k + 1] = S.dist.gsend[k][2 * p + 1];
+            g[8 * p + 4 + 2 * k] = S.dist.grecv[k][2 * p]; g[8 * p + 4 + 2 * k + 1] = S.dist.grecv[k][2 * p + 1];
+          }
+      put(g.data(), (int64_t)g.size(), 8);
+    }
     else if (n == "slab_kranges") {
       // per rank (first k0 column, count) of the slab-decomposed FFT's x slabs, world = this
       // context's world (the z slabs are n2 / world planes each)
@@ -380,13 +438,14 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
       // empty slots are the block's other columns with value 0)
       pmfem::require(!ctx->host_only && S.cbox_device, PMFEM_E_STATE, "C_box was not built on the device");
       const pmfem::DeviceState& D = ctx->D;
-      std::vector<int64_t> ptr(S.Np + 1);
-      cudaMemcpy(ptr.data(), D.c_ptr, sizeof(int64_t) * (S.Np + 1), cudaMemcpyDeviceToHost);
+      const int64_t nr = D.hi - D.lo;                // the rank's own rows
+      std::vector<int64_t> ptr(nr + 1);
+      cudaMemcpy(ptr.data(), D.c_ptr, sizeof(int64_t) * (nr + 1), cudaMemcpyDeviceToHost);
       const std::string tail = n.substr(12);
-      const int64_t nch = ptr[S.Np];
+      const int64_t nch = ptr[nr];
       if (D.cbox_format == 2 && (tail == "rowptr" || tail == "col" || tail == "val")) {
         // SEG: value offsets, the near columns decoded from the candidate bitmasks, the values
-        if (tail == "rowptr") put(ptr.data(), S.Np + 1, 8);
+        if (tail == "rowptr") put(ptr.data(), nr + 1, 8);
         else {
           *count = nch;
           if (dst && nch) {
@@ -404,7 +463,7 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
         }
       } else if (tail == "rowptr") {
         for (auto& v : ptr) v *= 4;
-        put(ptr.data(), S.Np + 1, 8);
+        put(ptr.data(), nr + 1, 8);
       } else if (tail == "val") {
         *count = 4 * nch;
         if (dst && nch) cudaMemcpy(dst, D.c_val, sizeof(float) * 4 * (size_t)nch, cudaMemcpyDeviceToHost);

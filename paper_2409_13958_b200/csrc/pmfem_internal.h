@@ -31,6 +31,7 @@ struct Csr {
 struct Z0Item {
   int64_t row;        // observer parent n
   int32_t tet;        // element id
+  int32_t slot;       // position of row n in the integration chunk (value block)
   int16_t code;       // packed lattice shift of the element image
   int8_t va;          // local vertex that coincides with the observer, or -1
   uint8_t flags;      // bit j: local vertex j is a near source of row n
@@ -42,6 +43,13 @@ struct Z0Item {
 struct DistPlan {
   int rank = 0, world = 1;
   std::vector<int64_t> bounds{0, 0};           // [world+1] internal row boundaries
+  std::vector<int32_t> planes{0, 0};           // [world+1] slab boundaries (anchor z planes) of the
+                                               // rows = the FFT's z slabs
+  int qband_lo = 0, qband_hi = 0;              // q halo: rows anchored within these many planes
+                                               // below / above the own slab (K2 stencils, C_box)
+  // U ghost planes (K4's stencils reach p planes above the own slab): per peer, the contiguous
+  // plane ranges (first plane, count) to send / receive; up to 2 ranges per peer (z wrap)
+  std::vector<int32_t> gsend[2], grecv[2];     // [world] x (plane0, count) for range 0 / 1
   std::vector<int64_t> send_ptr[3], recv_ptr[3];  // [world+1] per peer
   std::vector<int32_t> send_idx[3], recv_idx[3];  // my rows to send / peer rows to receive
   int64_t lo() const { return bounds[rank]; }
@@ -58,6 +66,9 @@ struct HostSetup {
   int periodic[3] = {0, 0, 0};
   double L[3] = {0, 0, 0};
   double match_tol = 0;
+  int axperm[3] = {0, 1, 2};        // internal axis i = user axis axperm[i] (N > 1: the slab axis,
+                                    // the longest grid axis, becomes internal z); every setup
+                                    // artifact is in the internal frame, m / H in the user frame
   int touching = 0, protruding = 0;
   // PBC / LCA
   int64_t Np = 0;
@@ -86,6 +97,7 @@ struct HostSetup {
   double rer_scale = 2.0;
   int z0_ring = 1;
   int z0_device = -1;               // >= 0: Z0 element integrals run on this CUDA device
+  std::vector<int64_t> z0_rows;     // rows (user parent ids) whose Z0 is built; empty = all rows
   std::vector<double> xw;           // [Np][3] wrapped parent coordinates
   std::vector<int32_t> st_s;        // [Np][3] unwrapped stencil start index
   std::vector<double> st_t;         // [Np][3] t - s (local coordinate in grid units)
@@ -107,13 +119,18 @@ void setup_operators(HostSetup& S);
 void setup_z0(HostSetup& S);
 void setup_aim(HostSetup& S, const pmfem_grid* g);
 void setup_order(HostSetup& S);
-void setup_dist(HostSetup& S, int rank, int world);
+void setup_dist(HostSetup& S, int rank, int world);          // partition (needs setup_order)
+void setup_dist_halos(HostSetup& S);                         // halo lists (needs Z0 of the own rows)
+// slab boundaries (anchor z planes, multiples of gz) balancing the internal rows over `world`
+// ranks; shared with the single-device slab simulation
+std::vector<int32_t> slab_planes(const HostSetup& S, int world, int gz);
+int slab_granularity(const HostSetup& S, int world);
 struct TriRules;
 void z0_device_begin(const HostSetup& S, const TriRules& rules);
 void z0_device_end(std::vector<std::vector<double>>& rval);
 void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& items,
                          const std::vector<std::vector<int32_t>>& rcol, std::vector<std::vector<double>>& rval,
-                         const TriRules& rules, int64_t r0, int64_t r1);
+                         const TriRules& rules, const int64_t* rows, int64_t nrows);
 
 // Periodic Green's function (Ewald) -- host/device fp64, defined in pgf.cuh.
 struct PgfParams {

@@ -79,6 +79,14 @@ void setup_z0(HostSetup& S) {
   S.rowsumZ.assign(3 * Np, 0.0);
   const bool on_device = S.z0_device >= 0;
   const int64_t chunk = on_device ? 250000 : Np;
+  // rows to integrate (user parent ids): all, or a rank's own rows (distributed device contexts)
+  std::vector<int64_t> rows_all;
+  if (S.z0_rows.empty()) {
+    rows_all.resize(Np);
+    for (int64_t n = 0; n < Np; ++n) rows_all[n] = n;
+  }
+  const std::vector<int64_t>& rows = S.z0_rows.empty() ? rows_all : S.z0_rows;
+  const int64_t nrows_tot = (int64_t)rows.size();
   std::string err;
   const bool verbose = std::getenv("PMFEM_VERBOSE") != nullptr;
   if (on_device) z0_device_begin(S, rules);
@@ -87,9 +95,9 @@ void setup_z0(HostSetup& S) {
     bool on; std::vector<std::vector<double>>* rv;
     ~PipeGuard() { if (on) { try { z0_device_end(*rv); } catch (...) {} } }
   } guard_pipe{on_device, &rval};
-  for (int64_t c0 = 0; c0 < Np && err.empty(); c0 += chunk) {
+  for (int64_t c0 = 0; c0 < nrows_tot && err.empty(); c0 += chunk) {
     const double t_chunk = omp_get_wtime();
-    const int64_t c1 = std::min(Np, c0 + chunk);
+    const int64_t c1 = std::min(nrows_tot, c0 + chunk);
     long long host_pts = 0;
     std::vector<std::vector<Z0Item>> titems(omp_get_max_threads());
 #pragma omp parallel reduction(+ : host_pts)
@@ -99,7 +107,8 @@ void setup_z0(HostSetup& S) {
       RowWork W;
       std::vector<Z0Item>& items = titems[omp_get_thread_num()];
 #pragma omp for schedule(dynamic, 16)
-      for (int64_t n = c0; n < c1; ++n) {
+      for (int64_t j = c0; j < c1; ++j) {
+        const int64_t n = rows[j];
         try {
           auto& near = W.near;
           auto& U = W.U;
@@ -184,6 +193,7 @@ void setup_z0(HostSetup& S) {
             if (on_device) {
               Z0Item z;
               z.row = n;
+              z.slot = (int32_t)(j - c0);
               z.tet = (int32_t)t;
               z.code = (int16_t)(it.key % NC);
               z.va = (int8_t)it.va;
@@ -236,7 +246,7 @@ void setup_z0(HostSetup& S) {
       host_pts += I.npts;
     }
     const double t_enum = omp_get_wtime();
-    if (on_device && err.empty()) z0_device_integrate(S, titems, rcol, rval, rules, c0, c1);
+    if (on_device && err.empty()) z0_device_integrate(S, titems, rcol, rval, rules, rows.data() + c0, c1 - c0);
     if (verbose)
       std::fprintf(stderr, "[pmfem]   z0 rows %lld-%lld: enumerate %.2f s, integrate %.2f s (host quadrature points %lld)\n",
                    (long long)c0, (long long)c1, t_enum - t_chunk, omp_get_wtime() - t_enum, host_pts);

@@ -61,7 +61,7 @@ __global__ void k_z0_items(const Z0Item* __restrict__ items, int64_t nitems, con
   for (int x = 0; x < 3; ++x) I.o[x] = xyz[3 * pn + x];
   I.run(it.va);
   const double Ms = Ms_tet[it.tet];
-  double* v = vals + rowbase[it.row - r0];
+  double* v = vals + rowbase[it.slot];
   for (int k = 0; k < 4; ++k) {
     if (!(it.flags & (1u << k))) continue;
     for (int m = 0; m < 4; ++m)
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
     // B_km,x = -(a_k a_m T1_x + (a_k g_m + a_m g_k) . T2_(.x) / 2 + g_k^T T3_(..x) g_m / 3)
     // (the per-point formulas of ConeIntegrator::quad with phi(y) = a + g . (y - o), regrouped)
     const double Ms = Ms_tet[it.tet];
-    double* v = vals + rowbase[it.row - r0];
+    double* v = vals + rowbase[it.slot];
     for (int t = lane; t < 48; t += 32) {
       const int k = t / 12, m = (t / 3) % 4, x = t % 3;
       if (!(it.flags & (1u << k))) continue;
@@ -282,7 +282,7 @@ struct Z0Pipe {
   TriRules* rules = nullptr;
   struct Chunk {
     bool busy = false;
-    int64_t r0 = 0, r1 = 0;
+    std::vector<int64_t> rows;     // user parent ids of the chunk's rows
     std::vector<int64_t> rowbase;
     Z0Item* items = nullptr;
     int64_t* base = nullptr;
@@ -313,10 +313,10 @@ void z0_device_begin(const HostSetup& S, const TriRules& rules) {
 static void z0_finish_chunk(Z0Pipe::Chunk& c, std::vector<std::vector<double>>& rval) {
   if (!c.busy) return;
   CKZ(cudaEventSynchronize(c.done));
-  for (int64_t r = c.r0; r < c.r1; ++r) {
-    const double* src = c.hvals + c.rowbase[r - c.r0];
-    std::vector<double>& dst = rval[r];
-    for (size_t j = 0; j < dst.size(); ++j) dst[j] += src[j];
+  for (size_t j = 0; j < c.rows.size(); ++j) {
+    const double* src = c.hvals + c.rowbase[j];
+    std::vector<double>& dst = rval[c.rows[j]];
+    for (size_t e = 0; e < dst.size(); ++e) dst[e] += src[e];
   }
   cudaFree(c.items); cudaFree(c.base); cudaFree(c.vals);
   c.items = nullptr; c.base = nullptr; c.vals = nullptr;
@@ -325,7 +325,7 @@ static void z0_finish_chunk(Z0Pipe::Chunk& c, std::vector<std::vector<double>>& 
 
 void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& titems,
                          const std::vector<std::vector<int32_t>>& rcol, std::vector<std::vector<double>>& rval,
-                         const TriRules& rules, int64_t r0, int64_t r1) {
+                         const TriRules& rules, const int64_t* rows, int64_t nrows) {
   (void)rules;
   Z0Pipe& P = g_z0;
   CKZ(cudaSetDevice(P.dev));
@@ -336,10 +336,10 @@ void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& t
   for (auto& v : titems) tot += v.size();
   items.reserve(tot);
   for (auto& v : titems) { items.insert(items.end(), v.begin(), v.end()); std::vector<Z0Item>().swap(v); }
-  c.r0 = r0; c.r1 = r1;
-  c.rowbase.assign(r1 - r0 + 1, 0);
-  for (int64_t n = r0; n < r1; ++n) c.rowbase[n - r0 + 1] = c.rowbase[n - r0] + 3 * (int64_t)rcol[n].size();
-  const int64_t nvals = c.rowbase[r1 - r0];
+  c.rows.assign(rows, rows + nrows);
+  c.rowbase.assign(nrows + 1, 0);
+  for (int64_t j = 0; j < nrows; ++j) c.rowbase[j + 1] = c.rowbase[j] + 3 * (int64_t)rcol[rows[j]].size();
+  const int64_t nvals = c.rowbase[nrows];
   c.items = up(items.data(), items.size());
   c.base = up(c.rowbase.data(), c.rowbase.size());
   CKZ(cudaMalloc(&c.vals, std::max<int64_t>(nvals, 1) * sizeof(double)));
@@ -354,7 +354,7 @@ void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& t
   static const bool thread_per_task = std::getenv("PMFEM_Z0_THREAD") != nullptr;
   if (n && thread_per_task) {
     k_z0_items<<<(unsigned)((n + 127) / 128), 128, 0, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules,
-                                                               c.base, r0, c.vals);
+                                                               c.base, 0, c.vals);
     CKZ(cudaGetLastError());
   } else if (n) {
     const size_t smem = ((sizeof(TriRules) + 15) / 16) * 16 + Z0W_WARPS * sizeof(Z0Warp);
@@ -364,7 +364,7 @@ void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& t
     const int64_t want = (n + Z0W_WARPS - 1) / Z0W_WARPS;
     const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)nsm * 32);
     k_z0_warp<<<blocks, 32 * Z0W_WARPS, smem, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules, c.base,
-                                                       r0, c.vals);
+                                                       0, c.vals);
     CKZ(cudaGetLastError());
   }
   if (nvals) CKZ(cudaMemcpyAsync(c.hvals, c.vals, nvals * sizeof(double), cudaMemcpyDeviceToHost, P.st));

@@ -91,7 +91,8 @@ _EXPORT_DTYPES = {"parent": np.int64, "lca": np.int64, "shift": np.int32, "ring1
                   "cbox_col": np.int32, "stencil_s": np.int32, "perm": np.int64, "dist_bounds": np.int64}
 _EXPORT_DTYPES.update({"cbox_device_rowptr": np.int64, "cbox_device_col": np.int32,
                        "cbox_device_val": np.float32, "cbox_device_chunks": np.int64,
-                       "cbox_device_format": np.int64, "slab_kranges": np.int64})
+                       "cbox_device_format": np.int64, "slab_kranges": np.int64,
+                       "dist_planes": np.int64, "dist_ghost": np.int64, "axis_perm": np.int64})
 for _k in "mqu":
     _EXPORT_DTYPES["send_%s_ptr" % _k] = np.int64
     _EXPORT_DTYPES["recv_%s_ptr" % _k] = np.int64

@@ -1,9 +1,10 @@
 """Slab-decomposed FFT convolution on CPU with world_size-2 gloo processes:
-each rank holds its z slab (n2/W planes) of the anterpolated grid, transforms x and y,
-sends rank p the k0 columns the library assigns it (pmfem_export "slab_kranges"), transforms z,
+each rank holds its z slab of the anterpolated grid -- the planes [Z_r, Z_r+1) of the library's
+row partition (pmfem_export "dist_planes", variable thickness balancing the rows) -- transforms
+x and y, sends rank p the k0 columns the library assigns it ("slab_kranges"), transforms z,
 multiplies by the spectrum, transforms back, returns the blocks and finishes y and x -- the
-same block layout the NCCL path of device.cu sends ([nzl][P1][H_p] blocks landing at plane
-offset q*nzl of the receiver's [P2][P1][H_r] x slab).  The gathered result must equal the
+same block layout the NCCL path of device.cu sends ([nz_r][P1][H_p] blocks landing at plane
+offset Z_r of the receiver's [P2][P1][H_p] x slab).  The gathered result must equal the
 single-process FFT convolution (circular on periodic axes, zero-padded on the others)."""
 import os
 import socket
@@ -63,7 +64,7 @@ def _worker(rank, world, port, key, out):
     ctx = Context(m.xyz, m.tets, cfg["periodic"], cfg["lattice"], spec["grid"], Ms=cfg["Ms"], Aex=cfg["Aex"],
                   order=spec["order"], rer_scale=spec["s"], z0_ring=spec["ring"], device=-1, rank=rank,
                   world=world)
-    n0, n1, n2 = spec["grid"]
+    n0, n1, n2 = ctx.query()["grid"]                          # internal frame (slab axis = z)
     P = ctx.query()["fft"]
     P0, P1, P2 = P
     H0 = P0 // 2 + 1
@@ -72,25 +73,26 @@ def _worker(rank, world, port, key, out):
     rng = np.random.default_rng(5)
     Q = rng.standard_normal((n2, n1, n0))                      # [z][y][x], same on every rank
     G = rng.standard_normal((P2, P1, H0))                      # a real spectrum [k2][k1][k0]
-    nzl = n2 // world
+    Z = ctx.export("dist_planes")
+    assert Z[0] == 0 and Z[-1] == n2 and np.all(np.diff(Z) > 0)
     # z slab: X (real -> half spectrum, padded to P0) and Y (padded to P1)
-    Cz = np.fft.rfft(Q[rank * nzl:(rank + 1) * nzl], n=P0, axis=2)
+    Cz = np.fft.rfft(Q[Z[rank]:Z[rank + 1]], n=P0, axis=2)
     Cz = np.fft.fft(Cz, n=P1, axis=1)                          # [nzl][P1][H0]
     blocks = [Cz[:, :, kr[p, 0]:kr[p, 0] + kr[p, 1]] for p in range(world)]
     got = _alltoall(blocks, rank, world)
     h, hn = kr[rank]
-    Cx = np.zeros((P2, P1, hn), complex)                       # x slab: planes q*nzl from rank q
+    Cx = np.zeros((P2, P1, hn), complex)                       # x slab: planes Z_q.. from rank q
     for q in range(world):
-        Cx[q * nzl:(q + 1) * nzl] = got[q]
+        Cx[Z[q]:Z[q + 1]] = got[q]
     Cx = np.fft.ifft(np.fft.fft(Cx, axis=0) * G[:, :, h:h + hn], axis=0)
-    back = _alltoall([Cx[q * nzl:(q + 1) * nzl] for q in range(world)], rank, world)
+    back = _alltoall([Cx[Z[q]:Z[q + 1]] for q in range(world)], rank, world)
     for p in range(world):
         Cz[:, :, kr[p, 0]:kr[p, 0] + kr[p, 1]] = back[p]
     Us = np.fft.irfft(np.fft.ifft(Cz, axis=1)[:, :n1], n=P0, axis=2)[:, :, :n0]
     # reference on the full grid
     ref = np.fft.irfftn(np.fft.fftn(np.fft.rfft(Q, n=P0, axis=2), s=(P2, P1), axes=(0, 1)) * G,
                         s=(P2, P1, P0), axes=(0, 1, 2))[:, :n1, :n0]
-    out[rank] = float(np.abs(Us - ref[rank * nzl:(rank + 1) * nzl]).max() / np.abs(ref).max())
+    out[rank] = float(np.abs(Us - ref[Z[rank]:Z[rank + 1]]).max() / np.abs(ref).max())
     dist.destroy_process_group()
 
 

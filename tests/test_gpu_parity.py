@@ -259,3 +259,23 @@ def test_row_split(key, split, monkeypatch):
     m = m_random(om.n_parents, seed=81)
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
     assert rel_l2(_run(ctx, "exchange", m, rank), om.exchange(m)) <= TOL
+
+
+@pytest.mark.parametrize("key,perm", [("C2p2", "2,1,0"), ("C5p2", "2,1,0"), ("C5p2", "1,2,0"), ("R1p2", "0,2,1"),
+                                      ("C3p1", "1,2,0")])
+def test_axis_permutation(key, perm, monkeypatch):
+    """The internal axis permutation of distributed contexts (the slab axis -- the longest grid
+    axis -- becomes the internal z) forced on one GPU: the setup runs in the permuted
+    frame, m and H stay in the user frame, and the field equals the oracle's."""
+    monkeypatch.setenv("PMFEM_AXIS_PERM", perm)
+    om = oracle_model(key)
+    ctx = lib_context(key, device=0)
+    ctx.build_pgf()
+    assert ",".join(str(v) for v in ctx.export("axis_perm")) == perm
+    rank = ctx.internal_to_parent_rank()
+    m = m_random(om.n_parents, seed=91)
+    H = _run(ctx, "heff", m, rank)
+    ref = om.heff(m, "aim")
+    assert rel_l2(H, ref) <= TOL
+    assert max_node_rel(H, ref) <= NODE_TOL
+    assert rel_l2(_run(ctx, "exchange", m, rank), om.exchange(m)) <= TOL
