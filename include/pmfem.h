@@ -122,19 +122,25 @@ pmfem_status pmfem_setup(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_per
                          const pmfem_grid* grid, int cuda_device);
 
 /* Multi-GPU context: every rank passes the FULL mesh; the library runs the
- * same deterministic setup, partitions the internal (box-sorted, z-slowest) rows into `world`
- * contiguous, cost-balanced slab ranges and builds halo lists for m (K1 columns), q (C_box
- * columns) and u (ring-1 columns).  m and H passed to the field calls then cover this rank's
- * rows only ([n_parents_local][3], order from pmfem_get_order).  Per evaluation: grouped
- * ncclSend/ncclRecv halo exchanges with every peer that shares a boundary, and the
- * slab-decomposed FFT convolution: ncclReduceScatter of the anterpolated grid Q into z slabs
- * (n2/world planes), X/Y passes, grouped send/recv all-to-all into k0 slabs (columns
- * [h_r, h_r + H_r), export "slab_kranges"), Z pass x G_hat, all-to-all back, Y'/X' passes,
- * ncclAllGather of U.  When n2 % world != 0 or H0 < world (or PMFEM_NO_SLAB is set): one
- * ncclAllReduce of Q and a replicated FFT instead.  nccl_unique_id: 128 bytes
- * from pmfem_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
- * cuda_device = -1 builds the host-only plan (exportable: dist_bounds, send_/recv_{m,q,u}_{ptr,idx}).
- * world = 1 is identical to pmfem_setup. */
+ * same deterministic host setup and derives every peer's plan without coordination:
+ *  - slab axis: the longest grid axis (z on ties) becomes the internal z (slowest) axis by an axis
+ *    permutation of the coordinates, periodicity and grid; m and H stay in the user frame, every
+ *    exported setup artifact and pmfem_info.grid/fft are in the internal frame (export "axis_perm");
+ *  - partition: rank r owns the rows anchored in the z planes [Z_r, Z_r+1) (export "dist_planes";
+ *    variable thickness balancing the row counts) = its z slab of the FFT; it builds Z0, the local
+ *    operators and C_box for its own rows only (setup time and operator memory ~1/world);
+ *  - per evaluation: grouped ncclSend/ncclRecv halos of m (the own rows' 2-ring), q (the rows
+ *    anchored within the anterpolation stencil / r_ER planes around the slab) and u (ring 1); K2
+ *    computes the own planes completely (no grid reduction); slab FFT: X, Y on the own planes, an
+ *    all-to-all into k0 columns [h_r, h_r + H_r) (export "slab_kranges"), Z x G_hat, the
+ *    all-to-all back, Y', X'; then the p U "ghost" planes above the slab that K4's stencils read
+ *    come from their owners (export "dist_ghost").
+ * The slab axis needs at least one plane per rank (else PMFEM_E_INVALID_ARG).  With fewer k0
+ * columns than ranks (or PMFEM_NO_SLAB set) the anterpolated grid is all-reduced and the FFT
+ * replicated instead.  nccl_unique_id: 128 bytes from
+ * pmfem_nccl_unique_id on rank 0, broadcast by the caller (e.g. torch.distributed).
+ * cuda_device = -1 builds the host-only plan (exportable: dist_bounds, dist_planes, dist_ghost,
+ * axis_perm, send_/recv_{m,q,u}_{ptr,idx}).  world = 1 is identical to pmfem_setup. */
 pmfem_status pmfem_setup_dist(pmfem_ctx* out, const pmfem_mesh* mesh, const pmfem_periodicity* per,
                               const pmfem_grid* grid, int cuda_device, const void* nccl_unique_id,
                               int rank, int world);
@@ -167,13 +173,35 @@ pmfem_status pmfem_heff_host(pmfem_ctx ctx, const float* m_host, float* H_host, 
 
 /* NEXT-2: `steps` classical RK4 steps of the LLG equation (P:67-71, P:101-105,
  * Eq. llg; reading R18) dm/dt = -gamma/(1+alpha^2) [m x H + alpha m x (m x H)],
- * H = H_ms + H_ex + H_applied (uniform, Oe), |m| renormalised to 1 after every step.
+ * H = H_ms + H_ex + H_an + H_applied (uniform, Oe; H_an from pmfem_set_anisotropy), |m|
+ * renormalised to 1 after every step.
  * m: device pointer [n_parents_local][3] fp32, updated in place.  dt in s, gamma in rad/(s Oe)
  * (1.7595e7 for electrons).  Each step = 4 pmfem_heff evaluations + 4 fused stage kernels; on a
  * non-default stream the step is captured once into a CUDA graph and replayed `steps` times.
  * H_applied may be NULL (zero).  Asynchronous like the field calls. */
 pmfem_status pmfem_llg_rk4(pmfem_ctx ctx, float* m, int64_t steps, double dt, double alpha, double gamma,
                            const double* H_applied, void* cuda_stream);
+
+/* NEXT-2: the local anisotropy field H_an of Eq. heff ("local ... straightforward")
+ * added by the LLG integrators (not by pmfem_heff, whose H_eff is H_ms + H_ex):
+ *   kind 0: none;  1: uniaxial, energy -K (m.u)^2, H = (2K/Ms) (m.u) u, axis u (normalised);
+ *   kind 2: cubic (crystal axes = x, y, z), energy K (mx^2 my^2 + my^2 mz^2 + mz^2 mx^2),
+ *           H = -(2K/Ms) (mx (my^2 + mz^2), my (mz^2 + mx^2), mz (mx^2 + my^2)).
+ * K in erg/cm^3, Ms of material region 0 (single-material meshes), axis in the user frame
+ * (may be NULL for kinds 0 and 2). */
+pmfem_status pmfem_set_anisotropy(pmfem_ctx ctx, int kind, double K, const double* axis);
+
+/* NEXT-2: the paper's adaptive second-order Adams predictor-corrector ("predictor-corrector
+ * schemes based on explicit second order Adams-Moulton (midpoint) approach"), t = 0 .. t_end:
+ * variable-step AB2 predictor (forward Euler on the first step), one H_eff evaluation, AM2
+ * (trapezoidal) corrector, |m| renormalised; Milne error estimate err = max_n |m_c - m_p| / 6
+ * (max over ranks on N > 1), accepted when err <= tol, next dt = dt min(2, max(0.2,
+ * 0.9 (tol/err)^(1/3))), capped by dt_max when dt_max > 0.  Two H_eff evaluations per accepted
+ * step.  The host reads the error after every attempt (the call synchronises the stream).
+ * m: device pointer [n_parents_local][3], updated in place; the step counts may be NULL. */
+pmfem_status pmfem_llg_am2(pmfem_ctx ctx, float* m, double t_end, double dt0, double tol, double alpha,
+                           double gamma, const double* H_applied, double dt_max, void* cuda_stream,
+                           int64_t* steps_accepted, int64_t* steps_rejected);
 
 pmfem_status pmfem_query(pmfem_ctx ctx, pmfem_info* out);
 

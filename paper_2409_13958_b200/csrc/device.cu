@@ -618,19 +618,41 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
 
 // ------------------------------------------------------------------ LLG RK4 stage (NEXT-2)
 // dm/dt = -g [ m x H + alpha m x (m x H) ], g = gamma / (1 + alpha^2)   (Eq. llg)
-// Stage s of classical RK4: k = f(ms, H + H_ap); acc (+)= w_s dt k; next stage state
+// Stage s of classical RK4: k = f(ms, H + H_ap + H_an(ms)); acc (+)= w_s dt k; next stage state
 // m0 + c_{s+1} dt k, or (last stage) m0 <- normalize(m0 + acc).  Rank-local rows.
+struct Anis { int kind; float hk; float ux, uy, uz; };   // hk = 2 K / Ms (NEXT-2)
+
+// H_an of the unit vector (sx, sy, sz) (oracle/llg.py anisotropy_field): uniaxial (2K/Ms)(m.u)u,
+// cubic -(2K/Ms)(mx(my^2+mz^2), my(mz^2+mx^2), mz(mx^2+my^2))
+__device__ __forceinline__ void anis_field(const Anis& a, float sx, float sy, float sz, float& hx, float& hy, float& hz) {
+  if (a.kind == 1) {
+    const float d = a.hk * (sx * a.ux + sy * a.uy + sz * a.uz);
+    hx += d * a.ux; hy += d * a.uy; hz += d * a.uz;
+  } else if (a.kind == 2) {
+    const float x2 = sx * sx, y2 = sy * sy, z2 = sz * sz;
+    hx -= a.hk * sx * (y2 + z2); hy -= a.hk * sy * (z2 + x2); hz -= a.hk * sz * (x2 + y2);
+  }
+}
+
+// dm/dt = -g [m x H + alpha m x (m x H)]
+__device__ __forceinline__ void llg_f(float sx, float sy, float sz, float Hx, float Hy, float Hz, float g, float alpha,
+                                      float& kx, float& ky, float& kz) {
+  const float cx = sy * Hz - sz * Hy, cy = sz * Hx - sx * Hz, cz = sx * Hy - sy * Hx;        // m x H
+  const float dx = sy * cz - sz * cy, dy = sz * cx - sx * cz, dz = sx * cy - sy * cx;        // m x (m x H)
+  kx = -g * (cx + alpha * dx); ky = -g * (cy + alpha * dy); kz = -g * (cz + alpha * dz);
+}
+
 __global__ void k_llg_stage(int64_t n, float* __restrict__ m0, const float* __restrict__ ms,
-                            const float* __restrict__ H, float hx, float hy, float hz, float g, float alpha,
+                            const float* __restrict__ H, float hx, float hy, float hz, Anis an, float g, float alpha,
                             float wdt, float cnext_dt, float* __restrict__ acc, float* __restrict__ mnext,
                             int first, int last) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float sx = ms[3 * i], sy = ms[3 * i + 1], sz = ms[3 * i + 2];
-  const float Hx = H[3 * i] + hx, Hy = H[3 * i + 1] + hy, Hz = H[3 * i + 2] + hz;
-  const float cx = sy * Hz - sz * Hy, cy = sz * Hx - sx * Hz, cz = sx * Hy - sy * Hx;        // m x H
-  const float dx = sy * cz - sz * cy, dy = sz * cx - sx * cz, dz = sx * cy - sy * cx;        // m x (m x H)
-  const float kx = -g * (cx + alpha * dx), ky = -g * (cy + alpha * dy), kz = -g * (cz + alpha * dz);
+  float Hx = H[3 * i] + hx, Hy = H[3 * i + 1] + hy, Hz = H[3 * i + 2] + hz;
+  anis_field(an, sx, sy, sz, Hx, Hy, Hz);
+  float kx, ky, kz;
+  llg_f(sx, sy, sz, Hx, Hy, Hz, g, alpha, kx, ky, kz);
   float ax = wdt * kx, ay = wdt * ky, az = wdt * kz;
   if (!first) { ax += acc[3 * i]; ay += acc[3 * i + 1]; az += acc[3 * i + 2]; }
   const float m0x = m0[3 * i], m0y = m0[3 * i + 1], m0z = m0[3 * i + 2];
@@ -642,6 +664,42 @@ __global__ void k_llg_stage(int64_t n, float* __restrict__ m0, const float* __re
     const float inv = rsqrtf(nx * nx + ny * ny + nz * nz);
     m0[3 * i] = nx * inv; m0[3 * i + 1] = ny * inv; m0[3 * i + 2] = nz * inv;
   }
+}
+
+// ---- AM2 predictor-corrector (oracle/llg.py am2_step)
+// f = dm/dt at (m, H + H_ap + H_an(m))
+__global__ void k_llg_rhs(int64_t n, const float* __restrict__ m, const float* __restrict__ H, float hx, float hy,
+                          float hz, Anis an, float g, float alpha, float* __restrict__ f) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float sx = m[3 * i], sy = m[3 * i + 1], sz = m[3 * i + 2];
+  float Hx = H[3 * i] + hx, Hy = H[3 * i + 1] + hy, Hz = H[3 * i + 2] + hz;
+  anis_field(an, sx, sy, sz, Hx, Hy, Hz);
+  llg_f(sx, sy, sz, Hx, Hy, Hz, g, alpha, f[3 * i], f[3 * i + 1], f[3 * i + 2]);
+}
+// predictor m_p = m + dt [(1 + r/2) f_n - (r/2) f_prev]  (r = 0: forward Euler)
+__global__ void k_am2_pred(int64_t n, const float* __restrict__ m, const float* __restrict__ fn,
+                           const float* __restrict__ fprev, float dt, float r, float* __restrict__ mp) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * n) return;
+  mp[i] = m[i] + dt * ((1.f + 0.5f * r) * fn[i] - (r > 0.f ? 0.5f * r * fprev[i] : 0.f));
+}
+// corrector m_c = m + dt/2 (f_n + f_p), normalised into mc; err = max |m_c - m_p| / 6 (float bits)
+__global__ void k_am2_corr(int64_t n, const float* __restrict__ m, const float* __restrict__ fn,
+                           const float* __restrict__ fp, const float* __restrict__ mp, float dt,
+                           float* __restrict__ mc, unsigned* __restrict__ err) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float e = 0.f;
+  if (i < n) {
+    float c[3];
+    for (int k = 0; k < 3; ++k) c[k] = m[3 * i + k] + 0.5f * dt * (fn[3 * i + k] + fp[3 * i + k]);
+    const float ex = c[0] - mp[3 * i], ey = c[1] - mp[3 * i + 1], ez = c[2] - mp[3 * i + 2];
+    e = sqrtf(ex * ex + ey * ey + ez * ez) / 6.f;
+    const float inv = rsqrtf(c[0] * c[0] + c[1] * c[1] + c[2] * c[2]);
+    for (int k = 0; k < 3; ++k) mc[3 * i + k] = c[k] * inv;
+  }
+  for (int o = 16; o > 0; o >>= 1) e = fmaxf(e, __shfl_xor_sync(0xffffffffu, e, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(err, __float_as_uint(e));   // e >= 0: bit order = value order
 }
 
 // ------------------------------------------------------------------ PGF table (fp64)
@@ -1445,27 +1503,100 @@ namespace pmfem {
 
 // One classical RK4 step of the LLG equation on the rank-local rows of m (in place):
 // 4 H_eff evaluations + 4 fused stage kernels (k_llg_stage).
-void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
-                         const double Hap[3]) {
-  const int64_t n = D.hi - D.lo;
-  if (n <= 0 && D.world == 1) return;     // a row-less rank still joins the evaluations' collectives
+static Anis anis_of(const DeviceState& D) {
+  Anis a{D.anis_kind, (float)(2.0 * D.anis_K / D.anis_Ms), (float)D.anis_u[0], (float)D.anis_u[1], (float)D.anis_u[2]};
+  return a;
+}
+
+static void llg_scratch(DeviceState& D, int64_t n) {
   if (!D.llg_ms) {
     D.llg_ms = dalloc<float>(3 * (size_t)std::max<int64_t>(n, 1));
     D.llg_H = dalloc<float>(3 * (size_t)std::max<int64_t>(n, 1));
     D.llg_acc = dalloc<float>(3 * (size_t)std::max<int64_t>(n, 1));
   }
+}
+
+void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
+                         const double Hap[3]) {
+  const int64_t n = D.hi - D.lo;
+  if (n <= 0 && D.world == 1) return;     // a row-less rank still joins the evaluations' collectives
+  llg_scratch(D, n);
   const float g = (float)(gamma / (1.0 + alpha * alpha));
   const unsigned blocks = (unsigned)((n + 255) / 256);
   const float w[4] = {(float)(dt / 6), (float)(dt / 3), (float)(dt / 3), (float)(dt / 6)};
   const float c[4] = {(float)(dt / 2), (float)(dt / 2), (float)dt, 0.f};
+  const Anis an = anis_of(D);
   for (int s = 0; s < 4; ++s) {
     const float* ms = (s == 0) ? m : D.llg_ms;
     device_eval(D, ms, D.llg_H, st, EVAL_HEFF);
     if (n > 0)
-    k_llg_stage<<<blocks, 256, 0, st>>>(n, m, ms, D.llg_H, (float)Hap[0], (float)Hap[1], (float)Hap[2], g,
+    k_llg_stage<<<blocks, 256, 0, st>>>(n, m, ms, D.llg_H, (float)Hap[0], (float)Hap[1], (float)Hap[2], an, g,
                                         (float)alpha, w[s], c[s], D.llg_acc, D.llg_ms, s == 0, s == 3);
     CK(cudaGetLastError());
   }
+}
+
+// Adaptive AM2 integration from t = 0 to t_end (oracle/llg.py am2_integrate): per attempt one
+// predictor, one H_eff evaluation, one corrector with the error reduction (read back by the host
+// to accept / reject), and on acceptance one more evaluation for f_{n+1}.  N > 1: the error is
+// max-reduced over the ranks.
+void device_llg_am2(DeviceState& D, float* m, cudaStream_t st, double t_end, double dt0, double tol, double alpha,
+                    double gamma, const double Hap[3], double dt_max, int64_t* acc_out, int64_t* rej_out) {
+  const int64_t n = D.hi - D.lo;
+  llg_scratch(D, n);
+  const size_t b = 3 * (size_t)std::max<int64_t>(n, 1) * sizeof(float);
+  float *fn = nullptr, *fprev = nullptr, *mp = nullptr, *fp = nullptr;
+  unsigned* err = nullptr;
+  CK(cudaMalloc(&fn, b)); CK(cudaMalloc(&fprev, b)); CK(cudaMalloc(&mp, b)); CK(cudaMalloc(&fp, b));
+  CK(cudaMalloc(&err, sizeof(unsigned)));
+  struct Free { void* p[5]; ~Free() { for (void* x : p) cudaFree(x); } } fr{{fn, fprev, mp, fp, err}};
+  const float g = (float)(gamma / (1.0 + alpha * alpha));
+  const unsigned blocks = (unsigned)std::max<int64_t>(1, (n + 255) / 256), blocks3 = (unsigned)std::max<int64_t>(1, (3 * n + 255) / 256);
+  const Anis an = anis_of(D);
+  auto rhs = [&](const float* x, float* f) {
+    device_eval(D, x, D.llg_H, st, EVAL_HEFF);
+    if (n > 0) k_llg_rhs<<<blocks, 256, 0, st>>>(n, x, D.llg_H, (float)Hap[0], (float)Hap[1], (float)Hap[2], an, g, (float)alpha, f);
+    CK(cudaGetLastError());
+  };
+  rhs(m, fn);
+  double t = 0.0, dt = dt0, dt_prev = 0.0;
+  int64_t acc = 0, rej = 0;
+  while (t < t_end * (1 - 1e-12)) {
+    dt = std::min(dt, t_end - t);
+    if (dt_max > 0) dt = std::min(dt, dt_max);
+    const double r = dt_prev > 0 ? dt / dt_prev : 0.0;
+    if (n > 0) k_am2_pred<<<blocks3, 256, 0, st>>>(n, m, fn, fprev, (float)dt, (float)r, mp);
+    CK(cudaGetLastError());
+    rhs(mp, fp);
+    CK(cudaMemsetAsync(err, 0, sizeof(unsigned), st));
+    if (n > 0) k_am2_corr<<<blocks, 256, 0, st>>>(n, m, fn, fp, mp, (float)dt, D.llg_ms, err);
+    CK(cudaGetLastError());
+    if (D.world > 1) {
+      ncclComm_t comm = (ncclComm_t)D.comm;
+      NCK(ncclAllReduce(err, err, 1, ncclUint32, ncclMax, comm, st));
+    }
+    unsigned eb = 0;
+    CK(cudaMemcpyAsync(&eb, err, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ef;
+    std::memcpy(&ef, &eb, sizeof(float));
+    const double e = ef;
+    const double fac = e == 0.0 ? 2.0 : std::min(2.0, std::max(0.2, 0.9 * std::cbrt(tol / e)));
+    if (e <= tol) {
+      t += dt;
+      if (n > 0) CK(cudaMemcpyAsync(m, D.llg_ms, 3 * (size_t)n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+      std::swap(fprev, fn);
+      rhs(m, fn);
+      dt_prev = dt;
+      ++acc;
+    } else {
+      ++rej;
+    }
+    dt *= fac;
+    fr.p[0] = fn; fr.p[1] = fprev;
+  }
+  *acc_out = acc;
+  *rej_out = rej;
 }
 
 }  // namespace pmfem

@@ -151,6 +151,8 @@ struct DeviceState {
   GraphSlot graphs[4];
   int graph_next = 0;
   // LLG RK4 scratch (rank-local rows) and the captured RK4 step
+  int anis_kind = 0;          // NEXT-2 anisotropy: 0 none, 1 uniaxial, 2 cubic (pmfem_set_anisotropy)
+  double anis_K = 0, anis_Ms = 1, anis_u[3] = {0, 0, 1};
   float* llg_ms = nullptr;
   float* llg_H = nullptr;
   float* llg_acc = nullptr;
@@ -162,6 +164,8 @@ struct DeviceState {
 
 void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
                          const double Hap[3]);
+void device_llg_am2(DeviceState& D, float* m, cudaStream_t st, double t_end, double dt0, double tol, double alpha,
+                    double gamma, const double Hap[3], double dt_max, int64_t* acc_out, int64_t* rej_out);
 
 void device_init_comm(DeviceState& D, const HostSetup& S, const void* nccl_id);
 int64_t device_build_cbox(DeviceState& D, const HostSetup& S);

@@ -261,6 +261,46 @@ static pmfem_status eval(pmfem_ctx ctx, const float* m, float* H, void* stream, 
   });
 }
 
+pmfem_status pmfem_set_anisotropy(pmfem_ctx ctx, int kind, double K, const double* axis) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    pmfem::require(kind >= 0 && kind <= 2 && std::isfinite(K), PMFEM_E_INVALID_ARG, "anisotropy kind 0, 1 or 2");
+    double u[3] = {0, 0, 1};
+    if (kind == 1) {
+      pmfem::require(axis != nullptr, PMFEM_E_INVALID_ARG, "NULL uniaxial axis");
+      const double nrm = std::sqrt(axis[0] * axis[0] + axis[1] * axis[1] + axis[2] * axis[2]);
+      pmfem::require(nrm > 0, PMFEM_E_INVALID_ARG, "zero uniaxial axis");
+      for (int a = 0; a < 3; ++a) u[a] = axis[a] / nrm;
+    }
+    pmfem::DeviceState& D = ctx->D;
+    D.anis_kind = kind;
+    D.anis_K = K;
+    D.anis_Ms = ctx->S.Ms_tet.empty() ? 1.0 : ctx->S.Ms_tet[0];
+    for (int a = 0; a < 3; ++a) D.anis_u[a] = u[a];
+    if (D.llg_exec) { cudaGraphExecDestroy(D.llg_exec); D.llg_exec = nullptr; }   // recapture
+  });
+}
+
+pmfem_status pmfem_llg_am2(pmfem_ctx ctx, float* m, double t_end, double dt0, double tol, double alpha, double gamma,
+                           const double* H_applied, double dt_max, void* stream, int64_t* steps_accepted,
+                           int64_t* steps_rejected) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    pmfem::require(!ctx->host_only, PMFEM_E_STATE, "host-only context (cuda_device = -1) cannot integrate");
+    pmfem::require(m != nullptr, PMFEM_E_INVALID_ARG, "NULL m");
+    pmfem::require(ctx->D.pgf_ready, PMFEM_E_STATE, "pmfem_build_pgf has not been called");
+    pmfem::require(t_end >= 0 && dt0 > 0 && tol > 0 && alpha >= 0 && gamma > 0, PMFEM_E_INVALID_ARG,
+                   "bad LLG parameters");
+    cudaSetDevice(ctx->D.device);
+    const double zero[3] = {0, 0, 0};
+    int64_t a = 0, r = 0;
+    pmfem::device_llg_am2(ctx->D, m, (cudaStream_t)stream, t_end, dt0, tol, alpha, gamma,
+                          H_applied ? H_applied : zero, dt_max, &a, &r);
+    if (steps_accepted) *steps_accepted = a;
+    if (steps_rejected) *steps_rejected = r;
+  });
+}
+
 pmfem_status pmfem_llg_rk4(pmfem_ctx ctx, float* m, int64_t steps, double dt, double alpha, double gamma,
                            const double* H_applied, void* stream) {
   if (!ctx) return PMFEM_E_INVALID_ARG;

@@ -22,7 +22,8 @@ STATUS = {0: "PMFEM_OK", 1: "PMFEM_E_INVALID_ARG", 2: "PMFEM_E_MESH", 3: "PMFEM_
           7: "PMFEM_E_PGF_NOT_CONVERGED", 8: "PMFEM_E_STATE", 9: "PMFEM_E_CUDA", 10: "PMFEM_E_NCCL",
           11: "PMFEM_E_OOM"}
 
-SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_llg_rk4", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
+SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_llg_rk4",
+           "pmfem_llg_am2", "pmfem_set_anisotropy", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
            "pmfem_heff_host", "pmfem_query", "pmfem_get_order", "pmfem_export", "pmfem_set_timing",
            "pmfem_get_timing", "pmfem_last_error", "pmfem_destroy"]
 
@@ -74,6 +75,10 @@ for _n in ("pmfem_demag", "pmfem_exchange", "pmfem_heff", "pmfem_heff_host"):
     getattr(_lib, _n).argtypes = [_vp, _vp, _vp, _vp]
 _lib.pmfem_llg_rk4.argtypes = [_vp, _vp, ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                               ctypes.c_void_p, _vp]
+_lib.pmfem_llg_am2.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                               ctypes.c_double, ctypes.c_void_p, ctypes.c_double, _vp,
+                               ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
+_lib.pmfem_set_anisotropy.argtypes = [_vp, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
 _lib.pmfem_query.argtypes = [_vp, ctypes.POINTER(_Info)]
 _lib.pmfem_get_order.argtypes = [_vp, ctypes.POINTER(ctypes.c_int64)]
 _lib.pmfem_export.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(ctypes.c_int64)]
@@ -230,6 +235,23 @@ class Context:
         self._check(_lib.pmfem_llg_rk4(self._h, _dev_ptr(m, self.n_parents_local, self.device), int(steps), float(dt), float(alpha), float(gamma),
                                        ctypes.cast(hap, ctypes.c_void_p), self._stream(stream)))
         return m
+
+    def set_anisotropy(self, kind, K=0.0, axis=(0.0, 0.0, 1.0)):
+        """NEXT-2 anisotropy used by the LLG integrators: kind 0 none, 1 uniaxial (axis), 2 cubic."""
+        ax = (ctypes.c_double * 3)(*[float(v) for v in axis])
+        self._check(_lib.pmfem_set_anisotropy(self._h, int(kind), float(K), ctypes.cast(ax, ctypes.c_void_p)))
+
+    def llg_am2(self, m, t_end, dt0, tol, alpha, gamma=1.7595e7, H_applied=(0.0, 0.0, 0.0), dt_max=0.0,
+                stream=None):
+        """Adaptive AM2 predictor-corrector LLG integration of m (in place) to t_end; returns
+        (accepted, rejected) step counts."""
+        hap = (ctypes.c_double * 3)(*[float(v) for v in H_applied])
+        acc, rej = ctypes.c_int64(0), ctypes.c_int64(0)
+        self._check(_lib.pmfem_llg_am2(self._h, _dev_ptr(m, self.n_parents_local, self.device), float(t_end),
+                                       float(dt0), float(tol), float(alpha), float(gamma),
+                                       ctypes.cast(hap, ctypes.c_void_p), float(dt_max), self._stream(stream),
+                                       ctypes.byref(acc), ctypes.byref(rej)))
+        return acc.value, rej.value
 
     def query(self):
         info = _Info()

@@ -25,6 +25,8 @@ CONFIGS = {
     # other periodic axes (parity coverage, not BASELINE workloads)
     "R1": "1D-periodic rod along z (PAPER.md:277: R = 20 nm, cell height 2R, touching), 16x16x16 AIM grid",
     "Y1": "1D-periodic strip along y with a slot (touching), 8x64x4 AIM grid",
+    # NEXT-2 spin-wave check (Eq. sw_disp): a continuous 2D-periodic film
+    "K1": "2D-periodic Permalloy film 200 nm x 40 nm x 10 nm (touching), 64x16x4 AIM grid",
 }
 
 
@@ -35,7 +37,7 @@ def _round_cells(length, h):
 def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
     """Return dict(mesh, periodic, L, grid, Ms, Aex, name, desc)."""
     if seed is None:
-        seed = {"C": 1000, "N": 2000, "R": 3000, "Y": 4000}[name[0]] + int(name[1:])
+        seed = {"C": 1000, "N": 2000, "R": 3000, "Y": 4000, "K": 5000}[name[0]] + int(name[1:])
     c = float(coarsen)
     if name == "C1":
         L = 100 * NM
@@ -149,6 +151,17 @@ def make_config(name, coarsen=1, jitter=0.15, seed=None, grid=None, cells=None):
         mesh = kuhn_voxel_mesh(mask, h, wrap=(False, True, False), jitter=jitter, seed=seed, name=name)
         periodic = (0, 1, 0); lattice = (0.0, Ly, 0.0)
         g = grid or (max(4, int(8 // c)), max(16, int(64 // c)), 4)
+        Ms, Aex = 637.0, 1.4e-6
+    elif name == "K1":
+        # Permalloy film, Ms = 637 emu/cm^3, A = 1.4e-6 erg/cm; the cell holds one spin-wave
+        # wavelength 2 pi / k = 200 nm along x
+        Lx, Ly, t = 200 * NM, 40 * NM, 10 * NM
+        h = 2.5 * NM * c
+        nx, ny, nz = _round_cells(Lx, h), _round_cells(Ly, h), max(1, _round_cells(t, h))
+        mask = np.ones((nx, ny, nz), bool)
+        mesh = kuhn_voxel_mesh(mask, Lx / nx, wrap=(True, True, False), jitter=jitter, seed=seed, name=name)
+        periodic = (1, 1, 0); lattice = (Lx, Ly, 0.0)
+        g = grid or (max(16, int(64 // c)), max(8, int(16 // c)), 4)
         Ms, Aex = 637.0, 1.4e-6
     else:
         raise KeyError(name)
