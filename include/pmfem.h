@@ -158,6 +158,19 @@ pmfem_status pmfem_nccl_unique_id(void* out128);
  * below fp64 resolution cannot be met.  The achieved value is reported in pmfem_info. */
 pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err);
 
+/* NEXT-4: the Bloch-phase periodic Green's function of Eq. 2 with k0 != 0
+ * (P:183-185), G(r; k0) = sum_i exp(-j k0.R_i) / |r - R_i|, by Ewald sums in fp64 (the static
+ * formulas with cos(k.r) -> exp(-j (G + k0).r) and the G = 0 term kept; no renormalisation is
+ * needed off the reciprocal lattice).  Tabulates the MODULATED kernel exp(j k0.r) G(r; k0) --
+ * L-periodic, so the AIM grid convolution of quasi-periodic data runs through it -- at every
+ * padded grid displacement (on the GPU for device contexts, on the host otherwise) and its full
+ * complex spectrum / #FFT points (host fp64 FFT); exports "kernel_bloch" and "spectrum_bloch"
+ * ([P2][P1][P0] complex, interleaved re/im).  k0[3] in rad/cm, user frame; must vanish on
+ * non-periodic axes and must not be a reciprocal lattice vector (PMFEM_E_INVALID_ARG).
+ * The complex field path (quasi-periodic m, complex H) is not built: the Bloch kernel feeds no
+ * field evaluation yet. */
+pmfem_status pmfem_build_pgf_bloch(pmfem_ctx ctx, const double* k0, double target_rel_err);
+
 /* Field evaluations.  m: device pointer [N'_local][3] fp32 (internal node order, unit vectors);
  * H: device pointer [N'][3] fp32, written (not accumulated); must not alias m.
  * cuda_stream: a cudaStream_t or NULL for the legacy default stream.  Asynchronous: nothing

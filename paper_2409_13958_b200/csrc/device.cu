@@ -728,6 +728,29 @@ __global__ void k_pgf_table(PgfDev pd, int P0, int P1, int P2, int n0, int n1, i
         K[((int64_t)a2[z] * P1 + a1[y]) * P0 + a0[x]] = v;
 }
 
+// NEXT-4: modulated Bloch kernel exp(j k0.r) G(r; k0) (pgf.cuh pgf_eval_bloch) at every padded
+// grid displacement, fp64 complex interleaved; one thread per point (no mirror symmetry)
+struct K0v { double k[3]; };
+__global__ void k_pgf_table_bloch(PgfDev pd, K0v k0, int P0, int P1, int P2, int n0, int n1, int n2, int per0,
+                                  int per1, int per2, double d0, double d1, double d2, double* __restrict__ K) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)P0 * P1 * P2) return;
+  const int j[3] = {(int)(idx % P0), (int)((idx / P0) % P1), (int)(idx / ((int64_t)P0 * P1))};
+  const int n[3] = {n0, n1, n2}, P[3] = {P0, P1, P2}, per[3] = {per0, per1, per2};
+  const double d[3] = {d0, d1, d2};
+  double r[3];
+  bool skip = false;
+  for (int a = 0; a < 3; ++a) {
+    if (!per[a] && j[a] == n[a]) skip = true;
+    const int jj = per[a] ? j[a] : (j[a] < n[a] ? j[a] : j[a] - P[a]);
+    r[a] = jj * d[a];
+  }
+  Cplx v{0.0, 0.0};
+  if (!skip) v = pgf_eval_bloch(pd, k0.k, r, j[0] == 0 && j[1] == 0 && j[2] == 0);
+  K[2 * idx] = v.re;
+  K[2 * idx + 1] = v.im;
+}
+
 __global__ void k_spec_finish(const double2* __restrict__ C, float* __restrict__ spec, int64_t tot, double scale) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= tot) return;
@@ -1159,6 +1182,28 @@ void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& Pp) {
   cudaFree(K);
   cudaFree(C);
   D.pgf_ready = true;
+}
+
+void device_bloch_table(DeviceState& D, const HostSetup& S, const PgfParams& Pp, const double k0[3],
+                        std::vector<double>& K) {
+  CK(cudaSetDevice(D.device));
+  PgfDev pd;
+  std::memset(&pd, 0, sizeof(pd));
+  pd.dim = Pp.dim;
+  for (int i = 0; i < 3; ++i) { pd.ax[i] = Pp.ax[i]; pd.L[i] = Pp.L[i]; pd.nreal[i] = Pp.nreal[i]; pd.mrec[i] = Pp.mrec[i]; }
+  pd.alpha = Pp.alpha;
+  pd.xr = Pp.xr;
+  gauss_legendre01(64, pd.gl_x, pd.gl_w);
+  const int64_t tot = (int64_t)D.P[0] * D.P[1] * D.P[2];
+  double* dK = dalloc<double>(2 * tot);
+  K0v kv{{k0[0], k0[1], k0[2]}};
+  k_pgf_table_bloch<<<(unsigned)((tot + 63) / 64), 64>>>(pd, kv, D.P[0], D.P[1], D.P[2], D.n[0], D.n[1], D.n[2],
+                                                           D.periodic[0], D.periodic[1], D.periodic[2], S.delta[0],
+                                                           S.delta[1], S.delta[2], dK);
+  CK(cudaGetLastError());
+  K.resize(2 * tot);
+  CK(cudaMemcpy(K.data(), dK, sizeof(double) * 2 * tot, cudaMemcpyDeviceToHost));
+  cudaFree(dK);
 }
 
 void device_free(DeviceState& D) {

@@ -173,6 +173,8 @@ void device_seg_decode(const DeviceState& D, int* d_col);
 
 void device_upload(DeviceState& D, const HostSetup& S);
 void device_build_pgf(DeviceState& D, const HostSetup& S, const PgfParams& P);
+void device_bloch_table(DeviceState& D, const HostSetup& S, const PgfParams& P, const double k0[3],
+                        std::vector<double>& K);
 void device_free(DeviceState& D);
 enum EvalMode { EVAL_HEFF = 0, EVAL_DEMAG = 1, EVAL_EXCHANGE = 2 };
 void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, EvalMode mode);

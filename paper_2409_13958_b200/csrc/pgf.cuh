@@ -167,3 +167,103 @@ PM_HD inline double pgf_eval(const PgfDev& P, const double r_in[3], bool self) {
 }
 
 }  // namespace pmfem
+
+namespace pmfem {
+
+// ---- NEXT-4: Bloch-phase PGF (Eq. 2 with k0 != 0):
+//   G(r; k0) = sum_i exp(-j k0.R_i) / |r - R_i|
+// Ewald split with the G = 0 reciprocal term kept (k0 off the reciprocal lattice):
+//   real: sum_i exp(-j k0.R_i) erfc(a |r - R_i|) / |r - R_i|
+//   3D: (4 pi / V) sum_G exp(-|q|^2/4a^2) / |q|^2 exp(-j q.r),      q = G + k0
+//   2D: (1 / A) sum_G (pi/|q|) [e^{|q|z} erfc(|q|/2a + az) + e^{-|q|z} erfc(|q|/2a - az)] exp(-j q.rho)
+//   1D: (1 / L) sum_m I(q^2/4a^2, rho^2 q^2/4) exp(-j q x)
+// The point is first wrapped into the unit cell, r = r_w + n L, and G(r) = exp(-j k0.nL) G(r_w).
+// Returns the MODULATED kernel exp(+j k0.r) G(r; k0), which is periodic (the AIM grid convolves
+// quasi-periodic data through it).  self = true: lim [G(r) - 1/r] at r = 0.
+struct Cplx { double re, im; };
+
+PM_HD inline Cplx pgf_eval_bloch(const PgfDev& P, const double k0_in[3], const double r_in[3], bool self) {
+  const double pi = 3.14159265358979323846;
+  const double a = P.alpha;
+  double rw[3] = {0, 0, 0}, rf[2] = {0, 0}, k0[3] = {0, 0, 0};
+  double ph_wrap = 0.0;                     // k0 . (n L) of the wrap
+  double kr = 0.0;                          // k0 . r (modulation)
+  for (int i = 0; i < P.dim; ++i) {
+    const double x = self ? 0.0 : r_in[P.ax[i]];
+    const double L = P.L[i];
+    const double nw = floor(x / L + 0.5);
+    rw[i] = x - nw * L;
+    k0[i] = k0_in[P.ax[i]];
+    ph_wrap += k0[i] * nw * L;
+    kr += k0[i] * x;
+  }
+  for (int i = P.dim; i < 3; ++i) rf[i - P.dim] = self ? 0.0 : r_in[P.ax[i]];
+  const double rf2 = rf[0] * rf[0] + rf[1] * rf[1];
+  double gre = 0.0, gim = 0.0;
+  // real space (images of the wrapped point)
+  const double rc = P.xr / a;
+  const int n0 = P.nreal[0] + 1, n1 = P.dim > 1 ? P.nreal[1] + 1 : 0, n2 = P.dim > 2 ? P.nreal[2] + 1 : 0;
+  for (int i = -n0; i <= n0; ++i)
+    for (int j = -n1; j <= n1; ++j)
+      for (int k = -n2; k <= n2; ++k) {
+        if (self && i == 0 && j == 0 && k == 0) continue;
+        const double Rx = i * P.L[0], Ry = P.dim > 1 ? j * P.L[1] : 0.0, Rz = P.dim > 2 ? k * P.L[2] : 0.0;
+        const double x = rw[0] - Rx, y = rw[1] - Ry, z = rw[2] - Rz;
+        const double d = sqrt(x * x + y * y + z * z + rf2);
+        if (d == 0.0 || d > rc + 1e-300) continue;
+        const double e = erfc(a * d) / d, ph = -(k0[0] * Rx + k0[1] * Ry + k0[2] * Rz);
+        gre += e * cos(ph); gim += e * sin(ph);
+      }
+  if (self) gre += -2.0 * a / sqrt(pi);
+  // reciprocal space, q = G + k0 (index ranges grown by the shift)
+  int mr[3] = {0, 0, 0};
+  for (int i = 0; i < P.dim; ++i) mr[i] = P.mrec[i] + 1 + (int)ceil(fabs(k0[i]) * P.L[i] / (2 * pi));
+  if (P.dim == 3) {
+    const double V = P.L[0] * P.L[1] * P.L[2];
+    for (int i = -mr[0]; i <= mr[0]; ++i)
+      for (int j = -mr[1]; j <= mr[1]; ++j)
+        for (int k = -mr[2]; k <= mr[2]; ++k) {
+          const double qx = 2 * pi * i / P.L[0] + k0[0], qy = 2 * pi * j / P.L[1] + k0[1], qz = 2 * pi * k / P.L[2] + k0[2];
+          const double q2 = qx * qx + qy * qy + qz * qz;
+          if (q2 == 0.0) continue;
+          const double e = 4 * pi / V * exp(-q2 / (4 * a * a)) / q2;
+          if (e < 1e-300) continue;
+          const double ph = -(qx * rw[0] + qy * rw[1] + qz * rw[2]);
+          gre += e * cos(ph); gim += e * sin(ph);
+        }
+  } else if (P.dim == 2) {
+    const double A = P.L[0] * P.L[1], z = rf[0];
+    for (int i = -mr[0]; i <= mr[0]; ++i)
+      for (int j = -mr[1]; j <= mr[1]; ++j) {
+        const double qx = 2 * pi * i / P.L[0] + k0[0], qy = 2 * pi * j / P.L[1] + k0[1];
+        const double q = sqrt(qx * qx + qy * qy);
+        if (q == 0.0) continue;
+        double br = 0.0;
+        for (int sg = -1; sg <= 1; sg += 2) {
+          const double w = q / (2 * a) + sg * a * z;
+          if (w >= 0) br += pm_erfcx(w) * exp(-q * q / (4 * a * a) - a * a * z * z);
+          else br += exp(sg * q * z) * erfc(w);
+        }
+        const double e = pi / (A * q) * br, ph = -(qx * rw[0] + qy * rw[1]);
+        gre += e * cos(ph); gim += e * sin(ph);
+      }
+  } else {
+    const double L = P.L[0];
+    for (int m = -mr[0]; m <= mr[0]; ++m) {
+      const double q = 2 * pi * m / L + k0[0];
+      if (q == 0.0) continue;
+      const double am = q * q / (4 * a * a);
+      if (am > 700) continue;
+      const double e = pm_incbessel(P, am, rf2 * q * q / 4.0) / L, ph = -q * rw[0];
+      gre += e * cos(ph); gim += e * sin(ph);
+    }
+  }
+  // undo the wrap (G(r) = e^{-j k0.nL} G(r_w)) and modulate by e^{+j k0.r}: net phase k0.r - k0.nL
+  const double ph = kr - ph_wrap;
+  Cplx out;
+  out.re = gre * cos(ph) - gim * sin(ph);
+  out.im = gre * sin(ph) + gim * cos(ph);
+  return out;
+}
+
+}  // namespace pmfem

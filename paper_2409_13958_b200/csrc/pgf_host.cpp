@@ -118,7 +118,7 @@ void host_kernel_table(const HostSetup& S, const PgfParams& P, std::vector<doubl
   }
 }
 
-static void fft1d(std::complex<double>* x, int n, int stride) {
+void fft1d(std::complex<double>* x, int n, int stride) {
   // iterative radix-2 DIT, forward (exp(-2 pi i k j / n))
   int logn = 0;
   while ((1 << logn) < n) ++logn;
@@ -160,6 +160,56 @@ void host_fft_spectrum(const HostSetup& S, const std::vector<double>& K, std::ve
       for (int64_t i0 = 0; i0 < H0; ++i0)
         Ghat[(i2 * P1 + i1) * H0 + i0] = c[(i2 * P1 + i1) * P0 + i0].real() / (double)tot;
   Ghat[0] = 0.0;
+}
+
+}  // namespace pmfem
+
+namespace pmfem {
+
+// NEXT-4: the modulated Bloch kernel exp(j k0.r) G(r; k0) at every padded grid displacement
+// (the same index -> displacement map as host_kernel_table), and its full complex spectrum
+// (the kernel is not even: no half-spectrum) divided by the number of FFT points.
+void bloch_grid_points(const HostSetup& S, int64_t idx, double r[3], bool& skip, bool& self) {
+  const int P0 = S.fft_n[0], P1 = S.fft_n[1];
+  const int j[3] = {(int)(idx % P0), (int)((idx / P0) % P1), (int)(idx / ((int64_t)P0 * P1))};
+  skip = false;
+  for (int a = 0; a < 3; ++a) {
+    if (!S.periodic[a] && j[a] == S.grid_n[a]) skip = true;
+    const int jj = S.periodic[a] ? j[a] : (j[a] < S.grid_n[a] ? j[a] : j[a] - S.fft_n[a]);
+    r[a] = jj * S.delta[a];
+  }
+  self = j[0] == 0 && j[1] == 0 && j[2] == 0;
+}
+
+void host_bloch_table(const HostSetup& S, const PgfParams& P, const double k0[3], std::vector<double>& K) {
+  const PgfDev pd = to_dev(P);
+  const int64_t tot = (int64_t)S.fft_n[0] * S.fft_n[1] * S.fft_n[2];
+  K.assign(2 * tot, 0.0);
+#pragma omp parallel for schedule(dynamic, 64)
+  for (int64_t idx = 0; idx < tot; ++idx) {
+    double r[3];
+    bool skip, self;
+    bloch_grid_points(S, idx, r, skip, self);
+    if (skip) continue;
+    const Cplx v = pgf_eval_bloch(pd, k0, r, self);
+    K[2 * idx] = v.re;
+    K[2 * idx + 1] = v.im;
+  }
+}
+
+void host_bloch_spectrum(const HostSetup& S, const std::vector<double>& K, std::vector<double>& Gh) {
+  const int P0 = S.fft_n[0], P1 = S.fft_n[1], P2 = S.fft_n[2];
+  const int64_t tot = (int64_t)P0 * P1 * P2;
+  std::vector<std::complex<double>> c(tot);
+  for (int64_t i = 0; i < tot; ++i) c[i] = {K[2 * i], K[2 * i + 1]};
+#pragma omp parallel for
+  for (int64_t r = 0; r < (int64_t)P1 * P2; ++r) fft1d(&c[r * P0], P0, 1);
+#pragma omp parallel for
+  for (int64_t r = 0; r < (int64_t)P0 * P2; ++r) fft1d(&c[(r / P0) * P0 * P1 + r % P0], P1, P0);
+#pragma omp parallel for
+  for (int64_t r = 0; r < (int64_t)P0 * P1; ++r) fft1d(&c[r], P2, P0 * P1);
+  Gh.assign(2 * tot, 0.0);
+  for (int64_t i = 0; i < tot; ++i) { Gh[2 * i] = c[i].real() / (double)tot; Gh[2 * i + 1] = c[i].imag() / (double)tot; }
 }
 
 }  // namespace pmfem

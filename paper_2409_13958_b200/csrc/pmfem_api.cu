@@ -211,6 +211,31 @@ pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err) {
   });
 }
 
+pmfem_status pmfem_build_pgf_bloch(pmfem_ctx ctx, const double* k0, double target_rel_err) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    pmfem::HostSetup& S = ctx->S;
+    pmfem::require(k0 != nullptr && target_rel_err > 0, PMFEM_E_INVALID_ARG, "NULL k0 or bad target");
+    double kin[3];
+    for (int a = 0; a < 3; ++a) {
+      kin[a] = k0[S.axperm[a]];          // internal frame
+      pmfem::require(S.periodic[a] || kin[a] == 0.0, PMFEM_E_INVALID_ARG, "k0 must vanish on non-periodic axes");
+    }
+    bool off = false;                    // k0 on the reciprocal lattice is the static kernel
+    for (int a = 0; a < 3; ++a)
+      if (S.periodic[a]) {
+        const double f = kin[a] * S.L[a] / (2 * M_PI);
+        off |= std::fabs(f - std::round(f)) > 1e-12;
+      }
+    pmfem::require(off, PMFEM_E_INVALID_ARG, "k0 on the reciprocal lattice: use pmfem_build_pgf");
+    pmfem::PgfParams P = pmfem::make_pgf_params(S.periodic, S.L, target_rel_err);
+    if (ctx->host_only) pmfem::host_bloch_table(S, P, kin, S.kernel_bloch);
+    else pmfem::device_bloch_table(ctx->D, S, P, kin, S.kernel_bloch);
+    pmfem::host_bloch_spectrum(S, S.kernel_bloch, S.spectrum_bloch);
+    for (int a = 0; a < 3; ++a) S.k0[a] = kin[a];
+  });
+}
+
 // One evaluation = ~9 kernel launches (+ NCCL calls on N>1).  On a non-default stream the
 // sequence is captured once per (m, H, stream, mode, timing) into a CUDA graph and replayed
 // (launch overhead paid once); PMFEM_NO_GRAPH=1 disables it.  The legacy default stream cannot
@@ -562,6 +587,8 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
         for (int64_t i = 0; i < cnt; ++i) o[i] = f[i];
       }
     }
+    else if (n == "kernel_bloch") put(S.kernel_bloch.data(), (int64_t)S.kernel_bloch.size(), 8);
+    else if (n == "spectrum_bloch") put(S.spectrum_bloch.data(), (int64_t)S.spectrum_bloch.size(), 8);
     else if (n == "kernel") put(S.kernel.data(), (int64_t)S.kernel.size(), 8);
     else if (n == "spectrum") put(S.spectrum.data(), (int64_t)S.spectrum.size(), 8);
     else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");

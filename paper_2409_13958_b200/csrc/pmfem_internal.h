@@ -109,6 +109,8 @@ struct HostSetup {
   // PGF
   std::vector<double> kernel;       // host-only contexts: K table [fft2][fft1][fft0]
   std::vector<double> spectrum;     // host-only: G_hat half spectrum [fft2][fft1][fft0/2+1]
+  std::vector<double> kernel_bloch, spectrum_bloch;   // NEXT-4 (complex interleaved, full grid)
+  double k0[3] = {0, 0, 0};
   double setup_seconds = 0, pgf_seconds = 0;
   double pgf_achieved_rel_err = 0;
   DistPlan dist;
@@ -151,5 +153,10 @@ double pgf_truncation_error(const HostSetup& S, const PgfParams& P);
 void gauss_legendre01(int n, double* x, double* w);
 void host_kernel_table(const HostSetup& S, const PgfParams& P, std::vector<double>& K);
 void host_fft_spectrum(const HostSetup& S, const std::vector<double>& K, std::vector<double>& Ghat);
+// NEXT-4 Bloch-phase PGF: modulated kernel exp(j k0.r) G(r; k0) on the padded grid (complex,
+// interleaved) and its full complex spectrum / #points
+void bloch_grid_points(const HostSetup& S, int64_t idx, double r[3], bool& skip, bool& self);
+void host_bloch_table(const HostSetup& S, const PgfParams& P, const double k0[3], std::vector<double>& K);
+void host_bloch_spectrum(const HostSetup& S, const std::vector<double>& K, std::vector<double>& Gh);
 
 }  // namespace pmfem

@@ -23,7 +23,8 @@ STATUS = {0: "PMFEM_OK", 1: "PMFEM_E_INVALID_ARG", 2: "PMFEM_E_MESH", 3: "PMFEM_
           11: "PMFEM_E_OOM"}
 
 SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_llg_rk4",
-           "pmfem_llg_am2", "pmfem_set_anisotropy", "pmfem_demag", "pmfem_exchange", "pmfem_heff",
+           "pmfem_llg_am2", "pmfem_set_anisotropy", "pmfem_build_pgf_bloch", "pmfem_demag", "pmfem_exchange",
+           "pmfem_heff",
            "pmfem_heff_host", "pmfem_query", "pmfem_get_order", "pmfem_export", "pmfem_set_timing",
            "pmfem_get_timing", "pmfem_last_error", "pmfem_destroy"]
 
@@ -79,6 +80,7 @@ _lib.pmfem_llg_am2.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_double, ctype
                                ctypes.c_double, ctypes.c_void_p, ctypes.c_double, _vp,
                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
 _lib.pmfem_set_anisotropy.argtypes = [_vp, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
+_lib.pmfem_build_pgf_bloch.argtypes = [_vp, ctypes.c_void_p, ctypes.c_double]
 _lib.pmfem_query.argtypes = [_vp, ctypes.POINTER(_Info)]
 _lib.pmfem_get_order.argtypes = [_vp, ctypes.POINTER(ctypes.c_int64)]
 _lib.pmfem_export.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(ctypes.c_int64)]
@@ -193,6 +195,17 @@ class Context:
 
     def build_pgf(self, target_rel_err=1e-12):
         self._check(_lib.pmfem_build_pgf(self._h, float(target_rel_err)))
+
+    def build_pgf_bloch(self, k0, target_rel_err=1e-12):
+        """NEXT-4: the modulated Bloch kernel table + complex spectrum (exports kernel_bloch,
+        spectrum_bloch as complex [P2][P1][P0])."""
+        k = (ctypes.c_double * 3)(*[float(v) for v in k0])
+        self._check(_lib.pmfem_build_pgf_bloch(self._h, ctypes.cast(k, ctypes.c_void_p), float(target_rel_err)))
+        P = self.query()["fft"]
+        K = self.export("kernel_bloch")
+        G = self.export("spectrum_bloch")
+        shape = (P[2], P[1], P[0])
+        return (K[0::2] + 1j * K[1::2]).reshape(shape), (G[0::2] + 1j * G[1::2]).reshape(shape)
 
     def _stream(self, stream):
         if stream is None:

@@ -49,3 +49,16 @@ def test_device_z0_matches_host(key):
     assert np.abs(a - b).max() <= 1e-11 * np.abs(b).max()
     a, b = dev.export("rowsumZ"), host.export("rowsumZ")
     assert np.abs(a - b).max() <= 1e-11 * np.abs(host.export("z0_val")).max()
+
+
+@pytest.mark.parametrize("key,k0", [("C1r0", (3.0e5, -1.0e5, 2.0e5)), ("C3p1", (1.0e5, 0, 0)),
+                                    ("C2p2", (-2.0e5, 1.5e5, 0)), ("R1p2", (0, 0, 4.0e5))])
+def test_device_bloch_kernel_matches_host(key, k0):
+    """NEXT-4: the Bloch-phase kernel tabulated on the GPU (k_pgf_table_bloch, fp64) equals the
+    host table, itself pinned to the oracle (tests/test_oracle_bloch.py)."""
+    dev = lib_context(key, device=0)
+    host = lib_context(key, device=-1)
+    Kd, Gd = dev.build_pgf_bloch(k0)
+    Kh, Gh = host.build_pgf_bloch(k0)
+    assert np.abs(Kd - Kh).max() <= 1e-12 * np.abs(Kh).max()
+    assert np.abs(Gd - Gh).max() <= 1e-12 * np.abs(Gh).max()
