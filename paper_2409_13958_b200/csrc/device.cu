@@ -378,21 +378,21 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
                                                       const int64_t* __restrict__ c_ptr, const unsigned long long* __restrict__ c_hdr,
                                                       const int* __restrict__ c_bidx,
                                                       const float4* __restrict__ c_val4, const float* __restrict__ q,
-                                                      const float* __restrict__ uloc, float* __restrict__ u) {
+                                                      const float* __restrict__ uloc, float* __restrict__ u, int64_t q4s) {
   const int lane = threadIdx.x & (G - 1);
   const int64_t n = rr.row0 + (int64_t)blockIdx.x * (blockDim.x / G) + (threadIdx.x / G);
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
   const int64_t b = valid ? c_ptr[n - rr.row0] : 0, e_end = valid ? c_ptr[n - rr.row0 + 1] : 0;
   if (F == 1 || F == 3) {
-    // B4: block index b, q4 = q viewed as float4 (aligned [4b, 4b+4)); U4: start column c,
-    // q4 = the per-evaluation shifted copy (q[c..c+3]) passed in place of q
+    // B4: block index b, q4 = q viewed as float4 (aligned [4b, 4b+4)); U4: start column c, q4 =
+    // the per-evaluation shifted copies q4x (passed in place of q), word (c & 3) * q4s + (c >> 2)
     const float4* q4 = reinterpret_cast<const float4*>(q);
 #pragma unroll 4
     for (int64_t e = b + lane; e < e_end; e += G) {
       const int bi = __ldg(c_bidx + e);
       const float4 vv = __ldg(c_val4 + e);
-      const float4 qq = __ldg(q4 + bi);
+      const float4 qq = __ldg(q4 + (F == 3 ? (int64_t)(bi & 3) * q4s + (bi >> 2) : (int64_t)bi));
       acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
     }
   } else if (F == 2) {
@@ -571,11 +571,15 @@ __global__ void __launch_bounds__(256) k4_seg(RowRange rr, const float* __restri
   if (valid && lane == 0) u[n] = acc + uloc[n];
 }
 
-// U4 C_box: q4[i] = (q[i], q[i+1], q[i+2], q[i+3]) (q carries 4 trailing zeros)
-__global__ void k_q4(int64_t n, const float* __restrict__ q, float4* __restrict__ q4) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  q4[i] = make_float4(q[i], q[i + 1], q[i + 2], q[i + 3]);
+// U4 C_box: four shifted float4 copies of q, q4x[r * S + k] = (q[4k+r], .., q[4k+r+3]), so the
+// q of the block starting at column c is q4x[(c & 3) * S + (c >> 2)] and consecutive blocks of a
+// run of columns (c, c+4, ..) read consecutive 16-byte words -- as dense as B4's aligned gathers
+// (a single copy q4[c] would put them 64 bytes apart).  q carries 16 trailing zeros.
+__global__ void k_q4(int64_t S, const float* __restrict__ q, float4* __restrict__ q4x) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= 4 * S) return;
+  const int64_t r = t / S, k = t - r * S, i = 4 * k + r;
+  q4x[t] = make_float4(q[i], q[i + 1], q[i + 2], q[i + 3]);
 }
 
 // ------------------------------------------------------------------ K5 gradient + sum
@@ -1022,9 +1026,13 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     D.tw32[a] = dupload(t32); D.tw64[a] = dupload(t64);
   }
   // q: + 4 zero floats so B4's aligned 4-column gathers stay in bounds
-  D.q = dalloc<float>(Np + 4); D.uloc = dalloc<float>(Np); D.u = dalloc<float>(Np);
-  if (D.cbox_format == 3) D.q4 = dalloc<float4>(Np);
-  CK(cudaMemset(D.q, 0, sizeof(float) * (size_t)(Np + 4)));
+  // q: + 16 zero floats so B4's aligned and U4's shifted 4-column gathers stay in bounds
+  D.q = dalloc<float>(Np + 16); D.uloc = dalloc<float>(Np); D.u = dalloc<float>(Np);
+  if (D.cbox_format == 3) {
+    D.q4s = (Np + 3) / 4 + 1;
+    D.q4 = dalloc<float4>(4 * D.q4s);
+  }
+  CK(cudaMemset(D.q, 0, sizeof(float) * (size_t)(Np + 16)));
   D.Q = dalloc<float>((size_t)D.n[0] * D.n[1] * D.n[2]);
   D.C = dalloc<float2>((size_t)D.H0 * D.P[1] * D.P[2]);
   D.spec = dalloc<float>((size_t)D.H0 * D.P[1] * D.P[2]);
@@ -1488,7 +1496,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   mark(3);
   const float4* v4 = reinterpret_cast<const float4*>(D.c_val);
   if (D.cbox_format == 3) {
-    k_q4<<<(unsigned)((D.Np + 255) / 256), 256, 0, st>>>(D.Np, D.q, D.q4);
+    k_q4<<<(unsigned)((4 * D.q4s + 255) / 256), 256, 0, st>>>(D.q4s, D.q, D.q4);
     CK(cudaGetLastError());
   }
   if (D.cbox_format == 2) {
@@ -1516,15 +1524,15 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   (D.cbox_format == 3                                                                                   \
        ? k4_interp_corr<PP, GG, 3><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4,                                \
-             reinterpret_cast<const float*>(D.q4), D.uloc, D.u)                                         \
+             reinterpret_cast<const float*>(D.q4), D.uloc, D.u, D.q4s)                                  \
    : D.cbox_format == 1                                                                                 \
        ? k4_interp_corr<PP, GG, 1><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
-             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0)   \
    : D.k4_vec                                                                                           \
        ? k4_interp_corr<PP, GG, 2><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
-             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u)               \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0)   \
        : k4_interp_corr<PP, GG, 0><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
-             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u))
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0))
 #define K4_BY_G(PP)                                                                                     \
   (D.k4_group == 8 ? K4_LAUNCH(PP, 8) : D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
     case 1: K4_BY_G(1); break;

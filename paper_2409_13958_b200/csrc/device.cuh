@@ -78,7 +78,8 @@ struct DeviceState {
   int64_t cbox_chunks = 0;             // C4x chunks or B4 blocks
   int cbox_format = 0;                // 0: C4x, 1: B4 (aligned 4-column blocks, c_bidx + c_val), 2: SEG,
                                       // 3: U4 (unaligned 4-column blocks, start in c_bidx, q4 gathers)
-  float4* q4 = nullptr;               // U4: per evaluation q4[i] = (q[i], q[i+1], q[i+2], q[i+3])
+  float4* q4 = nullptr;               // U4: per evaluation 4 shifted float4 copies of q (k_q4)
+  int64_t q4s = 0;                    // U4: words per copy
   SegGeom seg{};                      // SEG: candidate geometry
   int seg_maxseg = 0;                 // SEG: largest number of column runs of a row
   int64_t* seg_moff = nullptr;        // SEG: [N'+1] mask word offsets (c_ptr holds the value offsets)

@@ -48,6 +48,9 @@ def main():
     ap.add_argument("--settings", default="2,3;2,4;3,3;3,4")
     ap.add_argument("--ring", type=int, default=1)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--alpha-scale", type=float, default=None,
+                    help="Ewald splitting of the brute force (alpha-independent, tests/test_oracle_bf.py); "
+                         "default 3 for 3D periodicity (shorter real-space sum), 1 otherwise")
     a = ap.parse_args()
     from oracle import aim, bf, fem
     from oracle.heff import OracleModel
@@ -78,12 +81,16 @@ def main():
                          np.sin(th) * np.sin(k * xw[:, ax])], axis=1)
     fields = {"random": m_random(pm.n_parents, seed=77), "smooth": m_smooth}
     # brute force at the rows (C pair sums) -> H at the samples
+    from oracle.pgf import PgfSpec
+    import math
+    asc = a.alpha_scale if a.alpha_scale is not None else (3.0 if om.spec.dim == 3 else 1.0)
+    bf_spec = PgfSpec(om.periodic, om.lattice, alpha=asc * math.sqrt(math.pi) / om.spec.L.min())
     ref, hex_ = {}, {}
     t0 = time.time()
     for name, m in fields.items():
         q = om.charges(m)
         u = np.zeros(pm.n_parents)
-        u[rows] = bf.potential(xw[rows], xw, q, om.spec) + bf.pgf_self(om.spec) * q[rows] + om.u_loc(m)[rows]
+        u[rows] = bf.potential(xw[rows], xw, q, bf_spec) + bf.pgf_self(bf_spec) * q[rows] + om.u_loc(m)[rows]
         ref[name] = fem.gradient_field(ops, u)[samples]
         hex_[name] = om.exchange(m)[samples]
     t_bf = time.time() - t0

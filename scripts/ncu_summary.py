@@ -58,7 +58,7 @@ def rep(path):
             elif v == "us":
                 u = units[i]
                 f = float(val.replace(",", ""))
-                f *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(u, 1.0)
+                f *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(u, 1.0)
                 val = "%.2f" % f
             d[v] = val
         out.append(d)
