@@ -38,19 +38,24 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not _stale():
+def build(force=False, verbose=False, checked=False):
+    """checked=True builds lib/libpmfem_checked.so with -DPMFEM_DEVICE_CHECKS (device-side bounds
+    asserts in the hot kernels; load it with PMFEM_LIB=checked) -- the memory-safety evidence used
+    in place of compute-sanitizer, which is closed on the GPU pool."""
+    lib = LIB if not checked else os.path.join(HERE, "lib", "libpmfem_checked.so")
+    if not checked and not force and not _stale():
         return LIB
-    os.makedirs(os.path.dirname(LIB), exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     objs = []
-    objdir = os.path.join(HERE, "lib", "obj")
+    objdir = os.path.join(HERE, "lib", "obj_checked" if checked else "obj")
     os.makedirs(objdir, exist_ok=True)
     procs = []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         cmd = [nvcc(), "-c", os.path.join(CSRC, src), "-o", obj, "-O3", "-std=c++17", "-lineinfo",
                "-Xcompiler", "-fPIC,-fopenmp,-O3", "-I", os.path.join(HERE, "..", "include"), "-I", nccl_dirs()[0],
-               "--expt-relaxed-constexpr"] + ARCH + os.environ.get("PMFEM_EXTRA_NVCC", "").split()
+               "--expt-relaxed-constexpr"] + ARCH + os.environ.get("PMFEM_EXTRA_NVCC", "").split() + \
+              (["-DPMFEM_DEVICE_CHECKS"] if checked else [])
         if src.endswith(".cpp"):
             cmd += ["-x", "cu"] if False else []
         procs.append((src, cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -66,14 +71,13 @@ def build(force=False, verbose=False):
     if failed:
         raise RuntimeError("libpmfem build failed")
     inc, libdir = nccl_dirs()
-    link = [nvcc(), "-shared", "-o", LIB] + objs + ARCH + ["-Xcompiler", "-fopenmp", "-lgomp", "-L", libdir,
+    link = [nvcc(), "-shared", "-o", lib] + objs + ARCH + ["-Xcompiler", "-fopenmp", "-lgomp", "-L", libdir,
                                                            "-l:libnccl.so.2", "-Xlinker", "-rpath=" + libdir]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode())
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -58,6 +58,7 @@ float __int_as_float_host(int32_t c) { float f; std::memcpy(&f, &c, 4); return f
 struct RowRange {
   int64_t row0, row1, hoff;
   int c0, c1, c2;          // user component of internal axis 0, 1, 2 (axis permutation of m, H)
+  int64_t ncol;            // columns (all rows, N') -- bounds of the gathered vectors (checked build)
 };
 
 // halo pack / unpack: buf[i*w + c] <-> v[idx[i]*w + c]
@@ -134,6 +135,7 @@ __global__ void __launch_bounds__(256) k1_local_in(
   for (; j < w1; j += SPLIT, e += 32 * SPLIT, e1 += 32 * SPLIT) {
     const float4 zc = ld_stream(s_zc + e);
     const float4 LD = ld_stream(s_LD + e1);
+    DCHECK(colof(zc) >= 0 && colof(zc) < rr.ncol);
     const float4 mc = m4[colof(zc)];
     const float dx = mc.x - mn.x, dy = mc.y - mn.y, dz = mc.z - mn.z;
     hx = fmaf(LD.x, dx, hx); hy = fmaf(LD.x, dy, hy); hz = fmaf(LD.x, dz, hz);
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(256) k1_local_in(
 #pragma unroll 4
   for (; j < w; j += SPLIT, e += 32 * SPLIT) {
     const float4 zc = ld_stream(s_zc + e);
+    DCHECK(colof(zc) >= 0 && colof(zc) < rr.ncol);
     const float4 mc = m4[colof(zc)];
     ul = fmaf(zc.x, mc.x - mn.x, fmaf(zc.y, mc.y - mn.y, fmaf(zc.z, mc.z - mn.z, ul)));
   }
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const in
   const int cz = nz == 0 ? 0 : (rz[1] - rz[0] + 1) + (nz == 2 ? rz[3] - rz[2] + 1 : 0);
   const int cy = ny == 0 ? 0 : (ry[1] - ry[0] + 1) + (ny == 2 ? ry[3] - ry[2] + 1 : 0);
   const int nseg = cz * cy * nx;
+  DCHECK(nseg <= 256 * 8 && nseg <= k2_nseg(T1, T2, P));
   // segment table: rows [box_ptr(line + xa), box_ptr(line + xb + 1)) clipped to [lo, hi)
   constexpr int PER = 8;                                   // segments per thread in the scan
   int cnt[PER];
@@ -329,6 +333,7 @@ __global__ void __launch_bounds__(256) k2_tile(GridDims g, TileDims td, const in
   if (qmax > 0.f) {
     for (int f = threadIdx.x; f < total; f += blockDim.x) {
       const int64_t i = row_of(f);
+      DCHECK(i >= lo && i < hi);
       const int4 s = __ldg(st_s + i);
       const float4 t = __ldg(st_t + i);
       const float qn = __ldg(q + i) * scale;
@@ -392,6 +397,7 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     for (int64_t e = b + lane; e < e_end; e += G) {
       const int bi = __ldg(c_bidx + e);
       const float4 vv = __ldg(c_val4 + e);
+      DCHECK(bi >= 0 && (F == 3 ? bi < rr.ncol : 4 * (int64_t)bi < rr.ncol + 4));
       const float4 qq = __ldg(q4 + (F == 3 ? (int64_t)(bi & 3) * q4s + (bi >> 2) : (int64_t)bi));
       acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
     }
@@ -431,6 +437,7 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     const int k1 = k0 + (int)((h >> 28) & 0xFFF);
     const int k2 = k1 + (int)((h >> 40) & 0xFFF);
     const int k3 = k2 + (int)(h >> 52);
+    DCHECK(k0 >= 0 && k3 < rr.ncol && k0 <= k1 && k1 <= k2 && k2 <= k3);
     acc = fmaf(vv.x, q[k0], acc);
     acc = fmaf(vv.y, q[k1], acc);
     acc = fmaf(vv.z, q[k2], acc);
@@ -455,6 +462,7 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
 #pragma unroll
         for (int b = 0; b <= P; ++b)
           if (a == jy && b == jz) wyz = wy[a] * wz[b];
+      DCHECK(wrapi(s.z + jz, g.n2, g.per2) < g.n2 && wrapi(s.y + jy, g.n1, g.per1) < g.n1 && ix[0] >= 0 && ix[P] < g.n0);
       const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
       float v = 0.f;
 #pragma unroll
@@ -604,6 +612,7 @@ __global__ void __launch_bounds__(256) k5_grad_sum(RowRange rr, const float* __r
 #pragma unroll 4
   for (int j = part; j < w1; j += SPLIT, e1 += 32 * SPLIT) {
     const float4 gc = ld_stream(s_Gc + e1);
+    DCHECK(colof(gc) >= 0 && colof(gc) < rr.ncol);
     const float du = u[colof(gc)] - un;
     gx = fmaf(gc.x, du, gx); gy = fmaf(gc.y, du, gy); gz = fmaf(gc.z, du, gz);
   }
@@ -1418,7 +1427,7 @@ void slab_conv_sim(DeviceState& D, cudaStream_t st) {
 
 // m, H: [hi-lo][3] rank-local rows (the full [N'][3] on a single GPU)
 void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, EvalMode mode) {
-  const RowRange rr{D.lo, D.hi, D.lo, D.axperm[0], D.axperm[1], D.axperm[2]};
+  const RowRange rr{D.lo, D.hi, D.lo, D.axperm[0], D.axperm[1], D.axperm[2], D.Np};
   const int64_t nrows = D.hi - D.lo;
   // a rank without rows (thin slab) still takes part in every collective: only its row kernels
   // are skipped (launch grids of zero blocks are invalid)

@@ -1,7 +1,17 @@
 // Device-side state of a context: fp32 operators in internal (box-sorted) order, the PGF
 // spectrum, FFT twiddles and scratch.
 #pragma once
+#include <cassert>
 #include <cuda_runtime.h>
+
+// device-side bounds checks of the hot kernels, compiled in only for the checked build
+// (build.py --checked, PMFEM_LIB=checked): the memory-safety evidence in place of
+// compute-sanitizer, which is closed on the GPU pool
+#ifdef PMFEM_DEVICE_CHECKS
+#define DCHECK(c) assert(c)
+#else
+#define DCHECK(c) ((void)0)
+#endif
 #include <cstdint>
 #include <vector>
 #include "pmfem_internal.h"

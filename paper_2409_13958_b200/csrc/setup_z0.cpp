@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <omp.h>
 #include "pmfem_internal.h"
 #include "z0_cone.cuh"
@@ -62,9 +63,36 @@ inline void unpack_shift(int code, int s[3]) {
   s[0] = code - 8;
 }
 
+// open-addressing set of a row's columns (~65 unique among ~1000 candidates): insertion without
+// sorting the candidates, then O(1) slot lookups
+struct ColSet {
+  static constexpr int CAP = 1024;
+  int32_t key[CAP];
+  int32_t val[CAP];
+  int n = 0;
+  void clear() { std::memset(key, 0xff, sizeof(key)); n = 0; }
+  int find_pos(int32_t c) const {
+    unsigned h = ((unsigned)c * 2654435761u) & (CAP - 1);
+    while (key[h] != -1 && key[h] != c) h = (h + 1) & (CAP - 1);
+    return (int)h;
+  }
+  bool insert(int32_t c) {               // false when the set is too full (caller falls back)
+    const int h = find_pos(c);
+    if (key[h] == c) return true;
+    if (n >= CAP / 2) return false;
+    key[h] = c;
+    ++n;
+    return true;
+  }
+  int& slot(int32_t c) { return val[find_pos(c)]; }
+};
+
+struct ItemFlagsW { int64_t key; int va; unsigned flags; };
 struct RowWork {
   std::vector<std::pair<int64_t, int>> near;   // (parent, shift code)
   std::vector<int64_t> U;                       // tet * NC + code
+  std::vector<ItemFlagsW> its;
+  ColSet cs;
 };
 
 }  // namespace
@@ -149,8 +177,14 @@ void setup_z0(HostSetup& S) {
           // near sources (point-charge subtraction)
           std::vector<int32_t>& cols = rcol[n];
           cols.clear();
-          struct ItemFlags { int64_t key; int va; unsigned flags; };
-          std::vector<ItemFlags> its;
+          W.cs.clear();
+          bool cs_ok = true;
+          auto add_col = [&](int32_t c) {
+            if (cs_ok && !W.cs.insert(c)) cs_ok = false;
+            cols.push_back(c);
+          };
+          std::vector<ItemFlagsW>& its = W.its;
+          its.clear();
           for (int64_t key : U) {
             const int64_t t = key / NC;
             int s[3];
@@ -167,7 +201,7 @@ void setup_z0(HostSetup& S) {
             }
             if (!flags) continue;
             its.push_back({key, va, flags});
-            for (int j = 0; j < 4; ++j) cols.push_back(S.pid[tv[j]]);
+            for (int j = 0; j < 4; ++j) add_col(S.pid[tv[j]]);
           }
           const double* xn = &S.xyz[3 * S.parent[n]];
           for (auto& pr : near) {
@@ -177,14 +211,23 @@ void setup_z0(HostSetup& S) {
             double d[3];
             for (int x = 0; x < 3; ++x) d[x] = xn[x] - xp[x] - ell[x] * S.L[x];
             if (d[0] == 0 && d[1] == 0 && d[2] == 0) continue;
-            cols.push_back((int32_t)pr.first);
-            for (int64_t e = S.ring1.rowptr[pr.first]; e < S.ring1.rowptr[pr.first + 1]; ++e) cols.push_back(S.ring1.col[e]);
+            add_col((int32_t)pr.first);
+            for (int64_t e = S.ring1.rowptr[pr.first]; e < S.ring1.rowptr[pr.first + 1]; ++e) add_col(S.ring1.col[e]);
           }
-          std::sort(cols.begin(), cols.end());
-          cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+          if (cs_ok) {                     // the set's unique columns, sorted; slots from the set
+            cols.clear();
+            for (int h = 0; h < ColSet::CAP; ++h)
+              if (W.cs.key[h] != -1) cols.push_back(W.cs.key[h]);
+            std::sort(cols.begin(), cols.end());
+            for (size_t i = 0; i < cols.size(); ++i) W.cs.slot(cols[i]) = (int)i;
+          } else {
+            std::sort(cols.begin(), cols.end());
+            cols.erase(std::unique(cols.begin(), cols.end()), cols.end());
+          }
           std::vector<double>& vals = rval[n];
           vals.assign(3 * cols.size(), 0.0);
           auto slot = [&](int32_t col) {
+            if (cs_ok) return W.cs.slot(col);
             return (int)(std::lower_bound(cols.begin(), cols.end(), col) - cols.begin());
           };
           for (auto& it : its) {

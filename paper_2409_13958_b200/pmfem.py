@@ -10,7 +10,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpmfem.so")
+# PMFEM_LIB=checked loads the build with device-side bounds asserts (build.py --checked)
+LIB_PATH = os.path.join(_HERE, "lib", "libpmfem_checked.so" if os.environ.get("PMFEM_LIB") == "checked"
+                        else "libpmfem.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError("libpmfem.so not built (%s); run __graft_entry__.build() or "
