@@ -16,6 +16,7 @@
 // independent loads in flight.  C_box (~10^2-10^3 entries per row) is CSR with rows padded to
 // a multiple of 4 and is read by one warp per row with 16-byte vector loads.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -393,13 +394,26 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     // B4: block index b, q4 = q viewed as float4 (aligned [4b, 4b+4)); U4: start column c, q4 =
     // the per-evaluation shifted copies q4x (passed in place of q), word (c & 3) * q4s + (c >> 2)
     const float4* q4 = reinterpret_cast<const float4*>(q);
-#pragma unroll 4
-    for (int64_t e = b + lane; e < e_end; e += G) {
-      const int bi = __ldg(c_bidx + e);
-      const float4 vv = __ldg(c_val4 + e);
-      DCHECK(bi >= 0 && (F == 3 ? bi < rr.ncol : 4 * (int64_t)bi < rr.ncol + 4));
-      const float4 qq = __ldg(q4 + (F == 3 ? (int64_t)(bi & 3) * q4s + (bi >> 2) : (int64_t)bi));
-      acc = fmaf(vv.x, qq.x, fmaf(vv.y, qq.y, fmaf(vv.z, qq.z, fmaf(vv.w, qq.w, acc))));
+    // explicitly batched: the U block indices and values of KB blocks per lane are loaded first
+    // (independent), then their KB q gathers -- the gather depends on its index, so without the
+    // batching every block paid two dependent memory round trips (ncu: 80 % long-scoreboard)
+    constexpr int KB = 4;
+    for (int64_t base = b + lane; base < e_end; base += KB * G) {
+      int bi[KB];
+      float4 vv[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int64_t e = base + (int64_t)j * G;
+        const bool ok = e < e_end;
+        bi[j] = ok ? __ldg(c_bidx + e) : 0;
+        vv[j] = ok ? __ldg(c_val4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        DCHECK(bi[j] >= 0 && (F == 3 ? bi[j] < rr.ncol : 4 * (int64_t)bi[j] < rr.ncol + 4));
+        const float4 qq = __ldg(q4 + (F == 3 ? (int64_t)(bi[j] & 3) * q4s + (bi[j] >> 2) : (int64_t)bi[j]));
+        acc = fmaf(vv[j].x, qq.x, fmaf(vv[j].y, qq.y, fmaf(vv[j].z, qq.z, fmaf(vv[j].w, qq.w, acc))));
+      }
     }
   } else if (F == 2) {
     // C4x with vector gathers for run chunks (deltas 1,1,1): the 4 consecutive q values come
@@ -428,20 +442,32 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
       }
       acc = fmaf(vv.x, a0, fmaf(vv.y, a1, fmaf(vv.z, a2, fmaf(vv.w, a3, acc))));
     }
-  } else
-#pragma unroll 2
-  for (int64_t e = b + lane; e < e_end; e += G) {
-    const unsigned long long h = __ldg(c_hdr + e);
-    const float4 vv = __ldg(c_val4 + e);
-    const int k0 = (int)(h & 0xFFFFFFFull);
-    const int k1 = k0 + (int)((h >> 28) & 0xFFF);
-    const int k2 = k1 + (int)((h >> 40) & 0xFFF);
-    const int k3 = k2 + (int)(h >> 52);
-    DCHECK(k0 >= 0 && k3 < rr.ncol && k0 <= k1 && k1 <= k2 && k2 <= k3);
-    acc = fmaf(vv.x, q[k0], acc);
-    acc = fmaf(vv.y, q[k1], acc);
-    acc = fmaf(vv.z, q[k2], acc);
-    acc = fmaf(vv.w, q[k3], acc);
+  } else {
+    // C4x, batched like B4/U4: KB headers + values first, then their 4 KB scalar gathers
+    constexpr int KB = 2;
+    for (int64_t base = b + lane; base < e_end; base += KB * G) {
+      unsigned long long h[KB];
+      float4 vv[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int64_t e = base + (int64_t)j * G;
+        const bool ok = e < e_end;
+        h[j] = ok ? __ldg(c_hdr + e) : 0ull;
+        vv[j] = ok ? __ldg(c_val4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int k0 = (int)(h[j] & 0xFFFFFFFull);
+        const int k1 = k0 + (int)((h[j] >> 28) & 0xFFF);
+        const int k2 = k1 + (int)((h[j] >> 40) & 0xFFF);
+        const int k3 = k2 + (int)(h[j] >> 52);
+        DCHECK(k0 >= 0 && k3 < rr.ncol && k0 <= k1 && k1 <= k2 && k2 <= k3);
+        acc = fmaf(vv[j].x, __ldg(q + k0), acc);
+        acc = fmaf(vv[j].y, __ldg(q + k1), acc);
+        acc = fmaf(vv[j].z, __ldg(q + k2), acc);
+        acc = fmaf(vv[j].w, __ldg(q + k3), acc);
+      }
+    }
   }
   // interpolation: lane r < (P+1)^2 takes one (y, z) stencil row and its P+1 x-consecutive
   // grid values (index maths once per row, not per point)
@@ -879,6 +905,14 @@ void launch_yz_fused(const DeviceState& D, cudaStream_t st) {
 
 void device_upload(DeviceState& D, const HostSetup& S) {
   CK(cudaSetDevice(D.device));
+  static const bool verbose = std::getenv("PMFEM_VERBOSE") != nullptr;
+  auto t_up0 = std::chrono::steady_clock::now();
+  auto upload_stage = [&](const char* what) {
+    if (!verbose) return;
+    CK(cudaDeviceSynchronize());
+    std::fprintf(stderr, "[pmfem]   upload %-18s %8.2f s\n", what,
+                 std::chrono::duration<double>(std::chrono::steady_clock::now() - t_up0).count());
+  };
   const int64_t Np = S.Np;
   D.Np = Np;
   D.order = S.order;
@@ -985,6 +1019,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
                          __int_as_float_host(s[0]));
   }
   D.rowsum = dupload(rsum); D.st_s = dupload(sts); D.st_t = dupload(stt);
+  upload_stage("SELL + stencils");
   // K2 reads the rows of each anchor line through box_ptr: rows must be sorted by anchor box
   {
     const int64_t Gb = (int64_t)D.n[0] * D.n[1] * D.n[2];
@@ -1029,6 +1064,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   // ---- C_box: built on the device in internal order, stored in the chunked C4x format
   if (!S.cbox_device) throw Error(PMFEM_E_STATE, "device contexts build C_box on the device");
   device_build_cbox(D, S);
+  upload_stage("C_box");
   for (int a = 0; a < 3; ++a) {
     std::vector<float2> t32; std::vector<double2> t64;
     twiddles<float>(D.P[a], t32); twiddles<double>(D.P[a], t64);

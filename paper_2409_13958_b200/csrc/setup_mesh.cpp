@@ -122,10 +122,13 @@ void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* p
   S.vol.resize(S.T);
   S.grads.resize(12 * S.T);
   double sumv = 0;
+  int64_t bad_index = -1;
+#pragma omp parallel for reduction(+ : sumv) reduction(max : bad_index)
   for (int64_t t = 0; t < S.T; ++t) {
     int32_t* v = &S.tets[4 * t];
-    for (int k = 0; k < 4; ++k)
-      require(v[k] >= 0 && v[k] < S.N, PMFEM_E_MESH, "tet index out of range at tet " + std::to_string(t));
+    bool ok = true;
+    for (int k = 0; k < 4; ++k) ok &= v[k] >= 0 && v[k] < S.N;
+    if (!ok) { bad_index = std::max(bad_index, t); continue; }
     const double* p0 = &S.xyz[3 * v[0]];
     double e[3][3];
     for (int k = 0; k < 3; ++k)
@@ -137,9 +140,13 @@ void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* p
     S.vol[t] = std::fabs(det) / 6.0;
     sumv += S.vol[t];
   }
+  require(bad_index < 0, PMFEM_E_MESH, "tet index out of range at tet " + std::to_string(bad_index));
   double meanv = sumv / S.T;
+  int64_t degenerate = -1;
+#pragma omp parallel for reduction(max : degenerate)
   for (int64_t t = 0; t < S.T; ++t)
-    require(S.vol[t] >= 1e-12 * meanv, PMFEM_E_MESH, "degenerate tetrahedron " + std::to_string(t));
+    if (!(S.vol[t] >= 1e-12 * meanv)) degenerate = std::max(degenerate, t);
+  require(degenerate < 0, PMFEM_E_MESH, "degenerate tetrahedron " + std::to_string(degenerate));
 
   // element gradients grad(phi_i) = rows of J^-1 (J columns = P_i - P_0), phi_0 = 1 - sum
   double min_edge2 = 1e300;
