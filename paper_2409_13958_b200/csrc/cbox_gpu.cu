@@ -438,7 +438,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   // mask walk are latency-bound, profiles/ab/r02_*): candidate reach R_a = ceil(rho_a + 1) - 1, rho_a = r_ER / Delta_a; usable
   // when every row's near set (the for_near count above) is found among its candidates
   const char* fmt_env = std::getenv("PMFEM_CBOX_FORMAT");
-  const std::string fmt = fmt_env ? std::string(fmt_env) : std::string("u4");
+  const std::string fmt = fmt_env ? std::string(fmt_env) : std::string("auto");
   if (fmt == "seg" && D.world == 1) {
     SegGeom G{};
     for (int a = 0; a < 3; ++a) {
@@ -513,19 +513,24 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   CKC(cudaGetLastError());
   CKC(cudaMemcpy(nbk.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < Np; ++i) { cptr[i + 1] = cptr[i] + nch[i]; bptr[i + 1] = bptr[i] + nbk[i]; }
-  // B4 unless it streams > 15 % more bytes than C4x (its gathers are 4x fewer L1 requests:
-  // measured C2 +11 % bytes -> K4 4 % faster, C3 +33 % bytes -> 46 % slower);
-  // PMFEM_CBOX_FORMAT=c4x|b4 forces one (tests)
-  // U4 (default): never more blocks than B4 (greedy unaligned covering), one 16-byte q4 gather
-  // per block; PMFEM_CBOX_FORMAT=c4x|b4|u4|seg forces a format (tests, A/B)
+  // U4: never more blocks than B4 (greedy unaligned covering), one 16-byte gather per block from
+  // four shifted copies of q (4x q's footprint).  Measured (round 2, p = 3, s = 4, batched
+  // gathers; profiles/ab): U4 wins where the near columns form long runs and q is dense in the
+  // boxes (C4 9.64 vs C4x 9.87 ms, C5 2.03 vs B4 2.21 ms), C4x where the runs are short and
+  // sparse (C3, 0.74 nodes per box: 0.53 vs U4 0.73 ms).  Default: U4 when the mesh has >= 1
+  // node per grid box and U4 blocks hold >= 3.1 of their 4 slots, else C4x;
+  // PMFEM_CBOX_FORMAT=c4x|b4|u4|seg forces a format (tests, A/B)
+  std::vector<long long> nu(Np), uptr(Np + 1, 0);
+  k_u4_count<<<blocks, 128>>>(Np, d_ptr, d_col, d_nch);
+  CKC(cudaGetLastError());
+  CKC(cudaMemcpy(nu.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < Np; ++i) uptr[i + 1] = uptr[i] + nu[i];
+  const double per_box = (double)Nall / ((double)c.n[0] * c.n[1] * c.n[2]);
+  const double u4_fill = uptr[Np] ? (double)nnz / (double)uptr[Np] : 4.0;
   bool use_b4 = fmt == "b4";
-  const bool use_c4x = fmt == "c4x";
+  bool use_c4x = fmt == "c4x";
+  if (fmt != "b4" && fmt != "c4x" && fmt != "u4") use_c4x = !(per_box >= 1.0 && u4_fill >= 3.1);
   if (!use_b4 && !use_c4x) {
-    std::vector<long long> nu(Np), uptr(Np + 1, 0);
-    k_u4_count<<<blocks, 128>>>(Np, d_ptr, d_col, d_nch);
-    CKC(cudaGetLastError());
-    CKC(cudaMemcpy(nu.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
-    for (int64_t i = 0; i < Np; ++i) uptr[i + 1] = uptr[i] + nu[i];
     long long* d_uptr = dup_c(uptr);
     int* d_ustart = dalloc_c<int>(uptr[Np]);
     float* d_uval = dalloc_c<float>(4 * uptr[Np]);
