@@ -38,6 +38,52 @@ void build_tri_rules(TriRules& R);
 
 ZC_HD inline double zc_dot(const double* a, const double* b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
 
+// A sub-triangle of a face (F0, F1, F2) in dyadic barycentric form: vertex k is
+// F0 + (u_k E1 + v_k E2) / 2^depth with E1 = F1 - F0, E2 = F2 - F0 (exact for depth <= 7).
+struct DTri { short u[3], v[3], depth, pad; };
+ZC_HD inline DTri dtri_root() {
+  DTri t;
+  t.u[0] = 0; t.v[0] = 0; t.u[1] = 1; t.v[1] = 0; t.u[2] = 0; t.v[2] = 1; t.depth = 0; t.pad = 0;
+  return t;
+}
+ZC_HD inline void dtri_vertices(const double* F0, const double* E1, const double* E2, const DTri& t, double V[3][3]) {
+  const double s = 1.0 / (double)(1 << t.depth);
+  for (int k = 0; k < 3; ++k)
+    for (int x = 0; x < 3; ++x) V[k][x] = F0[x] + ((double)t.u[k] * E1[x] + (double)t.v[k] * E2[x]) * s;
+}
+// the 4 children (corner 0, corner 1, corner 2, centre) in the order of the round-1 subdivision
+ZC_HD inline void dtri_children(const DTri& t, DTri* c) {
+  short U[3], Vv[3], mu[3], mv[3];
+  for (int k = 0; k < 3; ++k) { U[k] = 2 * t.u[k]; Vv[k] = 2 * t.v[k]; }
+  // midpoints m01, m02, m12
+  mu[0] = t.u[0] + t.u[1]; mv[0] = t.v[0] + t.v[1];
+  mu[1] = t.u[0] + t.u[2]; mv[1] = t.v[0] + t.v[2];
+  mu[2] = t.u[1] + t.u[2]; mv[2] = t.v[1] + t.v[2];
+  const short cu[4][3] = {{U[0], mu[0], mu[1]}, {mu[0], U[1], mu[2]}, {mu[1], mu[2], U[2]}, {mu[2], mu[1], mu[0]}};
+  const short cv[4][3] = {{Vv[0], mv[0], mv[1]}, {mv[0], Vv[1], mv[2]}, {mv[1], mv[2], Vv[2]}, {mv[2], mv[1], mv[0]}};
+  for (int i = 0; i < 4; ++i) {
+    for (int k = 0; k < 3; ++k) { c[i].u[k] = cu[i][k]; c[i].v[k] = cv[i][k]; }
+    c[i].depth = t.depth + 1;
+    c[i].pad = 0;
+  }
+}
+// size (longest edge) and the distance lower bound max(|h|, |centroid - o| - circumradius)
+ZC_HD inline void dtri_measure(const double V[3][3], const double* o, double h, double& size, double& dest) {
+  double cen[3], e01[3], e02[3], e12[3];
+  for (int x = 0; x < 3; ++x) {
+    cen[x] = (V[0][x] + V[1][x] + V[2][x]) / 3.0;
+    e01[x] = V[1][x] - V[0][x]; e02[x] = V[2][x] - V[0][x]; e12[x] = V[2][x] - V[1][x];
+  }
+  size = sqrt(fmax(zc_dot(e01, e01), fmax(zc_dot(e02, e02), zc_dot(e12, e12))));
+  double rc = 0;
+  for (int k = 0; k < 3; ++k) {
+    const double d[3] = {V[k][0] - cen[0], V[k][1] - cen[1], V[k][2] - cen[2]};
+    rc = fmax(rc, sqrt(zc_dot(d, d)));
+  }
+  const double dc[3] = {cen[0] - o[0], cen[1] - o[1], cen[2] - o[2]};
+  dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
+}
+
 struct ConeIntegrator {
   double P[4][3], g[4][3], c[4];     // phi_i(r) = c_i + g_i . r
   double o[3], a[4];
@@ -74,47 +120,28 @@ struct ConeIntegrator {
     }
   }
 
-  // adaptive face integral: split into 4 while size > dest (distance lower bound), depth <= 7
+  // adaptive face integral: split into 4 while size > split * dest (distance lower bound),
+  // depth <= 7; sub-triangles in dyadic barycentric form (DTri, shared with the GPU's
+  // breadth-first version in z0_gpu.cu: the same leaves, the same vertex arithmetic).  The
+  // depth-first stack never overflows (3 per level + 4 <= 24 for depth < 7), so the leaf set does
+  // not depend on the traversal order.
   ZC_HD void face(const double* F0, const double* F1, const double* F2, double h) {
-    struct Tri { double v[3][3]; int depth; };
-    Tri stack[24];
-    int top = 0;
-    for (int x = 0; x < 3; ++x) { stack[0].v[0][x] = F0[x]; stack[0].v[1][x] = F1[x]; stack[0].v[2][x] = F2[x]; }
-    stack[0].depth = 0;
-    top = 1;
+    double E1[3], E2[3];
+    for (int x = 0; x < 3; ++x) { E1[x] = F1[x] - F0[x]; E2[x] = F2[x] - F0[x]; }
+    DTri stack[24];
+    int top = 1;
+    stack[0] = dtri_root();
     while (top > 0) {
-      const Tri T = stack[--top];
-      const double* V0 = T.v[0];
-      const double* V1 = T.v[1];
-      const double* V2 = T.v[2];
-      double cen[3], e01[3], e02[3], e12[3];
-      for (int x = 0; x < 3; ++x) {
-        cen[x] = (V0[x] + V1[x] + V2[x]) / 3.0;
-        e01[x] = V1[x] - V0[x]; e02[x] = V2[x] - V0[x]; e12[x] = V2[x] - V1[x];
-      }
-      const double size = sqrt(fmax(zc_dot(e01, e01), fmax(zc_dot(e02, e02), zc_dot(e12, e12))));
-      double rc = 0;
-      for (int k = 0; k < 3; ++k) {
-        const double d[3] = {T.v[k][0] - cen[0], T.v[k][1] - cen[1], T.v[k][2] - cen[2]};
-        rc = fmax(rc, sqrt(zc_dot(d, d)));
-      }
-      const double dc[3] = {cen[0] - o[0], cen[1] - o[1], cen[2] - o[2]};
-      const double dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
-      if (size > R->split * dest && T.depth < 7 && top + 4 <= 24) {
-        double m01[3], m02[3], m12[3];
-        for (int x = 0; x < 3; ++x) {
-          m01[x] = 0.5 * (V0[x] + V1[x]); m02[x] = 0.5 * (V0[x] + V2[x]); m12[x] = 0.5 * (V1[x] + V2[x]);
-        }
-        const double* kids[4][3] = {{V0, m01, m02}, {m01, V1, m12}, {m02, m12, V2}, {m12, m02, m01}};
-        for (int c4 = 0; c4 < 4; ++c4) {
-          Tri& N = stack[top++];
-          for (int k = 0; k < 3; ++k)
-            for (int x = 0; x < 3; ++x) N.v[k][x] = kids[c4][k][x];
-          N.depth = T.depth + 1;
-        }
+      const DTri T = stack[--top];
+      double V[3][3], size, dest;
+      dtri_vertices(F0, E1, E2, T, V);
+      dtri_measure(V, o, h, size, dest);
+      if (size > R->split * dest && T.depth < 7) {
+        dtri_children(T, stack + top);
+        top += 4;
         continue;
       }
-      quad(V0, V1, V2, h, size, dest);
+      quad(V[0], V[1], V[2], h, size, dest);
     }
   }
 

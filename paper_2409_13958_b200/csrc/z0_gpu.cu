@@ -72,17 +72,24 @@ __global__ void k_z0_items(const Z0Item* __restrict__ items, int64_t nitems, con
 // ---- one warp per task
 constexpr int Z0W_WARPS = 4;           // warps per CTA
 constexpr int Z0W_LEAVES = 48;         // leaf buffer per warp (flushed when full)
-constexpr int Z0W_STACK = 24;          // subdivision stack per warp (as ConeIntegrator::face)
+constexpr int Z0W_POP = 16;            // sub-triangles examined per step (one per lane 0..15)
+constexpr int Z0W_STACK = 512;         // >= 1 + 7 levels x 4 Z0W_POP: never overflows (see below)
 
 struct Z0Leaf { double v[9]; double wf; int rule; };
-struct Z0Tri { double v[9]; int depth; };
 struct Z0Warp {
   Z0Leaf leaf[Z0W_LEAVES];
-  Z0Tri stack[Z0W_STACK];
+  DTri stack[Z0W_STACK];
   double g[4][3], c[4], a[4], o[3];
   int start[Z0W_LEAVES + 1];
 };
 
+// The task's faces are subdivided by the whole warp: each step pops up to Z0W_POP sub-triangles
+// from the top of a shared stack (lanes 0..15 measure one each, ConeIntegrator's rule: split
+// while size > split * dest and depth < 7), pushes the children of the splitting ones (<= 64) and
+// appends the others to the leaf buffer.  Depths on the stack never decrease towards the top and
+// each push is one group of <= 64 of the next depth, so the stack holds <= 1 + 7 x 64 entries.
+// The leaf SET equals the host's depth-first one (the split test does not depend on the order);
+// the quadrature of the leaves is shared by all 32 lanes.
 __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
     const Z0Item* __restrict__ items, int64_t nitems, const double* __restrict__ xyz, const int32_t* __restrict__ tets,
     const int64_t* __restrict__ parent, const double* __restrict__ Ms_tet, Lat lat, const TriRules* __restrict__ rules,
@@ -94,6 +101,7 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
     reinterpret_cast<double*>(&R)[i] = reinterpret_cast<const double*>(rules)[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
   Z0Warp& w = W[wid];
   for (int64_t it_i = (int64_t)blockIdx.x * Z0W_WARPS + wid; it_i < nitems; it_i += (int64_t)gridDim.x * Z0W_WARPS) {
     const Z0Item it = items[it_i];
@@ -125,101 +133,88 @@ __global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
     double Mo[23];
 #pragma unroll
     for (int i = 0; i < 23; ++i) Mo[i] = 0.0;
+    int nleaf = 0;
+    // quadrature of the buffered leaves: their points flattened over the 32 lanes
+    auto flush = [&]() {
+      if (lane == 0) {
+        int acc = 0;
+        for (int l = 0; l < nleaf; ++l) { w.start[l] = acc; acc += R.cnt[w.leaf[l].rule]; }
+        w.start[nleaf] = acc;
+      }
+      __syncwarp();
+      const int npts = w.start[nleaf];
+      int l = 0;
+      for (int gq = lane; gq < npts; gq += 32) {
+        while (gq >= w.start[l + 1]) ++l;
+        const Z0Leaf& L = w.leaf[l];
+        const int q = R.off[L.rule] + (gq - w.start[l]);
+        double y[3], Rv[3];
+        for (int x = 0; x < 3; ++x) {
+          y[x] = R.l0[q] * L.v[x] + R.l1[q] * L.v[3 + x] + R.l2[q] * L.v[6 + x];
+          Rv[x] = y[x] - w.o[x];
+        }
+        const double inv = rsqrt(zc_dot(Rv, Rv));
+        const double wt = R.w[q] * L.wf;
+        const double wi = wt * inv, w3 = wi * inv * inv;
+        const double x = Rv[0], yy = Rv[1], z = Rv[2];
+        Mo[0] += wi;
+        Mo[1] += wi * x; Mo[2] += wi * yy; Mo[3] += wi * z;
+        Mo[4] += w3 * x; Mo[5] += w3 * yy; Mo[6] += w3 * z;
+        const double xx = w3 * x * x, xy = w3 * x * yy, xz = w3 * x * z, yv = w3 * yy * yy, yz = w3 * yy * z,
+                     zz = w3 * z * z;
+        Mo[7] += xx; Mo[8] += xy; Mo[9] += xz; Mo[10] += yv; Mo[11] += yz; Mo[12] += zz;
+        Mo[13] += xx * x; Mo[14] += xx * yy; Mo[15] += xx * z; Mo[16] += xy * yy; Mo[17] += xy * z;
+        Mo[18] += xz * z; Mo[19] += yv * yy; Mo[20] += yv * z; Mo[21] += yz * z; Mo[22] += zz * z;
+      }
+      __syncwarp();
+      nleaf = 0;
+    };
     for (int j = 0; j < 4; ++j) {
       if (it.va >= 0 && j != it.va) continue;                 // warp-uniform
       const double gn = sqrt(zc_dot(w.g[j], w.g[j]));
       const double h = w.a[j] / gn;                            // phi_j(o) = |g_j| h_j
       if (fabs(h) * gn < 1e-14) continue;
-      int top = 0;
-      if (lane == 0) {
-        const int f[3] = {(j + 1) % 4, (j + 2) % 4, (j + 3) % 4};
-        for (int k = 0; k < 3; ++k)
-          for (int x = 0; x < 3; ++x) w.stack[0].v[3 * k + x] = P[f[k]][x];
-        w.stack[0].depth = 0;
-        top = 1;
-      }
-      while (true) {
-        int nleaf = 0;
-        if (lane == 0) {          // adaptive subdivision (ConeIntegrator::face) until empty or full
-          while (top > 0 && nleaf < Z0W_LEAVES) {
-            const Z0Tri T = w.stack[--top];
-            const double* V0 = T.v;
-            const double* V1 = T.v + 3;
-            const double* V2 = T.v + 6;
-            double cen[3], e01[3], e02[3], e12[3];
-            for (int x = 0; x < 3; ++x) {
-              cen[x] = (V0[x] + V1[x] + V2[x]) / 3.0;
-              e01[x] = V1[x] - V0[x]; e02[x] = V2[x] - V0[x]; e12[x] = V2[x] - V1[x];
-            }
-            const double size = sqrt(fmax(zc_dot(e01, e01), fmax(zc_dot(e02, e02), zc_dot(e12, e12))));
-            double rc = 0;
-            for (int k = 0; k < 3; ++k) {
-              const double d[3] = {T.v[3 * k] - cen[0], T.v[3 * k + 1] - cen[1], T.v[3 * k + 2] - cen[2]};
-              rc = fmax(rc, sqrt(zc_dot(d, d)));
-            }
-            const double dc[3] = {cen[0] - w.o[0], cen[1] - w.o[1], cen[2] - w.o[2]};
-            const double dest = fmax(fabs(h), sqrt(zc_dot(dc, dc)) - rc);
-            if (size > R.split * dest && T.depth < 7 && top + 4 <= Z0W_STACK) {
-              double m01[3], m02[3], m12[3];
-              for (int x = 0; x < 3; ++x) {
-                m01[x] = 0.5 * (V0[x] + V1[x]); m02[x] = 0.5 * (V0[x] + V2[x]); m12[x] = 0.5 * (V1[x] + V2[x]);
-              }
-              const double* kids[4][3] = {{V0, m01, m02}, {m01, V1, m12}, {m02, m12, V2}, {m12, m02, m01}};
-              for (int c4 = 0; c4 < 4; ++c4) {
-                Z0Tri& N = w.stack[top++];
-                for (int k = 0; k < 3; ++k)
-                  for (int x = 0; x < 3; ++x) N.v[3 * k + x] = kids[c4][k][x];
-                N.depth = T.depth + 1;
-              }
-              continue;
-            }
-            // leaf: the rule by size / distance (ConeIntegrator::quad), weight area2 * h
-            const double cr[3] = {e01[1] * e02[2] - e01[2] * e02[1], e01[2] * e02[0] - e01[0] * e02[2],
-                                  e01[0] * e02[1] - e01[1] * e02[0]};
-            const double ratio = size / dest;
-            Z0Leaf& L = w.leaf[nleaf];
-            for (int k = 0; k < 9; ++k) L.v[k] = T.v[k];
-            L.wf = sqrt(zc_dot(cr, cr)) * h;
-            L.rule = tri_rule(R, ratio);
-            w.start[nleaf + 1] = 0;
-            ++nleaf;
-          }
-          int acc = 0;
-          for (int l = 0; l < nleaf; ++l) { w.start[l] = acc; acc += R.cnt[w.leaf[l].rule]; }
-          w.start[nleaf] = acc;
+      const int f0 = (j + 1) % 4, f1 = (j + 2) % 4, f2 = (j + 3) % 4;
+      double F0[3], E1[3], E2[3];
+      for (int x = 0; x < 3; ++x) { F0[x] = P[f0][x]; E1[x] = P[f1][x] - P[f0][x]; E2[x] = P[f2][x] - P[f0][x]; }
+      if (lane == 0) w.stack[0] = dtri_root();
+      int top = 1;
+      __syncwarp();
+      while (top > 0) {
+        const int np = top < Z0W_POP ? top : Z0W_POP;
+        const int base = top - np;
+        const bool act = lane < np;
+        DTri T = dtri_root();
+        double V[3][3], size = 0.0, dest = 1.0;
+        bool split = false;
+        if (act) {
+          T = w.stack[base + lane];
+          dtri_vertices(F0, E1, E2, T, V);
+          dtri_measure(V, w.o, h, size, dest);
+          split = size > R.split * dest && T.depth < 7;
         }
-        __syncwarp();
-        nleaf = __shfl_sync(0xffffffffu, nleaf, 0);
-        const int more = __shfl_sync(0xffffffffu, top, 0);
-        const int npts = w.start[nleaf];
-        int l = 0;
-        for (int gq = lane; gq < npts; gq += 32) {
-          while (gq >= w.start[l + 1]) ++l;
-          const Z0Leaf& L = w.leaf[l];
-          const int q = R.off[L.rule] + (gq - w.start[l]);
-          double y[3], Rv[3];
-          for (int x = 0; x < 3; ++x) {
-            y[x] = R.l0[q] * L.v[x] + R.l1[q] * L.v[3 + x] + R.l2[q] * L.v[6 + x];
-            Rv[x] = y[x] - w.o[x];
-          }
-          const double inv = rsqrt(zc_dot(Rv, Rv));
-          const double wt = R.w[q] * L.wf;
-          const double wi = wt * inv, w3 = wi * inv * inv;
-          const double x = Rv[0], yy = Rv[1], z = Rv[2];
-          Mo[0] += wi;
-          Mo[1] += wi * x; Mo[2] += wi * yy; Mo[3] += wi * z;
-          Mo[4] += w3 * x; Mo[5] += w3 * yy; Mo[6] += w3 * z;
-          const double xx = w3 * x * x, xy = w3 * x * yy, xz = w3 * x * z, yv = w3 * yy * yy, yz = w3 * yy * z,
-                       zz = w3 * z * z;
-          Mo[7] += xx; Mo[8] += xy; Mo[9] += xz; Mo[10] += yv; Mo[11] += yz; Mo[12] += zz;
-          Mo[13] += xx * x; Mo[14] += xx * yy; Mo[15] += xx * z; Mo[16] += xy * yy; Mo[17] += xy * z;
-          Mo[18] += xz * z; Mo[19] += yv * yy; Mo[20] += yv * z; Mo[21] += yz * z; Mo[22] += zz * z;
+        const unsigned bs = __ballot_sync(0xffffffffu, split), bl = __ballot_sync(0xffffffffu, act && !split);
+        __syncwarp();                                          // every lane has read its entry
+        const int nl = __popc(bl);
+        if (nleaf + nl > Z0W_LEAVES) flush();
+        if (act && !split) {
+          double e01[3], e02[3];
+          for (int x = 0; x < 3; ++x) { e01[x] = V[1][x] - V[0][x]; e02[x] = V[2][x] - V[0][x]; }
+          const double cr[3] = {e01[1] * e02[2] - e01[2] * e02[1], e01[2] * e02[0] - e01[0] * e02[2],
+                                e01[0] * e02[1] - e01[1] * e02[0]};
+          Z0Leaf& L = w.leaf[nleaf + __popc(bl & lt)];
+          for (int k = 0; k < 3; ++k)
+            for (int x = 0; x < 3; ++x) L.v[3 * k + x] = V[k][x];
+          L.wf = sqrt(zc_dot(cr, cr)) * h;
+          L.rule = tri_rule(R, size / dest);
         }
+        if (split) dtri_children(T, &w.stack[base + 4 * __popc(bs & lt)]);
+        nleaf += nl;
+        top = base + 4 * __popc(bs);
         __syncwarp();
-        if (!more) break;
-        top = more;
       }
     }
+    if (nleaf > 0) flush();
     // butterfly: every lane gets the task's moments
 #pragma unroll
     for (int i = 0; i < 23; ++i)
