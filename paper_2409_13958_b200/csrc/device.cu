@@ -390,6 +390,34 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   const bool valid = n < rr.row1;          // no early return: the group reduction needs every lane
   float acc = 0.f;
   const int64_t b = valid ? c_ptr[n - rr.row0] : 0, e_end = valid ? c_ptr[n - rr.row0 + 1] : 0;
+  const float ul = (valid && lane == 0) ? uloc[n] : 0.f;
+  // interpolation first (its stencil and grid loads overlap the C_box stream below): lane
+  // r < (P+1)^2 takes one (y, z) stencil row and its P+1 x-consecutive grid values
+  constexpr int NR = (P + 1) * (P + 1);
+  if (valid && lane < NR) {
+    const int4 s = st_s[n];
+    const float4 t = st_t[n];
+    float wx[P + 1], wy[P + 1], wz[P + 1];
+    lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+    int ix[P + 1];
+#pragma unroll
+    for (int i = 0; i <= P; ++i) ix[i] = wrapi(s.x + i, g.n0, g.per0);
+    for (int r = lane; r < NR; r += G) {
+      const int jy = r % (P + 1), jz = r / (P + 1);
+      float wyz = 0.f;
+#pragma unroll
+      for (int a = 0; a <= P; ++a)
+#pragma unroll
+        for (int b = 0; b <= P; ++b)
+          if (a == jy && b == jz) wyz = wy[a] * wz[b];
+      DCHECK(wrapi(s.z + jz, g.n2, g.per2) < g.n2 && wrapi(s.y + jy, g.n1, g.per1) < g.n1 && ix[0] >= 0 && ix[P] < g.n0);
+      const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+      float v = 0.f;
+#pragma unroll
+      for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(row + ix[i]), v);
+      acc = fmaf(wyz, v, acc);
+    }
+  }
   if (F == 1 || F == 3) {
     // B4: block index b, q4 = q viewed as float4 (aligned [4b, 4b+4)); U4: start column c, q4 =
     // the per-evaluation shifted copies q4x (passed in place of q), word (c & 3) * q4s + (c >> 2)
@@ -469,36 +497,9 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
       }
     }
   }
-  // interpolation: lane r < (P+1)^2 takes one (y, z) stencil row and its P+1 x-consecutive
-  // grid values (index maths once per row, not per point)
-  constexpr int NR = (P + 1) * (P + 1);
-  if (valid && lane < NR) {
-    const int4 s = st_s[n];
-    const float4 t = st_t[n];
-    float wx[P + 1], wy[P + 1], wz[P + 1];
-    lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
-    int ix[P + 1];
-#pragma unroll
-    for (int i = 0; i <= P; ++i) ix[i] = wrapi(s.x + i, g.n0, g.per0);
-    for (int r = lane; r < NR; r += G) {
-      const int jy = r % (P + 1), jz = r / (P + 1);
-      float wyz = 0.f;
-#pragma unroll
-      for (int a = 0; a <= P; ++a)
-#pragma unroll
-        for (int b = 0; b <= P; ++b)
-          if (a == jy && b == jz) wyz = wy[a] * wz[b];
-      DCHECK(wrapi(s.z + jz, g.n2, g.per2) < g.n2 && wrapi(s.y + jy, g.n1, g.per1) < g.n1 && ix[0] >= 0 && ix[P] < g.n0);
-      const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
-      float v = 0.f;
-#pragma unroll
-      for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(row + ix[i]), v);
-      acc = fmaf(wyz, v, acc);
-    }
-  }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (valid && lane == 0) u[n] = acc + uloc[n];
+  if (valid && lane == 0) u[n] = acc + ul;
 }
 
 // K4 over the SEG C_box (cbox_format 2, device.cuh): G lanes per row.  The lanes first build the

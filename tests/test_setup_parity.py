@@ -3,7 +3,7 @@
 The library (C++, cone-decomposition quadrature, hashed PBC detection, box-list near search,
 GPU-style FFT layout) and the oracle (NumPy/SciPy, Duffy quadrature, KD-tree search) share no
 code; both follow PAPER.md and the SURVEY.md 8(c) contract.  Bars: exact for integer data,
-1e-12 relative for closed-form assembly, 1e-7 relative for Z0 (two independent quadratures),
+1e-12 relative for closed-form assembly, 3e-8 relative for Z0 (two independent quadratures),
 1e-12 for the PGF spectrum.
 """
 import numpy as np
@@ -63,8 +63,10 @@ def test_z0(pair):
         r = Zo.sum(axis=1)
         np.fill_diagonal(Zo, 0)
         scale = np.abs(Zo).max()
-        assert np.abs(Z[:, :, x] - Zo).max() <= 1e-7 * scale
-        assert np.abs(rs[:, x] - r).max() <= 1e-7 * scale
+        # two independent quadratures (signed-cone adaptive Gauss vs Duffy + tensor Gauss), each at
+        # ~1e-9 .. 1e-8 of max |Z0| (measured worst 9.5e-9 on R1p2)
+        assert np.abs(Z[:, :, x] - Zo).max() <= 3e-8 * scale
+        assert np.abs(rs[:, x] - r).max() <= 3e-8 * scale
 
 
 def test_grid_stencils_cbox(pair):
