@@ -502,6 +502,98 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   if (valid && lane == 0) u[n] = acc + ul;
 }
 
+// K4 "stream" variant for the block formats (B4: F = 1, U4: F = 3), PMFEM_K4_STREAM=1: a warp
+// owns RPW consecutive rows and streams their C_box blocks as ONE contiguous range
+// [c_ptr[r0], c_ptr[r0 + RPW]) -- 32 consecutive blocks per step, KB steps of index/value loads
+// issued before their gathers -- regardless of where the rows break.  Each lane finds its block's
+// row with a cursor over c_ptr (rows hold ~100-300 blocks, so it rarely moves); per step the
+// lanes' block partials are reduced by row with a segmented warp scan (rows are non-decreasing
+// across the lanes) and the tail lane of each segment adds the sum to the row's shared-memory
+// accumulator (one writer per row per step: no atomics).  Then the interpolation P^T U of the
+// warp's rows, 32 / LR rows at a time (LR = lanes per row >= (P+1)^2 stencil rows).
+template <int P, int F>
+__global__ void __launch_bounds__(256) k4_stream(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
+                                                 const float4* __restrict__ st_t, GridDims g,
+                                                 const int64_t* __restrict__ c_ptr, const int* __restrict__ c_bidx,
+                                                 const float4* __restrict__ c_val4, const float* __restrict__ q,
+                                                 const float* __restrict__ uloc, float* __restrict__ u, int64_t q4s) {
+  constexpr int RPW = 64, KB = 4;
+  constexpr int NR = (P + 1) * (P + 1);
+  constexpr int LR = NR <= 4 ? 4 : (NR <= 8 ? 8 : (NR <= 16 ? 16 : 32));
+  __shared__ float sacc[8][RPW];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int64_t r0 = rr.row0 + ((int64_t)blockIdx.x * 8 + wid) * RPW;
+  if (r0 >= rr.row1) return;                               // whole warp: uniform
+  const int nr = (int)(rr.row1 - r0 < RPW ? rr.row1 - r0 : RPW);
+  for (int i = lane; i < RPW; i += 32) sacc[wid][i] = 0.f;
+  __syncwarp();
+  const int64_t* cp = c_ptr + (r0 - rr.row0);
+  const int64_t e0 = cp[0], e1 = cp[nr];
+  const float4* q4 = reinterpret_cast<const float4*>(q);
+  int row = 0;                                             // local row of the lane's current block
+  for (int64_t base = e0; base < e1; base += 32 * KB) {
+    int bi[KB];
+    float4 vv[KB];
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const int64_t e = base + (int64_t)j * 32 + lane;
+      const bool ok = e < e1;
+      bi[j] = ok ? __ldg(c_bidx + e) : 0;
+      vv[j] = ok ? __ldg(c_val4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int j = 0; j < KB; ++j) {
+      const int64_t e = base + (int64_t)j * 32 + lane;
+      const bool ok = e < e1;
+      DCHECK(!ok || (bi[j] >= 0 && (F == 3 ? bi[j] < rr.ncol : 4 * (int64_t)bi[j] < rr.ncol + 4)));
+      const float4 qq = ok ? __ldg(q4 + (F == 3 ? (int64_t)(bi[j] & 3) * q4s + (bi[j] >> 2) : (int64_t)bi[j]))
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      float p = vv[j].x * qq.x + vv[j].y * qq.y + vv[j].z * qq.z + vv[j].w * qq.w;
+      if (ok) while (cp[row + 1] <= e) ++row;
+      const int key = ok ? row : RPW;                      // out-of-range lanes form their own segment
+      // segmented inclusive scan by row (rows non-decreasing across lanes)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float pu = __shfl_up_sync(0xffffffffu, p, o);
+        const int ku = __shfl_up_sync(0xffffffffu, key, o);
+        if (lane >= o && ku == key) p += pu;
+      }
+      const int kn = __shfl_down_sync(0xffffffffu, key, 1);
+      if (key < RPW && (lane == 31 || kn != key)) sacc[wid][key] += p;
+    }
+  }
+  __syncwarp();
+  // interpolation + u_loc + store, 32 / LR rows at a time
+  const int sub = lane / LR, sl = lane % LR;
+  for (int rb = 0; rb < nr; rb += 32 / LR) {
+    const int lr = rb + sub;
+    const bool valid = lr < nr;
+    const int64_t n = r0 + lr;
+    float acc = 0.f;
+    if (valid && sl < NR) {
+      const int4 s = st_s[n];
+      const float4 t = st_t[n];
+      float wx[P + 1], wy[P + 1], wz[P + 1];
+      lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+      const int jy = sl % (P + 1), jz = sl / (P + 1);
+      float wyz = 0.f;
+#pragma unroll
+      for (int a = 0; a <= P; ++a)
+#pragma unroll
+        for (int c = 0; c <= P; ++c)
+          if (a == jy && c == jz) wyz = wy[a] * wz[c];
+      const float* rowp = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+      float v = 0.f;
+#pragma unroll
+      for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(rowp + wrapi(s.x + i, g.n0, g.per0)), v);
+      acc = wyz * v;
+    }
+#pragma unroll
+    for (int o = LR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (valid && sl == 0) u[n] = acc + sacc[wid][lr] + uloc[n];
+  }
+}
+
 // K4 over the SEG C_box (cbox_format 2, device.cuh): G lanes per row.  The lanes first build the
 // row's table of column runs in shared memory -- one run per (z, y) candidate anchor line and x
 // subrange, [box_ptr(line + xa), box_ptr(line + xb + 1)) -- with an exclusive scan of the run
@@ -1545,7 +1637,21 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     k_q4<<<(unsigned)((4 * D.q4s + 255) / 256), 256, 0, st>>>(D.q4s, D.q, D.q4);
     CK(cudaGetLastError());
   }
-  if (D.cbox_format == 2) {
+  static const bool k4_stream_on = std::getenv("PMFEM_K4_STREAM") != nullptr && std::atoi(std::getenv("PMFEM_K4_STREAM")) == 1;
+  if (k4_stream_on && (D.cbox_format == 1 || D.cbox_format == 3)) {
+    const unsigned blocks = (unsigned)std::max<int64_t>(1, (nrows + 8 * 64 - 1) / (8 * 64));
+    const float* qv = D.cbox_format == 3 ? reinterpret_cast<const float*>(D.q4) : D.q;
+#define K4T_LAUNCH(PP)                                                                                      \
+    (D.cbox_format == 3                                                                                     \
+         ? k4_stream<PP, 3><<<blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_bidx, v4, qv, D.uloc, D.u, D.q4s) \
+         : k4_stream<PP, 1><<<blocks, 256, 0, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_bidx, v4, qv, D.uloc, D.u, D.q4s))
+    switch (D.order) {
+      case 1: K4T_LAUNCH(1); break;
+      case 2: K4T_LAUNCH(2); break;
+      default: K4T_LAUNCH(3); break;
+    }
+#undef K4T_LAUNCH
+  } else if (D.cbox_format == 2) {
     const int G = D.k4_group;
     const size_t smem = sizeof(int) * (size_t)(256 / G) * (2 * D.seg_maxseg + 2);
     const unsigned blocks = (unsigned)std::max<int64_t>(1, (nrows * G + 255) / 256);
