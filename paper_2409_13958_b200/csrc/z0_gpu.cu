@@ -282,6 +282,7 @@ struct Z0Pipe {
     Z0Item* items = nullptr;
     int64_t* base = nullptr;
     double* vals = nullptr;
+    size_t items_cap = 0, base_cap = 0, vals_cap = 0;
     double* hvals = nullptr;       // pinned
     size_t hcap = 0;
     cudaEvent_t done = nullptr;
@@ -313,9 +314,19 @@ static void z0_finish_chunk(Z0Pipe::Chunk& c, std::vector<std::vector<double>>& 
     std::vector<double>& dst = rval[c.rows[j]];
     for (size_t e = 0; e < dst.size(); ++e) dst[e] += src[e];
   }
-  cudaFree(c.items); cudaFree(c.base); cudaFree(c.vals);
-  c.items = nullptr; c.base = nullptr; c.vals = nullptr;
-  c.busy = false;
+  c.busy = false;            // the slot's device buffers are kept (cudaFree would synchronise the device)
+}
+
+// grow-only device buffer of a pipeline slot (freed at z0_device_end)
+template <class T>
+static T* slot_buf(T*& p, size_t& cap, size_t n) {
+  n = std::max<size_t>(n, 1);
+  if (n > cap) {
+    if (p) CKZ(cudaFree(p));
+    CKZ(cudaMalloc(&p, n * sizeof(T)));
+    cap = n;
+  }
+  return p;
 }
 
 void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& titems,
@@ -335,9 +346,14 @@ void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& t
   c.rowbase.assign(nrows + 1, 0);
   for (int64_t j = 0; j < nrows; ++j) c.rowbase[j + 1] = c.rowbase[j] + 3 * (int64_t)rcol[rows[j]].size();
   const int64_t nvals = c.rowbase[nrows];
-  c.items = up(items.data(), items.size());
-  c.base = up(c.rowbase.data(), c.rowbase.size());
-  CKZ(cudaMalloc(&c.vals, std::max<int64_t>(nvals, 1) * sizeof(double)));
+  slot_buf(c.items, c.items_cap, items.size());
+  slot_buf(c.base, c.base_cap, c.rowbase.size());
+  slot_buf(c.vals, c.vals_cap, (size_t)std::max<int64_t>(nvals, 1));
+  // pageable sources: the copies return when staged; the private non-blocking stream orders them
+  // before the kernel without synchronising the device
+  if (!items.empty())
+    CKZ(cudaMemcpyAsync(c.items, items.data(), items.size() * sizeof(Z0Item), cudaMemcpyHostToDevice, P.st));
+  CKZ(cudaMemcpyAsync(c.base, c.rowbase.data(), c.rowbase.size() * sizeof(int64_t), cudaMemcpyHostToDevice, P.st));
   CKZ(cudaMemsetAsync(c.vals, 0, std::max<int64_t>(nvals, 1) * sizeof(double), P.st));
   if ((size_t)nvals > c.hcap) {
     if (c.hvals) cudaFreeHost(c.hvals);
@@ -376,6 +392,7 @@ void z0_device_end(std::vector<std::vector<double>>& rval) {
   for (auto& c : P.ch) {
     if (c.hvals) cudaFreeHost(c.hvals);
     c.hvals = nullptr; c.hcap = 0;
+    cudaFree(c.items); cudaFree(c.base); cudaFree(c.vals);
     cudaEventDestroy(c.done);
   }
   cudaFree(P.xyz); cudaFree(P.tets); cudaFree(P.parent); cudaFree(P.ms); cudaFree(P.rules);
