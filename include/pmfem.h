@@ -167,9 +167,36 @@ pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err);
  * complex spectrum / #FFT points (host fp64 FFT); exports "kernel_bloch" and "spectrum_bloch"
  * ([P2][P1][P0] complex, interleaved re/im).  k0[3] in rad/cm, user frame; must vanish on
  * non-periodic axes and must not be a reciprocal lattice vector (PMFEM_E_INVALID_ARG).
- * The complex field path (quasi-periodic m, complex H) is not built: the Bloch kernel feeds no
- * field evaluation yet. */
+ * The complex field path is pmfem_build_bloch / pmfem_*_bloch below. */
 pmfem_status pmfem_build_pgf_bloch(pmfem_ctx ctx, const double* k0, double target_rel_err);
+
+/* NEXT-4 complex field path.  Magnetisation amplitudes that are Bloch-periodic with the phase
+ * of Eq. 2, m(r + R) = exp(-j k0.R) m(r), have the potential
+ * u(r_n) = sum_m G_p(r_n - r_m; k0) q_m + Z0 terms, and everything in the static path carries
+ * over with phases (reading R21): folded local operators weight a tet entry between
+ * copies with lattice shifts s_a (row), s_b (column) by exp(j k0.L(s_a - s_b)); Z0 weights an
+ * element image by the shifts of its vertices; the AIM grid part runs on the modulated charges
+ * exp(j k0.r_n) q_n with the L-periodic kernel exp(j k0.r) G_p(r) (complex spectrum, nothing
+ * removed: k0 is off the reciprocal lattice) and the modulated precorrection.
+ * pmfem_build_bloch builds the Bloch kernel (as pmfem_build_pgf_bloch) and the phased operators
+ * (host fp64: ring-1 L/D/G, Z0 with host element integrals, C~) and uploads them; world = 1 only
+ * (PMFEM_E_STATE otherwise); k0 as in pmfem_build_pgf_bloch.  Replaces any previous Bloch build;
+ * the static path is unaffected.  On a host-only context the operators are kept for
+ * pmfem_export ("bloch_{r1,z0,cbox}_{rowptr,col,val}" in user parent order, complex values
+ * interleaved re/im -- r1: L, Dx, Dy, Dz, Gx, Gy, Gz with the diagonal; z0: Zx, Zy, Zz; cbox: C~
+ * -- and "bloch_mod", "bloch_fa", "bloch_fb") and no field can be evaluated.
+ * pmfem_{demag,exchange,heff}_bloch: m_re, m_im, H_re, H_im device pointers [N'][3] fp32 in
+ * internal node order as for pmfem_demag (the real and imaginary planes of m and H);
+ * H written, not accumulated; no output may alias an input or the other output
+ * (PMFEM_E_INVALID_ARG); PMFEM_E_STATE before pmfem_build_bloch.  Asynchronous on cuda_stream
+ * (plain launches, no graph capture). */
+pmfem_status pmfem_build_bloch(pmfem_ctx ctx, const double* k0, double target_rel_err);
+pmfem_status pmfem_demag_bloch   (pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im,
+                                  void* cuda_stream);
+pmfem_status pmfem_exchange_bloch(pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im,
+                                  void* cuda_stream);
+pmfem_status pmfem_heff_bloch    (pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im,
+                                  void* cuda_stream);
 
 /* Field evaluations.  m: device pointer [N'_local][3] fp32 (internal node order, unit vectors);
  * H: device pointer [N'][3] fp32, written (not accumulated); must not alias m.

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "lib", "libpmfem.so")
-SOURCES = ["pmfem_api.cu", "device.cu", "setup_mesh.cpp", "setup_operators.cpp", "setup_z0.cpp",
+SOURCES = ["pmfem_api.cu", "device.cu", "setup_mesh.cpp", "setup_operators.cpp", "setup_z0.cpp", "setup_bloch.cpp",
            "setup_aim.cpp", "setup_dist.cpp", "pgf_host.cpp", "cbox_gpu.cu", "z0_gpu.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1355,6 +1355,7 @@ void device_bloch_table(DeviceState& D, const HostSetup& S, const PgfParams& Pp,
 void device_free(DeviceState& D) {
   if (D.device < 0) return;
   cudaSetDevice(D.device);
+  device_bloch_free(D);
   void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_bidx, D.c_val,
                   D.seg_moff, D.seg_mask, D.q4,
                   D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
@@ -1802,6 +1803,281 @@ void device_llg_am2(DeviceState& D, float* m, cudaStream_t st, double t_end, dou
   }
   *acc_out = acc;
   *rej_out = rej;
+}
+
+}  // namespace pmfem
+
+// ====================================================================================== NEXT-4
+// Complex Bloch field path (host operators: setup_bloch.cpp, readings R21).
+// m(r + R) = exp(-j k0.R) m(r) enters as two fp32 planes (re, im) in user order; internally
+// every vector is complex (float2) in the box-sorted internal order.  The AIM grid part runs on
+// the MODULATED charges q~ = exp(j k0.r) q with the L-periodic kernel G~ = exp(j k0.r) G_p:
+// G~ = A + jB with A = Re G~ even and B = Im G~ odd, so both real grids Qr, Qi go through the
+// real-to-complex FFT of the static path (K2 and the X/Y/Z passes reused unchanged) and meet in
+// one pointwise 2x2 product of the half spectra,
+//   Ur^ = A^ Qr^ - B^ Qi^,   Ui^ = A^ Qi^ + B^ Qr^   (A^ real, B^ = j fb imaginary).
+namespace pmfem {
+
+struct BlochDev {
+  int64_t* r1_ptr = nullptr; int32_t* r1_col = nullptr; float2* r1_val = nullptr;   // 7 complex / entry
+  int64_t* z_ptr = nullptr;  int32_t* z_col = nullptr;  float2* z_val = nullptr;    // 3 complex / entry
+  int64_t* c_ptr = nullptr;  int32_t* c_col = nullptr;  float2* c_val = nullptr;    // 1 complex / entry
+  float2* mod = nullptr;     // exp(j k0 . r_n), internal order
+  float* fa = nullptr;       // half spectrum of Re G~ (real)
+  float* fb = nullptr;       // half spectrum of Im G~ (imaginary part)
+  float2* m = nullptr;       // [N'][3] internal
+  float* qr = nullptr;       // modulated charges, re / im (K2 inputs, N' + 16 padded)
+  float* qi = nullptr;
+  float2* uloc = nullptr;    // Z0 potential
+  float2* u = nullptr;       // total potential
+  float* Q2 = nullptr;       // second real grid (Qi, then Ui)
+  float2* C2 = nullptr;      // second half spectrum
+  int64_t nnz[3] = {0, 0, 0};
+};
+
+namespace {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) { return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 c) {
+  return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, c.y)));
+}
+
+__global__ void kb_gather(int64_t Np, const float* __restrict__ mre, const float* __restrict__ mim,
+                          float2* __restrict__ m) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= 3 * Np) return;
+  m[i] = make_float2(mre[i], mim[i]);
+}
+
+// K1 (complex): q~ = exp(j k0.r) (D m), u_loc = Z0 m, H_ex = L m (into H) -- thread per row
+__global__ void __launch_bounds__(256) kb_local(int64_t Np, const int64_t* __restrict__ r1_ptr,
+                                                const int32_t* __restrict__ r1_col, const float2* __restrict__ r1_val,
+                                                const int64_t* __restrict__ z_ptr, const int32_t* __restrict__ z_col,
+                                                const float2* __restrict__ z_val, const float2* __restrict__ m,
+                                                const float2* __restrict__ mod, float* __restrict__ qr, float* __restrict__ qi,
+                                                float2* __restrict__ uloc, float* __restrict__ Hre,
+                                                float* __restrict__ Him, int mode) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  float2 q = make_float2(0.f, 0.f), h[3] = {q, q, q};
+  for (int64_t e = r1_ptr[n]; e < r1_ptr[n + 1]; ++e) {
+    const int64_t c = r1_col[e];
+    DCHECK(c >= 0 && c < Np);
+    const float2* v = r1_val + 7 * e;
+    const float2 mx = m[3 * c], my = m[3 * c + 1], mz = m[3 * c + 2];
+    q = cfma(v[1], mx, cfma(v[2], my, cfma(v[3], mz, q)));
+    h[0] = cfma(v[0], mx, h[0]); h[1] = cfma(v[0], my, h[1]); h[2] = cfma(v[0], mz, h[2]);
+  }
+  if (mode == EVAL_EXCHANGE || mode == EVAL_HEFF) {
+    for (int x = 0; x < 3; ++x) { Hre[3 * n + x] = h[x].x; Him[3 * n + x] = h[x].y; }
+  }
+  if (mode == EVAL_EXCHANGE) return;
+  float2 ul = make_float2(0.f, 0.f);
+  for (int64_t e = z_ptr[n]; e < z_ptr[n + 1]; ++e) {
+    const int64_t c = z_col[e];
+    DCHECK(c >= 0 && c < Np);
+    const float2* v = z_val + 3 * e;
+    ul = cfma(v[0], m[3 * c], cfma(v[1], m[3 * c + 1], cfma(v[2], m[3 * c + 2], ul)));
+  }
+  uloc[n] = ul;
+  const float2 qt = cmul(mod[n], q);
+  qr[n] = qt.x;
+  qi[n] = qt.y;
+}
+
+// pointwise product of the two half spectra with A^ (real) and B^ = j fb
+__global__ void kb_spec_mul(int64_t tot, float2* __restrict__ Cr, float2* __restrict__ Ci,
+                            const float* __restrict__ fa, const float* __restrict__ fb) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= tot) return;
+  const float2 X = Cr[i], Y = Ci[i];
+  const float a = fa[i], b = fb[i];
+  Cr[i] = make_float2(fmaf(a, X.x, b * Y.y), fmaf(a, X.y, -b * Y.x));
+  Ci[i] = make_float2(fmaf(a, Y.x, -b * X.y), fmaf(a, Y.y, b * X.x));
+}
+
+// K4 (complex): u = exp(-j k0.r) (P^T U + C~ q~) + u_loc -- thread per row
+template <int P>
+__global__ void __launch_bounds__(256) kb_interp_corr(int64_t Np, const float* __restrict__ Ur,
+                                                      const float* __restrict__ Ui, const int4* __restrict__ st_s,
+                                                      const float4* __restrict__ st_t, GridDims g,
+                                                      const int64_t* __restrict__ c_ptr, const int32_t* __restrict__ c_col,
+                                                      const float2* __restrict__ c_val, const float* __restrict__ qr,
+                                                      const float* __restrict__ qi, const float2* __restrict__ mod,
+                                                      const float2* __restrict__ uloc, float2* __restrict__ u) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  const int4 s = st_s[n];
+  const float4 t = st_t[n];
+  float wx[P + 1], wy[P + 1], wz[P + 1];
+  lagr<P>(t.x, wx); lagr<P>(t.y, wy); lagr<P>(t.z, wz);
+  float2 acc = make_float2(0.f, 0.f);
+  for (int jz = 0; jz <= P; ++jz)
+    for (int jy = 0; jy <= P; ++jy) {
+      const int64_t row = ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+      const float w = wy[jy] * wz[jz];
+#pragma unroll
+      for (int i = 0; i <= P; ++i) {
+        const int64_t gi = row + wrapi(s.x + i, g.n0, g.per0);
+        acc.x = fmaf(w * wx[i], Ur[gi], acc.x);
+        acc.y = fmaf(w * wx[i], Ui[gi], acc.y);
+      }
+    }
+  for (int64_t e = c_ptr[n]; e < c_ptr[n + 1]; ++e) {
+    const int64_t c = c_col[e];
+    DCHECK(c >= 0 && c < Np);
+    acc = cfma(c_val[e], make_float2(qr[c], qi[c]), acc);
+  }
+  const float2 md = mod[n];
+  const float2 ul = uloc[n];
+  u[n] = make_float2(fmaf(md.x, acc.x, fmaf(md.y, acc.y, ul.x)), fmaf(md.x, acc.y, fmaf(-md.y, acc.x, ul.y)));
+}
+
+// K5 (complex): H = -G u (+ H_ex already in H for H_eff)
+__global__ void __launch_bounds__(256) kb_grad(int64_t Np, const int64_t* __restrict__ r1_ptr,
+                                               const int32_t* __restrict__ r1_col, const float2* __restrict__ r1_val,
+                                               const float2* __restrict__ u, float* __restrict__ Hre, float* __restrict__ Him, int add) {
+  const int64_t n = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= Np) return;
+  float2 h[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  for (int64_t e = r1_ptr[n]; e < r1_ptr[n + 1]; ++e) {
+    const float2 uc = u[r1_col[e]];
+    const float2* v = r1_val + 7 * e;
+    h[0] = cfma(v[4], uc, h[0]); h[1] = cfma(v[5], uc, h[1]); h[2] = cfma(v[6], uc, h[2]);
+  }
+  for (int x = 0; x < 3; ++x) {
+    const float ar = add ? Hre[3 * n + x] : 0.f, ai = add ? Him[3 * n + x] : 0.f;
+    Hre[3 * n + x] = ar - h[x].x;
+    Him[3 * n + x] = ai - h[x].y;
+  }
+}
+
+// user-order complex CSR -> internal order, fp32
+void csr_internal(const HostSetup& S, const Csr& R, int ncplx, int64_t*& ptr, int32_t*& col, float2*& val) {
+  const int64_t Np = S.Np;
+  std::vector<int64_t> p(Np + 1, 0);
+  for (int64_t i = 0; i < Np; ++i) {
+    const int64_t n = S.perm[i];
+    p[i + 1] = p[i] + (R.rowptr[n + 1] - R.rowptr[n]);
+  }
+  std::vector<int32_t> c(p[Np]);
+  std::vector<float2> v((size_t)ncplx * p[Np]);
+#pragma omp parallel for
+  for (int64_t i = 0; i < Np; ++i) {
+    const int64_t n = S.perm[i];
+    int64_t o = p[i];
+    for (int64_t e = R.rowptr[n]; e < R.rowptr[n + 1]; ++e, ++o) {
+      c[o] = (int32_t)S.iperm[R.col[e]];
+      for (int k = 0; k < ncplx; ++k)
+        v[(size_t)ncplx * o + k] = make_float2((float)R.val[2 * (ncplx * e + k)], (float)R.val[2 * (ncplx * e + k) + 1]);
+    }
+  }
+  ptr = dupload(p);
+  col = dupload(c);
+  val = dupload(v);
+}
+
+}  // namespace
+
+void device_bloch_free(DeviceState& D) {
+  if (!D.bloch) return;
+  BlochDev& B = *D.bloch;
+  void* ptrs[] = {B.r1_ptr, B.r1_col, B.r1_val, B.z_ptr, B.z_col, B.z_val, B.c_ptr, B.c_col, B.c_val, B.mod,
+                  B.fa, B.fb, B.m, B.qr, B.qi, B.uloc, B.u, B.Q2, B.C2};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete D.bloch;
+  D.bloch = nullptr;
+}
+
+void device_bloch_upload(DeviceState& D, const HostSetup& S, const BlochHost& H) {
+  CK(cudaSetDevice(D.device));
+  device_bloch_free(D);
+  D.bloch = new BlochDev();
+  BlochDev& B = *D.bloch;
+  const int64_t Np = S.Np;
+  csr_internal(S, H.r1, 7, B.r1_ptr, B.r1_col, B.r1_val);
+  csr_internal(S, H.z0, 3, B.z_ptr, B.z_col, B.z_val);
+  csr_internal(S, H.cbox, 1, B.c_ptr, B.c_col, B.c_val);
+  B.nnz[0] = H.r1.nnz(); B.nnz[1] = H.z0.nnz(); B.nnz[2] = H.cbox.nnz();
+  std::vector<float2> md(Np);
+  for (int64_t i = 0; i < Np; ++i) md[i] = make_float2((float)H.mod[2 * S.perm[i]], (float)H.mod[2 * S.perm[i] + 1]);
+  B.mod = dupload(md);
+  std::vector<float> fa(H.fa.begin(), H.fa.end()), fb(H.fb.begin(), H.fb.end());
+  B.fa = dupload(fa);
+  B.fb = dupload(fb);
+  B.m = dalloc<float2>(3 * (size_t)Np);
+  B.qr = dalloc<float>(Np + 16);
+  B.qi = dalloc<float>(Np + 16);
+  CK(cudaMemset(B.qr, 0, sizeof(float) * (Np + 16)));
+  CK(cudaMemset(B.qi, 0, sizeof(float) * (Np + 16)));
+  B.uloc = dalloc<float2>(Np);
+  B.u = dalloc<float2>(Np);
+  B.Q2 = dalloc<float>((size_t)D.n[0] * D.n[1] * D.n[2]);
+  B.C2 = dalloc<float2>((size_t)D.H0 * D.P[1] * D.P[2]);
+  CK(cudaDeviceSynchronize());
+}
+
+void device_bloch_eval(DeviceState& D, const float* m_re, const float* m_im, float* H_re, float* H_im,
+                       cudaStream_t st, EvalMode mode) {
+  require(D.bloch != nullptr, PMFEM_E_STATE, "pmfem_build_bloch has not been called");
+  require(D.world == 1 && D.slab_world <= 1, PMFEM_E_STATE, "the Bloch field path is single-device");
+  BlochDev& B = *D.bloch;
+  const int64_t Np = D.Np;
+  if (Np <= 0) return;
+  const unsigned rb = (unsigned)((Np + 255) / 256);
+  kb_gather<<<(unsigned)((3 * Np + 255) / 256), 256, 0, st>>>(Np, m_re, m_im, B.m);
+  kb_local<<<rb, 256, 0, st>>>(Np, B.r1_ptr, B.r1_col, B.r1_val, B.z_ptr, B.z_col, B.z_val, B.m, B.mod, B.qr, B.qi, B.uloc, H_re, H_im, (int)mode);
+  CK(cudaGetLastError());
+  if (mode == EVAL_EXCHANGE) return;
+  GridDims g{D.n[0], D.n[1], D.n[2], D.periodic[0], D.periodic[1], D.periodic[2]};
+  {
+    const TileDims td{D.k2_tile[0], D.k2_tile[1], D.k2_tile[2]};
+    const unsigned nt = (unsigned)(((size_t)D.n[0] / td.t0) * (D.n[1] / td.t1) * (D.n[2] / td.t2));
+    const size_t smem = sizeof(int) * ((size_t)3 * td.t0 * td.t1 * td.t2 + 2 * k2_nseg(td.t1, td.t2, D.order) + 1);
+#define KB2_LAUNCH(PP)                                                                                          \
+  do {                                                                                                          \
+    CK(cudaFuncSetAttribute(k2_tile<PP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));              \
+    k2_tile<PP><<<nt, 256, smem, st>>>(g, td, D.box_ptr, D.st_s, D.st_t, B.qr, 0, Np, D.box_max, 0, D.Q);      \
+    k2_tile<PP><<<nt, 256, smem, st>>>(g, td, D.box_ptr, D.st_s, D.st_t, B.qi, 0, Np, D.box_max, 0, B.Q2);     \
+  } while (0)
+    switch (D.order) {
+      case 1: KB2_LAUNCH(1); break;
+      case 2: KB2_LAUNCH(2); break;
+      default: KB2_LAUNCH(3); break;
+    }
+#undef KB2_LAUNCH
+    CK(cudaGetLastError());
+  }
+  {
+    const int n0 = D.n[0], n1 = D.n[1], n2 = D.n[2], P0 = D.P[0], P1 = D.P[1], P2 = D.P[2], H0 = D.H0;
+    float* Qs[2] = {D.Q, B.Q2};
+    float2* Cs[2] = {D.C, B.C2};
+    for (int k = 0; k < 2; ++k) {
+      launch_x<float>(true, Qs[k], Cs[k], nullptr, n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
+      launch_strided<float>(Cs[k], P1, H0, H0, n2, (long long)P1 * H0, n1, P1, 0, nullptr, 0, 0, D.tw32[1], st);
+      launch_strided<float>(Cs[k], P2, (long long)P1 * H0, H0, P1, H0, n2, P2, 0, nullptr, 0, 0, D.tw32[2], st);
+    }
+    const int64_t tot = (int64_t)P2 * P1 * H0;
+    kb_spec_mul<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tot, D.C, B.C2, B.fa, B.fb);
+    CK(cudaGetLastError());
+    for (int k = 0; k < 2; ++k) {
+      launch_strided<float>(Cs[k], P2, (long long)P1 * H0, H0, P1, H0, P2, n2, 1, nullptr, 0, 0, D.tw32[2], st);
+      launch_strided<float>(Cs[k], P1, H0, H0, n2, (long long)P1 * H0, P1, n1, 1, nullptr, 0, 0, D.tw32[1], st);
+      launch_x<float>(false, nullptr, Cs[k], Qs[k], n1 * n2, n0, P0, n1, P1, D.tw32[0], st);
+    }
+  }
+  switch (D.order) {
+    case 1: kb_interp_corr<1><<<rb, 256, 0, st>>>(Np, D.Q, B.Q2, D.st_s, D.st_t, g, B.c_ptr, B.c_col, B.c_val, B.qr, B.qi,
+                                                   B.mod, B.uloc, B.u); break;
+    case 2: kb_interp_corr<2><<<rb, 256, 0, st>>>(Np, D.Q, B.Q2, D.st_s, D.st_t, g, B.c_ptr, B.c_col, B.c_val, B.qr, B.qi,
+                                                   B.mod, B.uloc, B.u); break;
+    default: kb_interp_corr<3><<<rb, 256, 0, st>>>(Np, D.Q, B.Q2, D.st_s, D.st_t, g, B.c_ptr, B.c_col, B.c_val, B.qr,
+                                                    B.qi, B.mod, B.uloc, B.u); break;
+  }
+  CK(cudaGetLastError());
+  kb_grad<<<rb, 256, 0, st>>>(Np, B.r1_ptr, B.r1_col, B.r1_val, B.u, H_re, H_im, mode == EVAL_HEFF ? 1 : 0);
+  CK(cudaGetLastError());
 }
 
 }  // namespace pmfem

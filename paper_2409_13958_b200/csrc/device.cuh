@@ -171,6 +171,7 @@ struct DeviceState {
   const float* llg_key_m = nullptr;
   cudaStream_t llg_key_st = nullptr;
   double llg_key[6] = {0, 0, 0, 0, 0, 0};
+  struct BlochDev* bloch = nullptr;   // NEXT-4 complex field path (device_bloch_upload)
 };
 
 void device_llg_rk4_step(DeviceState& D, float* m, cudaStream_t st, double dt, double alpha, double gamma,
@@ -188,6 +189,12 @@ void device_bloch_table(DeviceState& D, const HostSetup& S, const PgfParams& P, 
                         std::vector<double>& K);
 void device_free(DeviceState& D);
 enum EvalMode { EVAL_HEFF = 0, EVAL_DEMAG = 1, EVAL_EXCHANGE = 2 };
+// NEXT-4 complex Bloch field path (single device): operators from setup_bloch_ops, then
+// H_re + j H_im = H(m_re + j m_im) for Bloch amplitudes m(r + R) = exp(-j k0.R) m(r)
+void device_bloch_upload(DeviceState& D, const HostSetup& S, const BlochHost& B);
+void device_bloch_eval(DeviceState& D, const float* m_re, const float* m_im, float* H_re, float* H_im,
+                       cudaStream_t st, EvalMode mode);
+void device_bloch_free(DeviceState& D);
 void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, EvalMode mode);
 
 }  // namespace pmfem

@@ -14,6 +14,7 @@ struct pmfem_ctx_s {
   pmfem::DeviceState D;
   std::string err;
   bool host_only = true;
+  pmfem::BlochHost bloch;       // NEXT-4 phased operators (kept on host-only contexts, for export)
 };
 
 namespace {
@@ -211,29 +212,77 @@ pmfem_status pmfem_build_pgf(pmfem_ctx ctx, double target_rel_err) {
   });
 }
 
+// Bloch kernel table + full complex spectrum of k0 (user frame) into S.kernel_bloch /
+// S.spectrum_bloch; S.k0 = k0 in the internal frame
+static void bloch_kernel(pmfem_ctx ctx, const double* k0, double target_rel_err) {
+  pmfem::HostSetup& S = ctx->S;
+  pmfem::require(k0 != nullptr && target_rel_err > 0, PMFEM_E_INVALID_ARG, "NULL k0 or bad target");
+  double kin[3];
+  for (int a = 0; a < 3; ++a) {
+    kin[a] = k0[S.axperm[a]];          // internal frame
+    pmfem::require(std::isfinite(kin[a]), PMFEM_E_INVALID_ARG, "k0 must be finite");
+    pmfem::require(S.periodic[a] || kin[a] == 0.0, PMFEM_E_INVALID_ARG, "k0 must vanish on non-periodic axes");
+  }
+  bool off = false;                    // k0 on the reciprocal lattice is the static kernel
+  for (int a = 0; a < 3; ++a)
+    if (S.periodic[a]) {
+      const double f = kin[a] * S.L[a] / (2 * M_PI);
+      off |= std::fabs(f - std::round(f)) > 1e-12;
+    }
+  pmfem::require(off, PMFEM_E_INVALID_ARG, "k0 on the reciprocal lattice: use pmfem_build_pgf");
+  pmfem::PgfParams P = pmfem::make_pgf_params(S.periodic, S.L, target_rel_err);
+  if (ctx->host_only) pmfem::host_bloch_table(S, P, kin, S.kernel_bloch);
+  else pmfem::device_bloch_table(ctx->D, S, P, kin, S.kernel_bloch);
+  pmfem::host_bloch_spectrum(S, S.kernel_bloch, S.spectrum_bloch);
+  for (int a = 0; a < 3; ++a) S.k0[a] = kin[a];
+}
+
 pmfem_status pmfem_build_pgf_bloch(pmfem_ctx ctx, const double* k0, double target_rel_err) {
   if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] { bloch_kernel(ctx, k0, target_rel_err); });
+}
+
+pmfem_status pmfem_build_bloch(pmfem_ctx ctx, const double* k0, double target_rel_err) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
   return guard(ctx, [&] {
-    pmfem::HostSetup& S = ctx->S;
-    pmfem::require(k0 != nullptr && target_rel_err > 0, PMFEM_E_INVALID_ARG, "NULL k0 or bad target");
-    double kin[3];
-    for (int a = 0; a < 3; ++a) {
-      kin[a] = k0[S.axperm[a]];          // internal frame
-      pmfem::require(S.periodic[a] || kin[a] == 0.0, PMFEM_E_INVALID_ARG, "k0 must vanish on non-periodic axes");
+    pmfem::require(ctx->host_only || ctx->D.world == 1, PMFEM_E_STATE,
+                   "the Bloch field path is single-device (world = 1)");
+    const double t0 = now();
+    bloch_kernel(ctx, k0, target_rel_err);
+    pmfem::BlochHost B;
+    pmfem::setup_bloch_ops(ctx->S, ctx->S.k0, B);
+    if (!ctx->host_only) pmfem::device_bloch_upload(ctx->D, ctx->S, B);
+    else ctx->bloch = std::move(B);      // host-only: kept for pmfem_export (setup parity tests)
+    if (std::getenv("PMFEM_VERBOSE")) {
+      std::fprintf(stderr, "[pmfem] build_bloch      %8.2f s\n", now() - t0);
+      std::fflush(stderr);
     }
-    bool off = false;                    // k0 on the reciprocal lattice is the static kernel
-    for (int a = 0; a < 3; ++a)
-      if (S.periodic[a]) {
-        const double f = kin[a] * S.L[a] / (2 * M_PI);
-        off |= std::fabs(f - std::round(f)) > 1e-12;
-      }
-    pmfem::require(off, PMFEM_E_INVALID_ARG, "k0 on the reciprocal lattice: use pmfem_build_pgf");
-    pmfem::PgfParams P = pmfem::make_pgf_params(S.periodic, S.L, target_rel_err);
-    if (ctx->host_only) pmfem::host_bloch_table(S, P, kin, S.kernel_bloch);
-    else pmfem::device_bloch_table(ctx->D, S, P, kin, S.kernel_bloch);
-    pmfem::host_bloch_spectrum(S, S.kernel_bloch, S.spectrum_bloch);
-    for (int a = 0; a < 3; ++a) S.k0[a] = kin[a];
   });
+}
+
+static pmfem_status eval_bloch(pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im,
+                               void* stream, pmfem::EvalMode mode) {
+  if (!ctx) return PMFEM_E_INVALID_ARG;
+  return guard(ctx, [&] {
+    check_eval(ctx, m_re, H_re);
+    pmfem::require(m_im != nullptr && H_im != nullptr, PMFEM_E_INVALID_ARG, "NULL m_im or H_im");
+    const void* outs[2] = {H_re, H_im};
+    const void* ins[2] = {m_re, m_im};
+    for (const void* o : outs)
+      for (const void* i : ins) pmfem::require(o != i, PMFEM_E_INVALID_ARG, "H must not alias m");
+    pmfem::require((const void*)H_re != (const void*)H_im, PMFEM_E_INVALID_ARG, "H_re must not alias H_im");
+    pmfem::device_bloch_eval(ctx->D, m_re, m_im, H_re, H_im, (cudaStream_t)stream, mode);
+  });
+}
+
+pmfem_status pmfem_demag_bloch(pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im, void* s) {
+  return eval_bloch(ctx, m_re, m_im, H_re, H_im, s, pmfem::EVAL_DEMAG);
+}
+pmfem_status pmfem_exchange_bloch(pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im, void* s) {
+  return eval_bloch(ctx, m_re, m_im, H_re, H_im, s, pmfem::EVAL_EXCHANGE);
+}
+pmfem_status pmfem_heff_bloch(pmfem_ctx ctx, const float* m_re, const float* m_im, float* H_re, float* H_im, void* s) {
+  return eval_bloch(ctx, m_re, m_im, H_re, H_im, s, pmfem::EVAL_HEFF);
 }
 
 // One evaluation = ~9 kernel launches (+ NCCL calls on N>1).  On a non-default stream the
@@ -589,6 +638,19 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
     }
     else if (n == "kernel_bloch") put(S.kernel_bloch.data(), (int64_t)S.kernel_bloch.size(), 8);
     else if (n == "spectrum_bloch") put(S.spectrum_bloch.data(), (int64_t)S.spectrum_bloch.size(), 8);
+    else if (n.rfind("bloch_", 0) == 0) {     // host-only contexts after pmfem_build_bloch
+      const pmfem::BlochHost& B = ctx->bloch;
+      const pmfem::Csr* R = n.rfind("bloch_r1_", 0) == 0 ? &B.r1 : n.rfind("bloch_z0_", 0) == 0 ? &B.z0
+                            : n.rfind("bloch_cbox_", 0) == 0 ? &B.cbox : nullptr;
+      const std::string f = R ? n.substr(n.find('_', 6) + 1) : "";
+      if (R && f == "rowptr") put(R->rowptr.data(), (int64_t)R->rowptr.size(), 8);
+      else if (R && f == "col") put(R->col.data(), R->nnz(), 4);
+      else if (R && f == "val") put(R->val.data(), (int64_t)R->val.size(), 8);
+      else if (n == "bloch_mod") put(B.mod.data(), (int64_t)B.mod.size(), 8);
+      else if (n == "bloch_fa") put(B.fa.data(), (int64_t)B.fa.size(), 8);
+      else if (n == "bloch_fb") put(B.fb.data(), (int64_t)B.fb.size(), 8);
+      else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");
+    }
     else if (n == "kernel") put(S.kernel.data(), (int64_t)S.kernel.size(), 8);
     else if (n == "spectrum") put(S.spectrum.data(), (int64_t)S.spectrum.size(), 8);
     else throw pmfem::Error(PMFEM_E_INVALID_ARG, "unknown export name '" + n + "'");

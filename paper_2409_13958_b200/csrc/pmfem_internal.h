@@ -1,6 +1,7 @@
 // Internal declarations of libpmfem (host setup in fp64, device path in fp32).
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -36,6 +37,17 @@ struct Z0Item {
   int8_t va;          // local vertex that coincides with the observer, or -1
   uint8_t flags;      // bit j: local vertex j is a near source of row n
   int16_t pos[4];     // row-relative column slot of each local vertex
+};
+
+// Z0 near-set enumeration of one observer row (setup_z0.cpp; shared by the static and the Bloch
+// operator builds): near(n) as (parent, packed lattice shift) pairs and the element images
+// (key = tet * Z0_NC + packed shift) with the near-source vertex flags and the observer vertex.
+constexpr int Z0_NC = 17 * 17 * 17;
+struct Z0RowEnum {
+  struct It { int64_t key; int va; unsigned flags; };
+  std::vector<std::pair<int64_t, int>> near;
+  std::vector<int64_t> U;           // scratch
+  std::vector<It> its;
 };
 
 // Multi-GPU plan: contiguous internal-row ranges per rank and halo exchange index lists
@@ -119,6 +131,22 @@ struct HostSetup {
 void setup_mesh(HostSetup& S, const pmfem_mesh* mesh, const pmfem_periodicity* per);
 void setup_operators(HostSetup& S);
 void setup_z0(HostSetup& S);
+void z0_enumerate_row(const HostSetup& S, int64_t n, Z0RowEnum& W);
+void z0_unpack_shift(int code, int s[3]);
+// host C_box rows (K8/K9, fp64): nv = 1 static; with kb (internal-frame k0) nv = 2, the
+// modulated Bloch precorrection (re, im)
+void host_cbox_rows(const HostSetup& S, const double* kb, std::vector<std::vector<int32_t>>& rcol,
+                    std::vector<std::vector<double>>& rval);
+// NEXT-4 complex field path: Bloch-phased operators in USER parent order (setup_bloch.cpp)
+struct BlochHost {
+  double k0[3] = {0, 0, 0};         // internal frame
+  Csr r1;                           // nv = 14: complex L, Dx, Dy, Dz, Gx, Gy, Gz (re, im), diagonal included
+  Csr z0;                           // nv = 6: complex Zx, Zy, Zz, diagonal included
+  Csr cbox;                         // nv = 2: complex modulated C~
+  std::vector<double> mod;          // [Np][2] exp(j k0 . r_n), r_n the unwrapped parent coordinate
+  std::vector<double> fa, fb;       // half spectra [P2][P1][H0] / #points of Re G~ (real) and Im G~ (imag part)
+};
+void setup_bloch_ops(const HostSetup& S, const double k0[3], BlochHost& B);
 void setup_aim(HostSetup& S, const pmfem_grid* g);
 void setup_order(HostSetup& S);
 void setup_dist(HostSetup& S, int rank, int world);          // partition (needs setup_order)

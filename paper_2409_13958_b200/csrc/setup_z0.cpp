@@ -87,15 +87,73 @@ struct ColSet {
   int& slot(int32_t c) { return val[find_pos(c)]; }
 };
 
-struct ItemFlagsW { int64_t key; int va; unsigned flags; };
 struct RowWork {
-  std::vector<std::pair<int64_t, int>> near;   // (parent, shift code)
-  std::vector<int64_t> U;                       // tet * NC + code
-  std::vector<ItemFlagsW> its;
+  Z0RowEnum e;
   ColSet cs;
 };
 
 }  // namespace
+
+void z0_unpack_shift(int code, int s[3]) { unpack_shift(code, s); }
+
+// near(n) (self, or the periodic 1-ring: every (LCA(v), relative shift) of the tets of every
+// copy of n) and the deduplicated element images U(n) of the near sources' supports
+// (Eq. dedup), with per image the near-source vertex flags and the observer vertex
+void z0_enumerate_row(const HostSetup& S, int64_t n, Z0RowEnum& W) {
+  const int NC = Z0_NC;
+  auto& near = W.near;
+  auto& U = W.U;
+  near.clear(); U.clear(); W.its.clear();
+  const int zero_code = ((8 * 17) + 8) * 17 + 8;
+  if (S.z0_ring == 0) {
+    near.push_back({n, zero_code});
+  } else {
+    for (int64_t ci = S.copies_ptr[n]; ci < S.copies_ptr[n + 1]; ++ci) {
+      const int64_t c = S.copies[ci];
+      for (int64_t ti = S.ntet_ptr[c]; ti < S.ntet_ptr[c + 1]; ++ti) {
+        const int64_t t = S.ntet[ti];
+        for (int b = 0; b < 4; ++b) {
+          const int32_t v = S.tets[4 * t + b];
+          int s[3];
+          for (int x = 0; x < 3; ++x) s[x] = S.shift[3 * v + x] - S.shift[3 * c + x];
+          near.push_back({S.pid[v], pack_shift(s)});
+        }
+      }
+    }
+    std::sort(near.begin(), near.end());
+    near.erase(std::unique(near.begin(), near.end()), near.end());
+  }
+  for (auto& pr : near) {
+    int ell[3];
+    unpack_shift(pr.second, ell);
+    for (int64_t ci = S.copies_ptr[pr.first]; ci < S.copies_ptr[pr.first + 1]; ++ci) {
+      const int64_t c = S.copies[ci];
+      int s[3];
+      for (int x = 0; x < 3; ++x) s[x] = ell[x] - S.shift[3 * c + x];
+      const int code = pack_shift(s);
+      for (int64_t ti = S.ntet_ptr[c]; ti < S.ntet_ptr[c + 1]; ++ti) U.push_back(S.ntet[ti] * NC + code);
+    }
+  }
+  std::sort(U.begin(), U.end());
+  U.erase(std::unique(U.begin(), U.end()), U.end());
+  for (int64_t key : U) {
+    const int64_t t = key / NC;
+    int s[3];
+    unpack_shift((int)(key % NC), s);
+    const int32_t* tv = &S.tets[4 * t];
+    unsigned flags = 0;
+    int va = -1;
+    for (int j = 0; j < 4; ++j) {
+      int sv[3];
+      for (int x = 0; x < 3; ++x) sv[x] = S.shift[3 * tv[j] + x] + s[x];
+      std::pair<int64_t, int> k2 = {S.pid[tv[j]], pack_shift(sv)};
+      if (std::binary_search(near.begin(), near.end(), k2)) flags |= 1u << j;
+      if (S.pid[tv[j]] == n && sv[0] == 0 && sv[1] == 0 && sv[2] == 0) va = j;
+    }
+    if (!flags) continue;
+    W.its.push_back({key, va, flags});
+  }
+}
 
 void setup_z0(HostSetup& S) {
   const int64_t Np = S.Np;
@@ -138,41 +196,8 @@ void setup_z0(HostSetup& S) {
       for (int64_t j = c0; j < c1; ++j) {
         const int64_t n = rows[j];
         try {
-          auto& near = W.near;
-          auto& U = W.U;
-          near.clear(); U.clear();
-          const int zero_code = ((8 * 17) + 8) * 17 + 8;
-          if (S.z0_ring == 0) {
-            near.push_back({n, zero_code});
-          } else {
-            for (int64_t ci = S.copies_ptr[n]; ci < S.copies_ptr[n + 1]; ++ci) {
-              const int64_t c = S.copies[ci];
-              for (int64_t ti = S.ntet_ptr[c]; ti < S.ntet_ptr[c + 1]; ++ti) {
-                const int64_t t = S.ntet[ti];
-                for (int b = 0; b < 4; ++b) {
-                  const int32_t v = S.tets[4 * t + b];
-                  int s[3];
-                  for (int x = 0; x < 3; ++x) s[x] = S.shift[3 * v + x] - S.shift[3 * c + x];
-                  near.push_back({S.pid[v], pack_shift(s)});
-                }
-              }
-            }
-            std::sort(near.begin(), near.end());
-            near.erase(std::unique(near.begin(), near.end()), near.end());
-          }
-          for (auto& pr : near) {
-            int ell[3];
-            unpack_shift(pr.second, ell);
-            for (int64_t ci = S.copies_ptr[pr.first]; ci < S.copies_ptr[pr.first + 1]; ++ci) {
-              const int64_t c = S.copies[ci];
-              int s[3];
-              for (int x = 0; x < 3; ++x) s[x] = ell[x] - S.shift[3 * c + x];
-              const int code = pack_shift(s);
-              for (int64_t ti = S.ntet_ptr[c]; ti < S.ntet_ptr[c + 1]; ++ti) U.push_back(S.ntet[ti] * NC + code);
-            }
-          }
-          std::sort(U.begin(), U.end());
-          U.erase(std::unique(U.begin(), U.end()), U.end());
+          z0_enumerate_row(S, n, W.e);
+          auto& near = W.e.near;
           // column list: every vertex of every contributing element image + the D rows of the
           // near sources (point-charge subtraction)
           std::vector<int32_t>& cols = rcol[n];
@@ -183,24 +208,9 @@ void setup_z0(HostSetup& S) {
             if (cs_ok && !W.cs.insert(c)) cs_ok = false;
             cols.push_back(c);
           };
-          std::vector<ItemFlagsW>& its = W.its;
-          its.clear();
-          for (int64_t key : U) {
-            const int64_t t = key / NC;
-            int s[3];
-            unpack_shift((int)(key % NC), s);
-            const int32_t* tv = &S.tets[4 * t];
-            unsigned flags = 0;
-            int va = -1;
-            for (int j = 0; j < 4; ++j) {
-              int sv[3];
-              for (int x = 0; x < 3; ++x) sv[x] = S.shift[3 * tv[j] + x] + s[x];
-              std::pair<int64_t, int> k2 = {S.pid[tv[j]], pack_shift(sv)};
-              if (std::binary_search(near.begin(), near.end(), k2)) flags |= 1u << j;
-              if (S.pid[tv[j]] == n && sv[0] == 0 && sv[1] == 0 && sv[2] == 0) va = j;
-            }
-            if (!flags) continue;
-            its.push_back({key, va, flags});
+          auto& its = W.e.its;
+          for (auto& it : its) {
+            const int32_t* tv = &S.tets[4 * (it.key / NC)];
             for (int j = 0; j < 4; ++j) add_col(S.pid[tv[j]]);
           }
           const double* xn = &S.xyz[3 * S.parent[n]];

@@ -26,7 +26,7 @@ STATUS = {0: "PMFEM_OK", 1: "PMFEM_E_INVALID_ARG", 2: "PMFEM_E_MESH", 3: "PMFEM_
 
 SYMBOLS = ["pmfem_setup", "pmfem_setup_dist", "pmfem_nccl_unique_id", "pmfem_build_pgf", "pmfem_llg_rk4",
            "pmfem_llg_am2", "pmfem_set_anisotropy", "pmfem_build_pgf_bloch", "pmfem_demag", "pmfem_exchange",
-           "pmfem_heff",
+           "pmfem_heff", "pmfem_build_bloch", "pmfem_demag_bloch", "pmfem_exchange_bloch", "pmfem_heff_bloch",
            "pmfem_heff_host", "pmfem_query", "pmfem_get_order", "pmfem_export", "pmfem_set_timing",
            "pmfem_get_timing", "pmfem_last_error", "pmfem_destroy"]
 
@@ -83,6 +83,9 @@ _lib.pmfem_llg_am2.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_double, ctype
                                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]
 _lib.pmfem_set_anisotropy.argtypes = [_vp, ctypes.c_int, ctypes.c_double, ctypes.c_void_p]
 _lib.pmfem_build_pgf_bloch.argtypes = [_vp, ctypes.c_void_p, ctypes.c_double]
+_lib.pmfem_build_bloch.argtypes = [_vp, ctypes.c_void_p, ctypes.c_double]
+for _n in ("pmfem_demag_bloch", "pmfem_exchange_bloch", "pmfem_heff_bloch"):
+    getattr(_lib, _n).argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
 _lib.pmfem_query.argtypes = [_vp, ctypes.POINTER(_Info)]
 _lib.pmfem_get_order.argtypes = [_vp, ctypes.POINTER(ctypes.c_int64)]
 _lib.pmfem_export.argtypes = [_vp, ctypes.c_char_p, _vp, ctypes.POINTER(ctypes.c_int64)]
@@ -102,6 +105,9 @@ _EXPORT_DTYPES.update({"cbox_device_rowptr": np.int64, "cbox_device_col": np.int
                        "cbox_device_val": np.float32, "cbox_device_chunks": np.int64,
                        "cbox_device_format": np.int64, "slab_kranges": np.int64,
                        "dist_planes": np.int64, "dist_ghost": np.int64, "axis_perm": np.int64})
+for _k in ("r1", "z0", "cbox"):
+    _EXPORT_DTYPES["bloch_%s_rowptr" % _k] = np.int64
+    _EXPORT_DTYPES["bloch_%s_col" % _k] = np.int32
 for _k in "mqu":
     _EXPORT_DTYPES["send_%s_ptr" % _k] = np.int64
     _EXPORT_DTYPES["recv_%s_ptr" % _k] = np.int64
@@ -208,6 +214,30 @@ class Context:
         G = self.export("spectrum_bloch")
         shape = (P[2], P[1], P[0])
         return (K[0::2] + 1j * K[1::2]).reshape(shape), (G[0::2] + 1j * G[1::2]).reshape(shape)
+
+    def build_bloch(self, k0, target_rel_err=1e-12):
+        """NEXT-4 complex field path: the Bloch kernel and the phased operators for k0 (rad/cm,
+        user frame); then demag_bloch / exchange_bloch / heff_bloch."""
+        k = (ctypes.c_double * 3)(*[float(v) for v in k0])
+        self._check(_lib.pmfem_build_bloch(self._h, ctypes.cast(k, ctypes.c_void_p), float(target_rel_err)))
+
+    def _eval_bloch(self, fn, m_re, m_im, H_re, H_im, stream):
+        import torch
+        H_re = torch.empty_like(m_re) if H_re is None else H_re
+        H_im = torch.empty_like(m_im) if H_im is None else H_im
+        n = self.n_parents_local
+        self._check(fn(self._h, _dev_ptr(m_re, n, self.device), _dev_ptr(m_im, n, self.device),
+                       _dev_ptr(H_re, n, self.device), _dev_ptr(H_im, n, self.device), self._stream(stream)))
+        return H_re, H_im
+
+    def demag_bloch(self, m_re, m_im, H_re=None, H_im=None, stream=None):
+        return self._eval_bloch(_lib.pmfem_demag_bloch, m_re, m_im, H_re, H_im, stream)
+
+    def exchange_bloch(self, m_re, m_im, H_re=None, H_im=None, stream=None):
+        return self._eval_bloch(_lib.pmfem_exchange_bloch, m_re, m_im, H_re, H_im, stream)
+
+    def heff_bloch(self, m_re, m_im, H_re=None, H_im=None, stream=None):
+        return self._eval_bloch(_lib.pmfem_heff_bloch, m_re, m_im, H_re, H_im, stream)
 
     def _stream(self, stream):
         if stream is None:

@@ -66,4 +66,36 @@ def max_node_rel(a, b):
     """Per-node bound: max_n |a_n - b_n| / rms_n |b_n| (rows = nodes)."""
     a = np.asarray(a).reshape(len(a), -1)
     b = np.asarray(b).reshape(len(b), -1)
-    return float(np.max(np.linalg.norm(a - b, axis=1)) / np.sqrt(np.mean(np.sum(b * b, axis=1))))
+    return float(np.max(np.linalg.norm(a - b, axis=1)) / np.sqrt(np.mean(np.sum(np.abs(b) ** 2, axis=1))))
+
+
+# NEXT-4: Bloch wave vectors of the parity tests (rad/cm, off the reciprocal lattice, generic
+# fractions of the reciprocal vectors so no phase is real)
+def bloch_k0(key):
+    cfg, _ = config(key)
+    out = np.zeros(3)
+    fr = iter((0.3, 0.2, 0.1))
+    for a in range(3):
+        if cfg["periodic"][a]:
+            out[a] = 2 * np.pi / cfg["lattice"][a] * next(fr)
+    return out
+
+
+@functools.lru_cache(maxsize=None)
+def bloch_oracle(key):
+    from oracle.bloch_heff import BlochModel
+    cfg, spec = config(key)
+    m = cfg["mesh"]
+    return BlochModel(m.xyz, m.tets, cfg["periodic"], cfg["lattice"], spec["grid"], bloch_k0(key), Ms=cfg["Ms"],
+                      Aex=cfg["Aex"], order=spec["order"], rer_scale=spec["s"], z0_ring=spec["ring"])
+
+
+def dense_c(ctx, prefix, nv, n):
+    """Dense [n, n, nv] complex matrix of a complex CSR export (values interleaved re/im)."""
+    rp = ctx.export(prefix + "_rowptr")
+    col = ctx.export(prefix + "_col")
+    v = ctx.export(prefix + "_val").reshape(-1, nv, 2)
+    A = np.zeros((n, n, nv), complex)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    np.add.at(A, (rows, col), v[..., 0] + 1j * v[..., 1])
+    return A
