@@ -173,7 +173,7 @@ pmfem_status pmfem_build_pgf_bloch(pmfem_ctx ctx, const double* k0, double targe
 /* NEXT-4 complex field path.  Magnetisation amplitudes that are Bloch-periodic with the phase
  * of Eq. 2, m(r + R) = exp(-j k0.R) m(r), have the potential
  * u(r_n) = sum_m G_p(r_n - r_m; k0) q_m + Z0 terms, and everything in the static path carries
- * over with phases (reading R21): folded local operators weight a tet entry between
+ * over with phases (reading R27): folded local operators weight a tet entry between
  * copies with lattice shifts s_a (row), s_b (column) by exp(j k0.L(s_a - s_b)); Z0 weights an
  * element image by the shifts of its vertices; the AIM grid part runs on the modulated charges
  * exp(j k0.r_n) q_n with the L-periodic kernel exp(j k0.r) G_p(r) (complex spectrum, nothing

@@ -3,7 +3,7 @@
 P:183-185 (Eq. 2): G_p(r) = sum_i exp(-j k0 . R_i) G_0(r - R_i).  It is the unit-cell kernel of
 a charge density that is Bloch-periodic with the same phase, rho(r + R) = exp(-j k0 . R) rho(r)
 (sum the free-space potential over the cells), so the field path of the static method carries
-over to complex magnetisation amplitudes m(r + R) = exp(-j k0 . R) m(r) (reading R21):
+over to complex magnetisation amplitudes m(r + R) = exp(-j k0 . R) m(r) (reading R27):
 
 * local operators (assembled over all tets and folded to the parents as in
   fem.py): a tet entry between copies a (row) and b (column) of parents n, m with lattice shifts

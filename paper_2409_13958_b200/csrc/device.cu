@@ -1808,7 +1808,7 @@ void device_llg_am2(DeviceState& D, float* m, cudaStream_t st, double t_end, dou
 }  // namespace pmfem
 
 // ====================================================================================== NEXT-4
-// Complex Bloch field path (host operators: setup_bloch.cpp, readings R21).
+// Complex Bloch field path (host operators: setup_bloch.cpp, reading R27).
 // m(r + R) = exp(-j k0.R) m(r) enters as two fp32 planes (re, im) in user order; internally
 // every vector is complex (float2) in the box-sorted internal order.  The AIM grid part runs on
 // the MODULATED charges q~ = exp(j k0.r) q with the L-periodic kernel G~ = exp(j k0.r) G_p:

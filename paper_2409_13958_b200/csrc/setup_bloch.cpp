@@ -1,7 +1,7 @@
 // Host setup of the NEXT-4 complex field path (fp64): the Bloch-phased operators.
 //   P:183-185  G_p(r) = sum_i exp(-j k0.R_i) G_0(r - R_i)  (Eq. 2): the unit-cell kernel of a
 //              Bloch-periodic charge rho(r + R) = exp(-j k0.R) rho(r); the magnetisation
-//              amplitudes obey the same condition, m(r + R) = exp(-j k0.R) m(r) (reading R21)
+//              amplitudes obey the same condition, m(r + R) = exp(-j k0.R) m(r) (reading R27)
 //   P:117-157, P:170-177  folded local operators: a tet entry between copies a (row) and b
 //              (column) with lattice shifts s_a, s_b carries exp(j k0.L(s_a - s_b))
 //   P:173, P:190, P:234   Z0: element image (t, s) seen from r_n -- vertex v carries

@@ -1,4 +1,4 @@
-"""Oracle pins of the Bloch field path (NEXT-4, oracle/bloch_heff.py; reading R21).
+"""Oracle pins of the Bloch field path (NEXT-4, oracle/bloch_heff.py; reading R27).
 
 1. Supercell identity (exact).  For k0 = 2 pi j / (M L) along a periodic axis, a Bloch mode of
    the unit cell, m(r + R) = exp(-j k0.R) m(r), IS an ordinary field of the M-cell supercell
