@@ -365,7 +365,7 @@ def main():
                         "slab-partitioned rows over %d GPUs: NCCL halos (m, q, u) + all-reduce of the "
                         "anterpolated grid, replicated FFT" % world), "n_parents_local": Nloc,
                        "k2_tile": info["k2_tile"],
-                       "cbox_format": ["C4x", "B4", "SEG", "U4"][info["cbox_format"]],
+                       "cbox_format": ["C4x", "B4", "SEG", "U4", "?", "W4"][info["cbox_format"]],
                        "cbox_packed_units": info["cbox_packed_units"]},
             "nodes_per_s": value * Np, "setup_s": t_setup, "build_pgf_s": t_pgf,
             "bytes_per_eval_algorithmic": alg_total,

@@ -366,6 +366,47 @@ __global__ void k_u4_fill(long long Np, const long long* __restrict__ rowptr, co
   }
 }
 
+// ---- W4: per own row, the CSR entries as nch = ceil(m/4) chunks of 4 with window-local
+// indices: the run of the row's tile containing column k (runs of a tile sorted by first row;
+// binary search) gives loc = run_loc + k - run_start.  Quarter-transposed: entry e of the row goes
+// to chunk e mod nch, slot e / nch, so the 32 lanes of a K4 group reading chunks c..c+31 gather
+// 32 CONSECUTIVE entries per slot -- consecutive window indices along a run, i.e. distinct
+// shared-memory banks (with 4 consecutive entries per chunk the lanes' indices were 4 apart: a
+// 4-way bank conflict on every gather).  Padding slots: value 0 at the row's first index.
+// Columns outside the window are counted in *miss (the build then falls back to another format).
+__global__ void k_w4_fill(long long Np, const long long* __restrict__ rowptr, const int* __restrict__ col,
+                          const float* __restrict__ val, const int* __restrict__ tile_of, const int* __restrict__ rptr,
+                          const int* __restrict__ rstart, const int* __restrict__ rlen, const int* __restrict__ rloc,
+                          const long long* __restrict__ cptr, float* __restrict__ cval, unsigned short* __restrict__ cidx,
+                          unsigned long long* __restrict__ miss) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Np) return;
+  const int t = tile_of[i];
+  const int r0 = rptr[t], r1 = rptr[t + 1];
+  const long long c0 = cptr[i], nch = cptr[i + 1] - c0, m = rowptr[i + 1] - rowptr[i];
+  unsigned short first = 0;
+  for (long long j = 0; j < m; ++j) {
+    const int k = col[rowptr[i] + j];
+    int lo = r0, hi = r1 - 1;           // last run with start <= k
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rstart[mid] <= k) lo = mid; else hi = mid - 1;
+    }
+    unsigned short loc = 0;
+    if (rstart[lo] <= k && k < rstart[lo] + rlen[lo]) loc = (unsigned short)(rloc[lo] + (k - rstart[lo]));
+    else atomicAdd(miss, 1ull);
+    if (j == 0) first = loc;
+    const long long o = 4 * (c0 + j % nch) + j / nch;
+    cidx[o] = loc;
+    cval[o] = val[rowptr[i] + j];
+  }
+  for (long long j = m; j < 4 * nch; ++j) {
+    const long long o = 4 * (c0 + j % nch) + j / nch;
+    cidx[o] = first;
+    cval[o] = 0.f;
+  }
+}
+
 template <class T>
 T* dalloc_c(size_t n) {
   T* p = nullptr;
@@ -525,6 +566,124 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   CKC(cudaGetLastError());
   CKC(cudaMemcpy(nu.data(), d_nch, sizeof(long long) * Np, cudaMemcpyDeviceToHost));
   for (int64_t i = 0; i < Np; ++i) uptr[i + 1] = uptr[i] + nu[i];
+  // ---- W4 (windowed, format 5): tiles of consecutive own rows of one anchor (y, z) line; the
+  // window of a tile = the rows of the anchor boxes within the candidate reach R_a (as SEG:
+  // R_a = ceil(r_ER / Delta_a + 1) - 1, stored anchors) of the tile's boxes, as runs of internal
+  // rows; a tile is halved until its window fits W4_WMAX floats of shared memory.  Every near
+  // column must fall in its row's window (checked: otherwise another format is used).
+  if (fmt == "w4") {
+    constexpr int W4_TMAX = 128;
+    const int W4_WMAX = std::getenv("PMFEM_W4_WMAX") ? std::atoi(std::getenv("PMFEM_W4_WMAX")) : 4096;
+    int R[3], lim[3];
+    for (int a = 0; a < 3; ++a) {
+      R[a] = (int)std::ceil(c.rer / c.delta[a] + 1.0) - 1;
+      lim[a] = c.per[a] ? c.n[a] - 1 : c.n[a] - 1 - p;
+    }
+    // stored anchors (wrapped / clamped) of the internal rows and the anchor-box row pointers
+    std::vector<int> an(3 * Nall);
+    for (int64_t i = 0; i < Nall; ++i)
+      for (int a = 0; a < 3; ++a) {
+        int v = su[3 * i + a];
+        if (c.per[a]) v = ((v % c.n[a]) + c.n[a]) % c.n[a];
+        an[3 * i + a] = v;
+      }
+    const int64_t nbox = (int64_t)c.n[0] * c.n[1] * c.n[2];
+    std::vector<int64_t> bp(nbox + 1, 0);
+    for (int64_t i = 0; i < Nall; ++i) bp[((int64_t)an[3 * i + 2] * c.n[1] + an[3 * i + 1]) * c.n[0] + an[3 * i] + 1]++;
+    for (int64_t b = 0; b < nbox; ++b) bp[b + 1] += bp[b];
+    // anchor ranges of axis a around [lo, hi] (stored anchors), up to two increasing ranges
+    auto ranges = [&](int a, int lo, int hi, int* r) {
+      const int N = c.n[a];
+      lo -= R[a]; hi += R[a];
+      if (!c.per[a]) { r[0] = std::max(lo, 0); r[1] = std::min(hi, lim[a]); return r[0] <= r[1] ? 1 : 0; }
+      if (hi - lo + 1 >= N) { r[0] = 0; r[1] = N - 1; return 1; }
+      const int wl = ((lo % N) + N) % N, wh = ((hi % N) + N) % N;
+      if (wl <= wh) { r[0] = wl; r[1] = wh; return 1; }
+      r[0] = 0; r[1] = wh; r[2] = wl; r[3] = N - 1; return 2;
+    };
+    std::vector<int64_t> trow;
+    std::vector<int> rptr(1, 0), rstart, rlen, rloc, tile_of(Np);
+    std::vector<std::pair<int64_t, int64_t>> runs;
+    auto window = [&](int64_t i0, int64_t i1) {      // runs of the window of own rows [i0, i1)
+      runs.clear();
+      const int y = an[3 * i0 + 1], z = an[3 * i0 + 2];
+      int xa = an[3 * i0], xb = an[3 * (i1 - 1)];
+      int rx[4], ry[4], rz[4];
+      const int nx = ranges(0, xa, xb, rx), ny = ranges(1, y, y, ry), nz = ranges(2, z, z, rz);
+      int64_t tot = 0;
+      for (int iz = 0; iz < nz; ++iz)
+        for (int zz = rz[2 * iz]; zz <= rz[2 * iz + 1]; ++zz)
+          for (int iy = 0; iy < ny; ++iy)
+            for (int yy = ry[2 * iy]; yy <= ry[2 * iy + 1]; ++yy) {
+              const int64_t line = ((int64_t)zz * c.n[1] + yy) * c.n[0];
+              for (int ix = 0; ix < nx; ++ix) {
+                const int64_t k0 = bp[line + rx[2 * ix]], k1 = bp[line + rx[2 * ix + 1] + 1];
+                if (k1 > k0) { runs.push_back({k0, k1 - k0}); tot += k1 - k0; }
+              }
+            }
+      return tot;
+    };
+    int wmax = 0;
+    bool fits = true;
+    for (int64_t i = r0; i < r0 + Np && fits;) {
+      int64_t j = i + 1;
+      while (j < r0 + Np && j - i < W4_TMAX && an[3 * j + 1] == an[3 * i + 1] && an[3 * j + 2] == an[3 * i + 2]) ++j;
+      int64_t w = window(i, j);
+      while (w > W4_WMAX && j - i > 1) { j = i + (j - i) / 2; w = window(i, j); }
+      if (w > W4_WMAX || w > 65535) { fits = false; break; }
+      std::sort(runs.begin(), runs.end());
+      int loc = 0;
+      for (auto& rn : runs) { rstart.push_back((int)rn.first); rlen.push_back((int)rn.second); rloc.push_back(loc); loc += (int)rn.second; }
+      rptr.push_back((int)rstart.size());
+      for (int64_t k = i; k < j; ++k) tile_of[k - r0] = (int)trow.size();
+      trow.push_back(i);
+      wmax = std::max<int>(wmax, (int)w);
+      i = j;
+    }
+    trow.push_back(r0 + Np);
+    if (fits) {
+      std::vector<long long> wptr(Np + 1, 0);
+      for (int64_t i = 0; i < Np; ++i) wptr[i + 1] = wptr[i] + (cnt[i] + 3) / 4;
+      long long* d_wptr = dup_c(wptr);
+      int* d_tof = dup_c(tile_of);
+      int* d_rptr = dup_c(rptr);
+      int* d_rs = dup_c(rstart);
+      int* d_rl = dup_c(rlen);
+      int* d_rc = dup_c(rloc);
+      float* d_wval = dalloc_c<float>(4 * (size_t)wptr[Np]);
+      unsigned short* d_widx = dalloc_c<unsigned short>(4 * (size_t)wptr[Np]);
+      unsigned long long* d_miss = dalloc_c<unsigned long long>(1);
+      CKC(cudaMemset(d_miss, 0, sizeof(unsigned long long)));
+      k_w4_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_tof, d_rptr, d_rs, d_rl, d_rc, d_wptr, d_wval, d_widx, d_miss);
+      CKC(cudaGetLastError());
+      unsigned long long miss = 0;
+      CKC(cudaMemcpy(&miss, d_miss, sizeof(miss), cudaMemcpyDeviceToHost));
+      cudaFree(d_miss); cudaFree(d_tof);
+      if (miss == 0) {
+        D.c_ptr = reinterpret_cast<int64_t*>(d_wptr);
+        D.c_val = d_wval;
+        D.w_idx = reinterpret_cast<ushort4*>(d_widx);
+        D.w_trow = dup_c(trow);
+        D.w_rptr = d_rptr; D.w_rstart = d_rs; D.w_rlen = d_rl; D.w_rloc = d_rc;
+        D.w_ntiles = (int64_t)trow.size() - 1;
+        D.w_max = std::max(wmax, 1);
+        D.cbox_chunks = wptr[Np];
+        D.cbox_format = 5;
+        if (std::getenv("PMFEM_VERBOSE"))
+          std::fprintf(stderr, "[pmfem] W4 C_box: %lld tiles, %zu runs, largest window %d rows\n",
+                       (long long)D.w_ntiles, rstart.size(), wmax);
+        CKC(cudaDeviceSynchronize());
+        cudaFree(d_xw); cudaFree(d_tl); cudaFree(d_su); cudaFree(d_cnt); cudaFree(d_nch);
+        cudaFree(d_ptr); cudaFree(d_col); cudaFree(d_val);
+        D.cbox_nnz = nnz;
+        return nnz;
+      }
+      cudaFree(d_wptr); cudaFree(d_rptr); cudaFree(d_rs); cudaFree(d_rl); cudaFree(d_rc); cudaFree(d_wval);
+      cudaFree(d_widx);
+    }
+    if (std::getenv("PMFEM_VERBOSE"))
+      std::fprintf(stderr, "[pmfem] W4 C_box not usable (%s): packed format\n", fits ? "near columns outside a window" : "window too large");
+  }
   const double per_box = (double)Nall / ((double)c.n[0] * c.n[1] * c.n[2]);
   const double u4_fill = uptr[Np] ? (double)nnz / (double)uptr[Np] : 4.0;
   bool use_b4 = fmt == "b4";

@@ -502,6 +502,88 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
   if (valid && lane == 0) u[n] = acc + ul;
 }
 
+// K4 over the W4 C_box (cbox_format 5, cbox_gpu.cu): ONE CTA PER TILE of consecutive rows of
+// one anchor line.  The tile's q window -- the rows of every anchor box within the candidate
+// reach of the tile, as runs of consecutive internal rows -- is staged into shared memory once;
+// the C_box chunks (float4 values + ushort4 window-local indices, 24 bytes per 4 entries)
+// stream from HBM and their gathers hit shared memory instead of L1/L2 (the q gathers made the
+// global-index formats L1-request bound: ncu C4 C4x L1 hit 77 %, DRAM 49-61 % of peak).  G lanes
+// per row as k4_interp_corr; rows of the tile in passes of 256 / G.
+template <int P, int G>
+__global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
+                                              const float4* __restrict__ st_t, GridDims g,
+                                              const int64_t* __restrict__ tile_row, const int* __restrict__ run_ptr,
+                                              const int* __restrict__ run_start, const int* __restrict__ run_len,
+                                              const int* __restrict__ run_loc, const int64_t* __restrict__ c_ptr,
+                                              const float4* __restrict__ c_val4, const ushort4* __restrict__ c_idx,
+                                              const float* __restrict__ q, const float* __restrict__ uloc,
+                                              float* __restrict__ u, int wmax) {
+  extern __shared__ float qs[];
+  const int t = blockIdx.x;
+  {
+    const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+    for (int r = run_ptr[t] + warp; r < run_ptr[t + 1]; r += blockDim.x >> 5) {
+      const int s0 = run_start[r], len = run_len[r], loc = run_loc[r];
+      DCHECK(loc >= 0 && loc + len <= wmax && s0 >= 0 && s0 + len <= rr.ncol);
+      for (int j = l32; j < len; j += 32) qs[loc + j] = __ldg(q + s0 + j);
+    }
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & (G - 1);
+  const int64_t row0 = tile_row[t], row1 = tile_row[t + 1];
+  for (int64_t base = row0; base < row1; base += 256 / G) {
+    const int64_t n = base + (threadIdx.x / G);
+    const bool valid = n < row1;
+    float acc = 0.f;
+    const int64_t b = valid ? c_ptr[n - rr.row0] : 0, e_end = valid ? c_ptr[n - rr.row0 + 1] : 0;
+    const float ul = (valid && lane == 0) ? uloc[n] : 0.f;
+    constexpr int NR = (P + 1) * (P + 1);
+    if (valid && lane < NR) {
+      const int4 s = st_s[n];
+      const float4 tt = st_t[n];
+      float wx[P + 1], wy[P + 1], wz[P + 1];
+      lagr<P>(tt.x, wx); lagr<P>(tt.y, wy); lagr<P>(tt.z, wz);
+      int ix[P + 1];
+#pragma unroll
+      for (int i = 0; i <= P; ++i) ix[i] = wrapi(s.x + i, g.n0, g.per0);
+      for (int r = lane; r < NR; r += G) {
+        const int jy = r % (P + 1), jz = r / (P + 1);
+        float wyz = 0.f;
+#pragma unroll
+        for (int a = 0; a <= P; ++a)
+#pragma unroll
+          for (int c = 0; c <= P; ++c)
+            if (a == jy && c == jz) wyz = wy[a] * wz[c];
+        const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+        float v = 0.f;
+#pragma unroll
+        for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(row + ix[i]), v);
+        acc = fmaf(wyz, v, acc);
+      }
+    }
+    constexpr int KB = 4;
+    for (int64_t e0 = b + lane; e0 < e_end; e0 += KB * G) {
+      ushort4 id[KB];
+      float4 vv[KB];
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        const int64_t e = e0 + (int64_t)j * G;
+        const bool ok = e < e_end;
+        id[j] = ok ? __ldcs(c_idx + e) : make_ushort4(0, 0, 0, 0);
+        vv[j] = ok ? __ldcs(c_val4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < KB; ++j) {
+        DCHECK(id[j].x < wmax && id[j].y < wmax && id[j].z < wmax && id[j].w < wmax);
+        acc = fmaf(vv[j].x, qs[id[j].x], fmaf(vv[j].y, qs[id[j].y], fmaf(vv[j].z, qs[id[j].z], fmaf(vv[j].w, qs[id[j].w], acc))));
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (valid && lane == 0) u[n] = acc + ul;
+  }
+}
+
 // K4 "stream" variant for the block formats (B4: F = 1, U4: F = 3), PMFEM_K4_STREAM=1: a warp
 // owns RPW consecutive rows and streams their C_box blocks as ONE contiguous range
 // [c_ptr[r0], c_ptr[r0 + RPW]) -- 32 consecutive blocks per step, KB steps of index/value loads
@@ -1283,7 +1365,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     D.kernel_bytes[3] = nloc * (16.0 + 16 + 16 + 4 + 4 + 4) + (double)cnnz * 4 + (double)D.seg_mask_words * 4 + Gl * 4.0;
   else if (D.cbox_format == 3)   // + the q4 copy (4-byte read, 16-byte write per row)
     D.kernel_bytes[3] = nloc * (16.0 + 16 + 8 + 4 + 4 + 4) + Np * 20.0 + (double)cnnz * 5 + Gl * 4.0;
-  else
+  else   // C4x and W4: 4-byte value + 2 bytes of chunk header / window index per near pair
     D.kernel_bytes[3] = nloc * (16.0 + 16 + 8 + 4 + 4 + 4) + (double)cnnz * (D.cbox_format == 1 ? 5 : 6) + Gl * 4.0;
   D.kernel_bytes[4] = nloc * (4.0 + 12 + 12) + n1e * 16;        // u, H read+write, (G, col)
 }
@@ -1357,7 +1439,7 @@ void device_free(DeviceState& D) {
   cudaSetDevice(D.device);
   device_bloch_free(D);
   void* ptrs[] = {D.sl_off, D.sl1_off, D.s_zc, D.s_LD, D.s_Gc, D.m4, D.rowsum, D.c_ptr, D.c_hdr, D.c_bidx, D.c_val,
-                  D.seg_moff, D.seg_mask, D.q4,
+                  D.seg_moff, D.seg_mask, D.q4, D.w_trow, D.w_rptr, D.w_rstart, D.w_rlen, D.w_rloc, D.w_idx,
                   D.st_s, D.st_t, D.box_ptr, D.spec, D.q, D.uloc, D.u, D.Q, D.C, D.m_stage, D.H_stage,
                   D.tw32[0], D.tw32[1], D.tw32[2], D.tw64[0], D.tw64[1], D.tw64[2],
                   D.send_buf, D.recv_buf, D.slab_cx, D.slab_buf, D.slab_spec, D.send_idx[0], D.send_idx[1], D.send_idx[2],
@@ -1652,6 +1734,26 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
       default: K4T_LAUNCH(3); break;
     }
 #undef K4T_LAUNCH
+  } else if (D.cbox_format == 5) {
+    const size_t smem = sizeof(float) * (size_t)D.w_max;
+#define K4W_LAUNCH(PP, GG)                                                                                  \
+  do {                                                                                                      \
+    CK(cudaFuncSetAttribute(k4_win<PP, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
+    k4_win<PP, GG><<<(unsigned)D.w_ntiles, 256, smem, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.w_trow, D.w_rptr,   \
+                                                            D.w_rstart, D.w_rlen, D.w_rloc, D.c_ptr, v4,      \
+                                                            D.w_idx, D.q, D.uloc, D.u, D.w_max);            \
+  } while (0)
+#define K4W_BY_G(PP) \
+  if (D.k4_group == 8) K4W_LAUNCH(PP, 8); else if (D.k4_group == 16) K4W_LAUNCH(PP, 16); else K4W_LAUNCH(PP, 32)
+    if (D.w_ntiles > 0) {
+      switch (D.order) {
+        case 1: K4W_BY_G(1); break;
+        case 2: K4W_BY_G(2); break;
+        default: K4W_BY_G(3); break;
+      }
+    }
+#undef K4W_BY_G
+#undef K4W_LAUNCH
   } else if (D.cbox_format == 2) {
     const int G = D.k4_group;
     const size_t smem = sizeof(int) * (size_t)(256 / G) * (2 * D.seg_maxseg + 2);

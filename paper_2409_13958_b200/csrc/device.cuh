@@ -96,6 +96,17 @@ struct DeviceState {
   uint32_t* seg_mask = nullptr;       // SEG: candidate bitmasks
   int64_t seg_mask_words = 0;
   int* c_bidx = nullptr;              // B4 block index (column >> 2) per block
+  // W4 (cbox_format 5): tiles of consecutive own rows of one anchor line; per tile the runs of
+  // internal rows forming its q window (staged in shared memory by K4) and per chunk the
+  // window-local indices of its 4 entries
+  int64_t w_ntiles = 0;
+  int w_max = 0;                      // largest window (floats of shared memory)
+  int64_t* w_trow = nullptr;          // [ntiles+1] first internal row of each tile
+  int* w_rptr = nullptr;              // [ntiles+1] run offsets
+  int* w_rstart = nullptr;            // run first internal row
+  int* w_rlen = nullptr;              // run length
+  int* w_rloc = nullptr;              // run offset in the window
+  ushort4* w_idx = nullptr;           // [chunks] window-local indices
   int k4_group = 32;          // lanes per row in K4 (8/16/32 from the mean padded row length)
   // stencils
   int4* st_s = nullptr;       // wrapped (periodic) / clamped anchors

@@ -1,4 +1,5 @@
 // extern "C" entry points of libpmfem (include/pmfem.h).  No exception crosses the ABI.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -581,6 +582,32 @@ pmfem_status pmfem_export(pmfem_ctx ctx, const char* name, void* dst, int64_t* c
       } else if (tail == "val") {
         *count = 4 * nch;
         if (dst && nch) cudaMemcpy(dst, D.c_val, sizeof(float) * 4 * (size_t)nch, cudaMemcpyDeviceToHost);
+      } else if (tail == "col" && D.cbox_format == 5) {
+        // W4: window-local index -> run (runs of a tile sorted by first row, window offsets
+        // increasing with it) -> internal row
+        *count = 4 * nch;
+        if (dst && nch) {
+          const int64_t nt = D.w_ntiles;
+          std::vector<int64_t> trow(nt + 1);
+          std::vector<int> rptr(nt + 1);
+          cudaMemcpy(trow.data(), D.w_trow, sizeof(int64_t) * (nt + 1), cudaMemcpyDeviceToHost);
+          cudaMemcpy(rptr.data(), D.w_rptr, sizeof(int) * (nt + 1), cudaMemcpyDeviceToHost);
+          std::vector<int> rs(rptr[nt]), rc(rptr[nt]);
+          cudaMemcpy(rs.data(), D.w_rstart, sizeof(int) * rs.size(), cudaMemcpyDeviceToHost);
+          cudaMemcpy(rc.data(), D.w_rloc, sizeof(int) * rc.size(), cudaMemcpyDeviceToHost);
+          std::vector<uint16_t> id(4 * (size_t)nch);
+          cudaMemcpy(id.data(), D.w_idx, sizeof(uint16_t) * id.size(), cudaMemcpyDeviceToHost);
+          int32_t* c = static_cast<int32_t*>(dst);
+          // (slot order inside a row is quarter-transposed; the export lists the slots as stored)
+          for (int64_t t = 0; t < nt; ++t)
+            for (int64_t e = 4 * ptr[trow[t] - D.lo]; e < 4 * ptr[trow[t + 1] - D.lo]; ++e) {
+              const int* b = rc.data() + rptr[t];
+              const int* en = rc.data() + rptr[t + 1];
+              const int* f = std::upper_bound(b, en, (int)id[e]);
+              const int r = (int)(f - b) - 1 + rptr[t];
+              c[e] = rs[r] + ((int)id[e] - rc[r]);
+            }
+        }
       } else if (tail == "col" && (D.cbox_format == 1 || D.cbox_format == 3)) {
         // B4: aligned block index b -> columns 4b..4b+3; U4: start column c -> c..c+3
         *count = 4 * nch;

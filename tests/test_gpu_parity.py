@@ -232,7 +232,7 @@ def test_slab_fft_simulated_ranks(key, world, monkeypatch):
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
 
 
-@pytest.mark.parametrize("fmt", ["u4", "u4-stream", "b4-stream", "seg", "c4x", "c4x-vec", "b4"])
+@pytest.mark.parametrize("fmt", ["u4", "u4-stream", "b4-stream", "seg", "c4x", "c4x-vec", "b4", "w4"])
 @pytest.mark.parametrize("key", ["C2p2", "C3p1", "N1p2", "C4p3"])
 def test_cbox_formats(key, fmt, monkeypatch):
     """K4 streaming either packed C_box format (C4x also with vector gathers of run chunks; the

@@ -9,13 +9,13 @@ from helpers import SMALL, lib_context
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("fmt", ["u4", "seg", "c4x", "b4"])
+@pytest.mark.parametrize("fmt", ["u4", "seg", "c4x", "b4", "w4"])
 @pytest.mark.parametrize("key", sorted(SMALL))
 def test_device_cbox_matches_host(key, fmt, monkeypatch):
     """Both packed C_box formats (C4x chunks, B4 aligned blocks) decode to the host matrix."""
     monkeypatch.setenv("PMFEM_CBOX_FORMAT", fmt)
     dev = lib_context(key, device=0)
-    assert dev.export("cbox_device_format")[0] == {"c4x": 0, "b4": 1, "seg": 2, "u4": 3}[fmt]
+    assert dev.export("cbox_device_format")[0] == {"c4x": 0, "b4": 1, "seg": 2, "u4": 3, "w4": 5}[fmt]
     host = lib_context(key, device=-1)
     n = host.n_parents
     perm = dev.export("perm")                     # internal -> user parent id
