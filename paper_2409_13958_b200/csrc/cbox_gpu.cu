@@ -572,7 +572,6 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   // rows; a tile is halved until its window fits W4_WMAX floats of shared memory.  Every near
   // column must fall in its row's window (checked: otherwise another format is used).
   if (fmt == "w4") {
-    constexpr int W4_TMAX = 128;
     const int W4_WMAX = std::getenv("PMFEM_W4_WMAX") ? std::atoi(std::getenv("PMFEM_W4_WMAX")) : 4096;
     int R[3], lim[3];
     for (int a = 0; a < 3; ++a) {
@@ -623,14 +622,14 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
             }
       return tot;
     };
-    int wmax = 0;
+    int wmax = 0, umax = 0;
     bool fits = true;
     for (int64_t i = r0; i < r0 + Np && fits;) {
       int64_t j = i + 1;
       while (j < r0 + Np && j - i < W4_TMAX && an[3 * j + 1] == an[3 * i + 1] && an[3 * j + 2] == an[3 * i + 2]) ++j;
       int64_t w = window(i, j);
-      while (w > W4_WMAX && j - i > 1) { j = i + (j - i) / 2; w = window(i, j); }
-      if (w > W4_WMAX || w > 65535) { fits = false; break; }
+      while ((w > W4_WMAX || runs.size() > (size_t)W4_RMAX) && j - i > 1) { j = i + (j - i) / 2; w = window(i, j); }
+      if (w > W4_WMAX || w > 65535 || runs.size() > (size_t)W4_RMAX) { fits = false; break; }
       std::sort(runs.begin(), runs.end());
       int loc = 0;
       for (auto& rn : runs) { rstart.push_back((int)rn.first); rlen.push_back((int)rn.second); rloc.push_back(loc); loc += (int)rn.second; }
@@ -638,6 +637,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
       for (int64_t k = i; k < j; ++k) tile_of[k - r0] = (int)trow.size();
       trow.push_back(i);
       wmax = std::max<int>(wmax, (int)w);
+      umax = std::max<int>(umax, ((an[3 * (j - 1)] - an[3 * i] + p + 1) | 1) * (p + 1) * (p + 1));
       i = j;
     }
     trow.push_back(r0 + Np);
@@ -667,6 +667,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
         D.w_rptr = d_rptr; D.w_rstart = d_rs; D.w_rlen = d_rl; D.w_rloc = d_rc;
         D.w_ntiles = (int64_t)trow.size() - 1;
         D.w_max = std::max(wmax, 1);
+        D.w_umax = umax;
         D.cbox_chunks = wptr[Np];
         D.cbox_format = 5;
         if (std::getenv("PMFEM_VERBOSE"))

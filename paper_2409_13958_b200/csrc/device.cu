@@ -503,13 +503,18 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
 }
 
 // K4 over the W4 C_box (cbox_format 5, cbox_gpu.cu): ONE CTA PER TILE of consecutive rows of
-// one anchor line.  The tile's q window -- the rows of every anchor box within the candidate
-// reach of the tile, as runs of consecutive internal rows -- is staged into shared memory once;
-// the C_box chunks (float4 values + ushort4 window-local indices, 24 bytes per 4 entries)
-// stream from HBM and their gathers hit shared memory instead of L1/L2 (the q gathers made the
-// global-index formats L1-request bound: ncu C4 C4x L1 hit 77 %, DRAM 49-61 % of peak).  G lanes
-// per row as k4_interp_corr; rows of the tile in passes of 256 / G.
-template <int P, int G>
+// one anchor line.  Staged once per tile in shared memory:
+//  * the q window -- the rows of every anchor box within the candidate reach of the tile, as
+//    runs of consecutive internal rows (a warp per run);
+//  * the U sub-grid of the tile's stencils -- the rows share the (y, z) anchor, so their
+//    (P+1)^3 stencils lie in (P+1)^2 grid lines over x in [xa, xb + P] (xa, xb the first and
+//    last row's x anchor), stored with an odd line pitch (distinct banks across the lines).
+// The C_box chunks (float4 values + ushort4 window-local indices, 24 bytes per 4 entries) then
+// stream from HBM and every gather -- q and U -- hits shared memory: the global-index formats
+// were L1-request bound (ncu C4 C4x: L1 hit 77 %, DRAM 49-61 % of peak), and the (P+1)^2
+// scattered U line gathers per row were as many L1 wavefronts as the q gathers.  G lanes per
+// row as k4_interp_corr; rows of the tile in passes of 256 / G.
+template <int P, int G, int KB>
 __global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
                                               const float4* __restrict__ st_t, GridDims g,
                                               const int64_t* __restrict__ tile_row, const int* __restrict__ run_ptr,
@@ -517,35 +522,76 @@ __global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restri
                                               const int* __restrict__ run_loc, const int64_t* __restrict__ c_ptr,
                                               const float4* __restrict__ c_val4, const ushort4* __restrict__ c_idx,
                                               const float* __restrict__ q, const float* __restrict__ uloc,
-                                              float* __restrict__ u, int wmax) {
+                                              float* __restrict__ u, int wmax, int umax) {
   extern __shared__ float qs[];
+  float* us = qs + wmax;
+  __shared__ int64_t cp[W4_TMAX + 1];     // the tile's chunk offsets (no dependent load per row)
+  __shared__ int rs_s[W4_RMAX], rl_s[W4_RMAX + 1];   // the tile's runs: first row, window offset
+  constexpr int NR = (P + 1) * (P + 1);
   const int t = blockIdx.x;
+  const int64_t row0 = tile_row[t], row1 = tile_row[t + 1];
+  DCHECK(row1 - row0 <= W4_TMAX);
+  for (int i = threadIdx.x; i <= (int)(row1 - row0); i += blockDim.x) cp[i] = c_ptr[row0 - rr.row0 + i];
+  const int4 sa = st_s[row0];
+  const int xa = sa.x, nxs = st_s[row1 - 1].x - xa + P + 1, pitch = nxs | 1;
+  DCHECK(pitch * NR <= umax);
   {
-    const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
-    for (int r = run_ptr[t] + warp; r < run_ptr[t + 1]; r += blockDim.x >> 5) {
-      const int s0 = run_start[r], len = run_len[r], loc = run_loc[r];
-      DCHECK(loc >= 0 && loc + len <= wmax && s0 >= 0 && s0 + len <= rr.ncol);
-      for (int j = l32; j < len; j += 32) qs[loc + j] = __ldg(q + s0 + j);
+    // run descriptors into shared memory (one round trip), then the window copy flattened over
+    // all threads (each finds its element's run by binary search): ~3 dependent round trips per
+    // tile instead of two per run and warp (ncu C4: the per-warp run loop was 27 % of the stalls)
+    const int rp0 = run_ptr[t], nrun = run_ptr[t + 1] - rp0;
+    DCHECK(nrun <= W4_RMAX);
+    for (int r = threadIdx.x; r < nrun; r += blockDim.x) {
+      rs_s[r] = run_start[rp0 + r];
+      rl_s[r] = run_loc[rp0 + r];
+    }
+    if (threadIdx.x == 0) rl_s[nrun] = nrun ? run_loc[rp0 + nrun - 1] + run_len[rp0 + nrun - 1] : 0;
+    for (int i = threadIdx.x; i < nxs * NR; i += blockDim.x) {
+      const int ix = i % nxs, l = i / nxs, jy = l % (P + 1), jz = l / (P + 1);
+      us[l * pitch + ix] = __ldg(U + ((int64_t)wrapi(sa.z + jz, g.n2, g.per2) * g.n1 + wrapi(sa.y + jy, g.n1, g.per1)) * g.n0 +
+                                wrapi(xa + ix, g.n0, g.per0));
+    }
+    __syncthreads();
+    const int wlen = rl_s[nrun];
+    DCHECK(wlen <= wmax);
+    constexpr int CB = 8;
+    for (int f0 = threadIdx.x; f0 < wlen; f0 += CB * blockDim.x) {
+      float v[CB];
+      int at[CB];
+#pragma unroll
+      for (int c = 0; c < CB; ++c) {
+        const int f = f0 + c * blockDim.x;
+        at[c] = -1;
+        v[c] = 0.f;
+        if (f < wlen) {
+          int lo = 0, hi = nrun - 1;                       // last run with loc <= f
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rl_s[mid] <= f) lo = mid; else hi = mid - 1;
+          }
+          DCHECK(rs_s[lo] + (f - rl_s[lo]) < rr.ncol);
+          v[c] = __ldg(q + rs_s[lo] + (f - rl_s[lo]));
+          at[c] = f;
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CB; ++c)
+        if (at[c] >= 0) qs[at[c]] = v[c];
     }
   }
   __syncthreads();
   const int lane = threadIdx.x & (G - 1);
-  const int64_t row0 = tile_row[t], row1 = tile_row[t + 1];
   for (int64_t base = row0; base < row1; base += 256 / G) {
     const int64_t n = base + (threadIdx.x / G);
     const bool valid = n < row1;
     float acc = 0.f;
-    const int64_t b = valid ? c_ptr[n - rr.row0] : 0, e_end = valid ? c_ptr[n - rr.row0 + 1] : 0;
+    const int64_t b = valid ? cp[n - row0] : 0, e_end = valid ? cp[n - row0 + 1] : 0;
     const float ul = (valid && lane == 0) ? uloc[n] : 0.f;
-    constexpr int NR = (P + 1) * (P + 1);
     if (valid && lane < NR) {
-      const int4 s = st_s[n];
+      const int sx = st_s[n].x - xa;
       const float4 tt = st_t[n];
       float wx[P + 1], wy[P + 1], wz[P + 1];
       lagr<P>(tt.x, wx); lagr<P>(tt.y, wy); lagr<P>(tt.z, wz);
-      int ix[P + 1];
-#pragma unroll
-      for (int i = 0; i <= P; ++i) ix[i] = wrapi(s.x + i, g.n0, g.per0);
       for (int r = lane; r < NR; r += G) {
         const int jy = r % (P + 1), jz = r / (P + 1);
         float wyz = 0.f;
@@ -554,14 +600,14 @@ __global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restri
 #pragma unroll
           for (int c = 0; c <= P; ++c)
             if (a == jy && c == jz) wyz = wy[a] * wz[c];
-        const float* row = U + ((int64_t)wrapi(s.z + jz, g.n2, g.per2) * g.n1 + wrapi(s.y + jy, g.n1, g.per1)) * g.n0;
+        const float* row = us + r * pitch + sx;
         float v = 0.f;
 #pragma unroll
-        for (int i = 0; i <= P; ++i) v = fmaf(wx[i], __ldg(row + ix[i]), v);
+        for (int i = 0; i <= P; ++i) v = fmaf(wx[i], row[i], v);
         acc = fmaf(wyz, v, acc);
       }
     }
-    constexpr int KB = 4;
+    // KB chunks per lane in flight: the whole row's loads at once for rows of <= KB * G chunks
     for (int64_t e0 = b + lane; e0 < e_end; e0 += KB * G) {
       ushort4 id[KB];
       float4 vv[KB];
@@ -1735,13 +1781,13 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     }
 #undef K4T_LAUNCH
   } else if (D.cbox_format == 5) {
-    const size_t smem = sizeof(float) * (size_t)D.w_max;
+    const size_t smem = sizeof(float) * ((size_t)D.w_max + D.w_umax);
 #define K4W_LAUNCH(PP, GG)                                                                                  \
   do {                                                                                                      \
-    CK(cudaFuncSetAttribute(k4_win<PP, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));       \
-    k4_win<PP, GG><<<(unsigned)D.w_ntiles, 256, smem, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.w_trow, D.w_rptr,   \
+    CK(cudaFuncSetAttribute(k4_win<PP, GG, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    k4_win<PP, GG, 6><<<(unsigned)D.w_ntiles, 256, smem, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.w_trow, D.w_rptr, \
                                                             D.w_rstart, D.w_rlen, D.w_rloc, D.c_ptr, v4,      \
-                                                            D.w_idx, D.q, D.uloc, D.u, D.w_max);            \
+                                                            D.w_idx, D.q, D.uloc, D.u, D.w_max, D.w_umax);  \
   } while (0)
 #define K4W_BY_G(PP) \
   if (D.k4_group == 8) K4W_LAUNCH(PP, 8); else if (D.k4_group == 16) K4W_LAUNCH(PP, 16); else K4W_LAUNCH(PP, 32)

@@ -62,6 +62,9 @@ __host__ __device__ __forceinline__ int seg_at(const int* r, int i) {
   return i < l0 ? r[0] + i : r[2] + (i - l0);
 }
 
+constexpr int W4_TMAX = 128;   // W4 C_box: rows per tile (cbox_gpu.cu builder, K4 k4_win)
+constexpr int W4_RMAX = 512;   // W4 C_box: runs per tile (the builder splits tiles above it)
+
 struct DeviceState {
   int device = -1;
   int64_t Np = 0;
@@ -101,6 +104,7 @@ struct DeviceState {
   // window-local indices of its 4 entries
   int64_t w_ntiles = 0;
   int w_max = 0;                      // largest window (floats of shared memory)
+  int w_umax = 0;                     // largest U sub-grid of a tile (odd line pitch x (P+1)^2 floats)
   int64_t* w_trow = nullptr;          // [ntiles+1] first internal row of each tile
   int* w_rptr = nullptr;              // [ntiles+1] run offsets
   int* w_rstart = nullptr;            // run first internal row
