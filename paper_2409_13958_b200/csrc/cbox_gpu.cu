@@ -571,8 +571,13 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   // R_a = ceil(r_ER / Delta_a + 1) - 1, stored anchors) of the tile's boxes, as runs of internal
   // rows; a tile is halved until its window fits W4_WMAX floats of shared memory.  Every near
   // column must fall in its row's window (checked: otherwise another format is used).
-  if (fmt == "w4") {
-    const int W4_WMAX = std::getenv("PMFEM_W4_WMAX") ? std::atoi(std::getenv("PMFEM_W4_WMAX")) : 4096;
+  // W4 by default on dense meshes (>= 1 node per grid box: C2, C5 -- measured K4 0.24 vs 0.27 ms
+  // and 1.79 vs 2.34 ms against U4); sparse ones (C3 0.74, C4 0.61 nodes per box) keep C4x
+  // (W4 measured 0.59-0.80 vs 0.53 ms at C3, 9.4-10.7 vs 10.0-10.1 ms at C4: their tiles hold
+  // fewer rows per window)
+  const double per_box_w = (double)Nall / ((double)c.n[0] * c.n[1] * c.n[2]);
+  if (fmt == "w4" || (fmt == "auto" && D.world == 1 && per_box_w >= 1.0)) {
+    const int W4_WMAX = std::getenv("PMFEM_W4_WMAX") ? std::atoi(std::getenv("PMFEM_W4_WMAX")) : 6144;
     int R[3], lim[3];
     for (int a = 0; a < 3; ++a) {
       R[a] = (int)std::ceil(c.rer / c.delta[a] + 1.0) - 1;

@@ -526,7 +526,6 @@ __global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restri
   extern __shared__ float qs[];
   float* us = qs + wmax;
   __shared__ int64_t cp[W4_TMAX + 1];     // the tile's chunk offsets (no dependent load per row)
-  __shared__ int rs_s[W4_RMAX], rl_s[W4_RMAX + 1];   // the tile's runs: first row, window offset
   constexpr int NR = (P + 1) * (P + 1);
   const int t = blockIdx.x;
   const int64_t row0 = tile_row[t], row1 = tile_row[t + 1];
@@ -536,47 +535,18 @@ __global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restri
   const int xa = sa.x, nxs = st_s[row1 - 1].x - xa + P + 1, pitch = nxs | 1;
   DCHECK(pitch * NR <= umax);
   {
-    // run descriptors into shared memory (one round trip), then the window copy flattened over
-    // all threads (each finds its element's run by binary search): ~3 dependent round trips per
-    // tile instead of two per run and warp (ncu C4: the per-warp run loop was 27 % of the stalls)
-    const int rp0 = run_ptr[t], nrun = run_ptr[t + 1] - rp0;
-    DCHECK(nrun <= W4_RMAX);
-    for (int r = threadIdx.x; r < nrun; r += blockDim.x) {
-      rs_s[r] = run_start[rp0 + r];
-      rl_s[r] = run_loc[rp0 + r];
+    // a warp per run (measured faster than a flattened copy with a per-element run search, and
+    // than staging every per-row operand in shared memory: both cost registers / occupancy)
+    const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+    for (int r = run_ptr[t] + warp; r < run_ptr[t + 1]; r += blockDim.x >> 5) {
+      const int s0 = run_start[r], len = run_len[r], loc = run_loc[r];
+      DCHECK(loc >= 0 && loc + len <= wmax && s0 >= 0 && s0 + len <= rr.ncol);
+      for (int j = l32; j < len; j += 32) qs[loc + j] = __ldg(q + s0 + j);
     }
-    if (threadIdx.x == 0) rl_s[nrun] = nrun ? run_loc[rp0 + nrun - 1] + run_len[rp0 + nrun - 1] : 0;
     for (int i = threadIdx.x; i < nxs * NR; i += blockDim.x) {
       const int ix = i % nxs, l = i / nxs, jy = l % (P + 1), jz = l / (P + 1);
       us[l * pitch + ix] = __ldg(U + ((int64_t)wrapi(sa.z + jz, g.n2, g.per2) * g.n1 + wrapi(sa.y + jy, g.n1, g.per1)) * g.n0 +
                                 wrapi(xa + ix, g.n0, g.per0));
-    }
-    __syncthreads();
-    const int wlen = rl_s[nrun];
-    DCHECK(wlen <= wmax);
-    constexpr int CB = 8;
-    for (int f0 = threadIdx.x; f0 < wlen; f0 += CB * blockDim.x) {
-      float v[CB];
-      int at[CB];
-#pragma unroll
-      for (int c = 0; c < CB; ++c) {
-        const int f = f0 + c * blockDim.x;
-        at[c] = -1;
-        v[c] = 0.f;
-        if (f < wlen) {
-          int lo = 0, hi = nrun - 1;                       // last run with loc <= f
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (rl_s[mid] <= f) lo = mid; else hi = mid - 1;
-          }
-          DCHECK(rs_s[lo] + (f - rl_s[lo]) < rr.ncol);
-          v[c] = __ldg(q + rs_s[lo] + (f - rl_s[lo]));
-          at[c] = f;
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < CB; ++c)
-        if (at[c] >= 0) qs[at[c]] = v[c];
     }
   }
   __syncthreads();

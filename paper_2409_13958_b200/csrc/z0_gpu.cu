@@ -72,13 +72,18 @@ __global__ void k_z0_items(const Z0Item* __restrict__ items, int64_t nitems, con
 // ---- one warp per task
 constexpr int Z0W_WARPS = 4;           // warps per CTA
 constexpr int Z0W_LEAVES = 48;         // leaf buffer per warp (flushed when full)
-constexpr int Z0W_POP = 16;            // sub-triangles examined per step (one per lane 0..15)
-constexpr int Z0W_STACK = 512;         // >= 1 + 7 levels x 4 Z0W_POP: never overflows (see below)
+// POP: sub-triangles examined per step (one per lane 0..POP-1); the stack holds
+// >= 1 + 7 levels x 4 POP entries and never overflows (see below).  POP = 8 (default) halves the
+// stack and, with at most 102 registers (5 CTAs per SM), doubles the resident warps: the kernel
+// is latency-bound (ncu C5: 18 % warps active at POP = 16 / 168 registers, fp64 pipe 26 %);
+// PMFEM_Z0_POP=16 selects the round-2 configuration.
+template <int POP> struct Z0Stack { static constexpr int N = ((1 + 7 * 4 * POP) + 31) / 32 * 32; };
 
 struct Z0Leaf { double v[9]; double wf; int rule; };
+template <int POP>
 struct Z0Warp {
   Z0Leaf leaf[Z0W_LEAVES];
-  DTri stack[Z0W_STACK];
+  DTri stack[Z0Stack<POP>::N];
   double g[4][3], c[4], a[4], o[3];
   int start[Z0W_LEAVES + 1];
 };
@@ -90,19 +95,21 @@ struct Z0Warp {
 // each push is one group of <= 64 of the next depth, so the stack holds <= 1 + 7 x 64 entries.
 // The leaf SET equals the host's depth-first one (the split test does not depend on the order);
 // the quadrature of the leaves is shared by all 32 lanes.
-__global__ void __launch_bounds__(32 * Z0W_WARPS) k_z0_warp(
+template <int POP, int MINB>
+__global__ void __launch_bounds__(32 * Z0W_WARPS, MINB) k_z0_warp(
     const Z0Item* __restrict__ items, int64_t nitems, const double* __restrict__ xyz, const int32_t* __restrict__ tets,
     const int64_t* __restrict__ parent, const double* __restrict__ Ms_tet, Lat lat, const TriRules* __restrict__ rules,
     const int64_t* __restrict__ rowbase, int64_t r0, double* __restrict__ vals) {
+  constexpr int Z0W_POP = POP;
   extern __shared__ __align__(16) unsigned char z0w_smem[];
   TriRules& R = *reinterpret_cast<TriRules*>(z0w_smem);
-  Z0Warp* W = reinterpret_cast<Z0Warp*>(z0w_smem + ((sizeof(TriRules) + 15) / 16) * 16);
+  Z0Warp<POP>* W = reinterpret_cast<Z0Warp<POP>*>(z0w_smem + ((sizeof(TriRules) + 15) / 16) * 16);
   for (int i = threadIdx.x; i < (int)(sizeof(TriRules) / sizeof(double)); i += blockDim.x)
     reinterpret_cast<double*>(&R)[i] = reinterpret_cast<const double*>(rules)[i];
   __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  Z0Warp& w = W[wid];
+  Z0Warp<POP>& w = W[wid];
   for (int64_t it_i = (int64_t)blockIdx.x * Z0W_WARPS + wid; it_i < nitems; it_i += (int64_t)gridDim.x * Z0W_WARPS) {
     const Z0Item it = items[it_i];
     int code = it.code;
@@ -368,14 +375,23 @@ void z0_device_integrate(const HostSetup& S, std::vector<std::vector<Z0Item>>& t
                                                                c.base, 0, c.vals);
     CKZ(cudaGetLastError());
   } else if (n) {
-    const size_t smem = ((sizeof(TriRules) + 15) / 16) * 16 + Z0W_WARPS * sizeof(Z0Warp);
-    CKZ(cudaFuncSetAttribute(k_z0_warp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    static const bool pop16 = std::getenv("PMFEM_Z0_POP") && std::atoi(std::getenv("PMFEM_Z0_POP")) == 16;
     int nsm = 148;
     CKZ(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, P.dev));
     const int64_t want = (n + Z0W_WARPS - 1) / Z0W_WARPS;
     const unsigned blocks = (unsigned)std::min<int64_t>(want, (int64_t)nsm * 32);
-    k_z0_warp<<<blocks, 32 * Z0W_WARPS, smem, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules, c.base,
-                                                       0, c.vals);
+    const size_t rb = ((sizeof(TriRules) + 15) / 16) * 16;
+    if (pop16) {
+      const size_t smem = rb + Z0W_WARPS * sizeof(Z0Warp<16>);
+      CKZ(cudaFuncSetAttribute(k_z0_warp<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_z0_warp<16, 1><<<blocks, 32 * Z0W_WARPS, smem, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules,
+                                                               c.base, 0, c.vals);
+    } else {
+      const size_t smem = rb + Z0W_WARPS * sizeof(Z0Warp<8>);
+      CKZ(cudaFuncSetAttribute(k_z0_warp<8, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      k_z0_warp<8, 5><<<blocks, 32 * Z0W_WARPS, smem, P.st>>>(c.items, n, P.xyz, P.tets, P.parent, P.ms, lat, P.rules,
+                                                              c.base, 0, c.vals);
+    }
     CKZ(cudaGetLastError());
   }
   if (nvals) CKZ(cudaMemcpyAsync(c.hvals, c.vals, nvals * sizeof(double), cudaMemcpyDeviceToHost, P.st));
