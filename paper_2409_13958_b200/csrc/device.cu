@@ -472,7 +472,8 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     }
   } else {
     // C4x, batched like B4/U4: KB headers + values first, then their 4 KB scalar gathers
-    constexpr int KB = 2;
+    // (F = 4: KB = 4, PMFEM_K4_KB=4 -- fewer dependent round trips per row, more registers)
+    constexpr int KB = F == 4 ? 4 : 2;
     for (int64_t base = b + lane; base < e_end; base += KB * G) {
       unsigned long long h[KB];
       float4 vv[KB];
@@ -1789,7 +1790,8 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     }
 #undef K4S_BY_G
 #undef K4S_LAUNCH
-  } else
+  } else {
+  static const bool k4_kb4 = std::getenv("PMFEM_K4_KB") != nullptr && std::atoi(std::getenv("PMFEM_K4_KB")) == 4;
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
   (D.cbox_format == 3                                                                                   \
@@ -1802,6 +1804,9 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
    : D.k4_vec                                                                                           \
        ? k4_interp_corr<PP, GG, 2><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0)   \
+   : k4_kb4                                                                                             \
+       ? k4_interp_corr<PP, GG, 4><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
+             rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0)   \
        : k4_interp_corr<PP, GG, 0><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0))
 #define K4_BY_G(PP)                                                                                     \
@@ -1811,6 +1816,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     default: K4_BY_G(3); break;
 #undef K4_BY_G
 #undef K4_LAUNCH
+  }
   }
   CK(cudaGetLastError());
   halo(D, 2, D.u, 1, st);

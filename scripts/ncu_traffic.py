@@ -11,7 +11,7 @@ import json
 import os
 import subprocess
 
-KMAP = {"k1_local_in": "K1_local_in", "k2_tile": "K2_anterp", "k4_interp_corr": "K4_interp_corr",
+KMAP = {"k1_local_in": "K1_local_in", "k2_tile": "K2_anterp", "k4_interp_corr": "K4_interp_corr", "k4_win": "K4_interp_corr",
         "k5_grad_sum": "K5_grad_sum", "fft_yz_fused": "K3_fft_yz_fused", "fft_x_forward<float>": "K3_fft_x_forward",
         "fft_x_inverse<float>": "K3_fft_x_inverse", "fft_strided<float": "K3_fft_strided"}
 
