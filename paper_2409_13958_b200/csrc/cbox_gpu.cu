@@ -578,6 +578,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
   const double per_box_w = (double)Nall / ((double)c.n[0] * c.n[1] * c.n[2]);
   if (fmt == "w4" || (fmt == "auto" && D.world == 1 && per_box_w >= 1.0)) {
     const int W4_WMAX = std::getenv("PMFEM_W4_WMAX") ? std::atoi(std::getenv("PMFEM_W4_WMAX")) : 6144;
+    const bool w4_tma = std::getenv("PMFEM_W4_TMA") != nullptr && std::atoi(std::getenv("PMFEM_W4_TMA")) == 1;
     int R[3], lim[3];
     for (int a = 0; a < 3; ++a) {
       R[a] = (int)std::ceil(c.rer / c.delta[a] + 1.0) - 1;
@@ -632,6 +633,16 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
     for (int64_t i = r0; i < r0 + Np && fits;) {
       int64_t j = i + 1;
       while (j < r0 + Np && j - i < W4_TMAX && an[3 * j + 1] == an[3 * i + 1] && an[3 * j + 2] == an[3 * i + 2]) ++j;
+      // TMA variant: the tile's chunk block must fit the shared-memory stage (W4_CCAP chunks)
+      if (w4_tma) {
+        int64_t ch = 0, k = i;
+        for (; k < j; ++k) {
+          const int64_t ck = (cnt[k - r0] + 3) / 4;
+          if (k > i && ch + ck > W4_CCAP - 2) break;
+          ch += ck;
+        }
+        j = k;
+      }
       int64_t w = window(i, j);
       while ((w > W4_WMAX || runs.size() > (size_t)W4_RMAX) && j - i > 1) { j = i + (j - i) / 2; w = window(i, j); }
       if (w > W4_WMAX || w > 65535 || runs.size() > (size_t)W4_RMAX) { fits = false; break; }
@@ -655,8 +666,11 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
       int* d_rs = dup_c(rstart);
       int* d_rl = dup_c(rlen);
       int* d_rc = dup_c(rloc);
-      float* d_wval = dalloc_c<float>(4 * (size_t)wptr[Np]);
-      unsigned short* d_widx = dalloc_c<unsigned short>(4 * (size_t)wptr[Np]);
+      // + 2 chunks: the TMA variant copies from an even chunk index in whole 16-byte units
+      float* d_wval = dalloc_c<float>(4 * ((size_t)wptr[Np] + 2));
+      unsigned short* d_widx = dalloc_c<unsigned short>(4 * ((size_t)wptr[Np] + 2));
+      CKC(cudaMemset(d_wval + 4 * (size_t)wptr[Np], 0, 8 * sizeof(float)));
+      CKC(cudaMemset(d_widx + 4 * (size_t)wptr[Np], 0, 8 * sizeof(unsigned short)));
       unsigned long long* d_miss = dalloc_c<unsigned long long>(1);
       CKC(cudaMemset(d_miss, 0, sizeof(unsigned long long)));
       k_w4_fill<<<blocks, 128>>>(Np, d_ptr, d_col, d_val, d_tof, d_rptr, d_rs, d_rl, d_rc, d_wptr, d_wval, d_widx, d_miss);
@@ -673,6 +687,7 @@ int64_t device_build_cbox(DeviceState& D, const HostSetup& S) {
         D.w_ntiles = (int64_t)trow.size() - 1;
         D.w_max = std::max(wmax, 1);
         D.w_umax = umax;
+        D.w_tma = w4_tma;
         D.cbox_chunks = wptr[Np];
         D.cbox_format = 5;
         if (std::getenv("PMFEM_VERBOSE"))

@@ -601,6 +601,120 @@ __global__ void __launch_bounds__(256) k4_win(RowRange rr, const float* __restri
   }
 }
 
+// W4 with the tile's whole chunk block (values and indices, <= W4_CCAP chunks) copied into shared
+// memory by the bulk-copy engine (cp.async.bulk, one mbarrier with the byte count): the HBM stream
+// no longer waits on any per-row dependency -- the copy is issued first, the q window and the U
+// sub-grid are staged by the threads meanwhile, and the rows then read everything from shared
+// memory (PMFEM_W4_TMA=1).
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src), "r"(bytes),
+               "r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  unsigned done = 0;
+  while (!done) {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(phase) : "memory");
+  }
+}
+
+template <int P, int G>
+__global__ void __launch_bounds__(256) k4_win_tma(RowRange rr, const float* __restrict__ U, const int4* __restrict__ st_s,
+                                                  const float4* __restrict__ st_t, GridDims g,
+                                                  const int64_t* __restrict__ tile_row, const int* __restrict__ run_ptr,
+                                                  const int* __restrict__ run_start, const int* __restrict__ run_len,
+                                                  const int* __restrict__ run_loc, const int64_t* __restrict__ c_ptr,
+                                                  const float4* __restrict__ c_val4, const ushort4* __restrict__ c_idx,
+                                                  const float* __restrict__ q, const float* __restrict__ uloc,
+                                                  float* __restrict__ u, int wmax, int umax) {
+  extern __shared__ __align__(16) unsigned char w4t_smem[];
+  float4* vs = reinterpret_cast<float4*>(w4t_smem);                       // [W4_CCAP]
+  ushort4* is = reinterpret_cast<ushort4*>(vs + W4_CCAP);                 // [W4_CCAP]
+  float* qs = reinterpret_cast<float*>(is + W4_CCAP);                     // [wmax]
+  float* us = qs + wmax;                                                  // [umax]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int64_t cp[W4_TMAX + 1];
+  constexpr int NR = (P + 1) * (P + 1);
+  const int t = blockIdx.x;
+  const int64_t row0 = tile_row[t], row1 = tile_row[t + 1];
+  const int64_t ce0 = c_ptr[row0 - rr.row0] & ~(int64_t)1;               // even: 16-byte aligned index block
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    const int64_t ce1 = c_ptr[row1 - rr.row0];
+    const unsigned nch = (unsigned)((ce1 - ce0 + 1) & ~(int64_t)1);
+    DCHECK(nch <= W4_CCAP);
+    mbar_expect_tx(&bar, nch * 24u);
+    bulk_g2s(vs, c_val4 + ce0, nch * 16u, &bar);
+    bulk_g2s(is, c_idx + ce0, nch * 8u, &bar);
+  }
+  for (int i = threadIdx.x; i <= (int)(row1 - row0); i += blockDim.x) cp[i] = c_ptr[row0 - rr.row0 + i] - ce0;
+  const int4 sa = st_s[row0];
+  const int xa = sa.x, nxs = st_s[row1 - 1].x - xa + P + 1, pitch = nxs | 1;
+  DCHECK(pitch * NR <= umax);
+  {
+    const int warp = threadIdx.x >> 5, l32 = threadIdx.x & 31;
+    for (int r = run_ptr[t] + warp; r < run_ptr[t + 1]; r += blockDim.x >> 5) {
+      const int s0 = run_start[r], len = run_len[r], loc = run_loc[r];
+      DCHECK(loc >= 0 && loc + len <= wmax && s0 >= 0 && s0 + len <= rr.ncol);
+      for (int j = l32; j < len; j += 32) qs[loc + j] = __ldg(q + s0 + j);
+    }
+    for (int i = threadIdx.x; i < nxs * NR; i += blockDim.x) {
+      const int ix = i % nxs, l = i / nxs, jy = l % (P + 1), jz = l / (P + 1);
+      us[l * pitch + ix] = __ldg(U + ((int64_t)wrapi(sa.z + jz, g.n2, g.per2) * g.n1 + wrapi(sa.y + jy, g.n1, g.per1)) * g.n0 +
+                                wrapi(xa + ix, g.n0, g.per0));
+    }
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  const int lane = threadIdx.x & (G - 1);
+  for (int64_t base = row0; base < row1; base += 256 / G) {
+    const int64_t n = base + (threadIdx.x / G);
+    const bool valid = n < row1;
+    float acc = 0.f;
+    const int b = valid ? (int)cp[n - row0] : 0, e_end = valid ? (int)cp[n - row0 + 1] : 0;
+    const float ul = (valid && lane == 0) ? uloc[n] : 0.f;
+    if (valid && lane < NR) {
+      const int sx = st_s[n].x - xa;
+      const float4 tt = st_t[n];
+      float wx[P + 1], wy[P + 1], wz[P + 1];
+      lagr<P>(tt.x, wx); lagr<P>(tt.y, wy); lagr<P>(tt.z, wz);
+      for (int r = lane; r < NR; r += G) {
+        const int jy = r % (P + 1), jz = r / (P + 1);
+        float wyz = 0.f;
+#pragma unroll
+        for (int a = 0; a <= P; ++a)
+#pragma unroll
+          for (int c = 0; c <= P; ++c)
+            if (a == jy && c == jz) wyz = wy[a] * wz[c];
+        const float* row = us + r * pitch + sx;
+        float v = 0.f;
+#pragma unroll
+        for (int i = 0; i <= P; ++i) v = fmaf(wx[i], row[i], v);
+        acc = fmaf(wyz, v, acc);
+      }
+    }
+#pragma unroll 4
+    for (int e = b + lane; e < e_end; e += G) {
+      const ushort4 id = is[e];
+      const float4 vv = vs[e];
+      DCHECK(id.x < wmax && id.y < wmax && id.z < wmax && id.w < wmax);
+      acc = fmaf(vv.x, qs[id.x], fmaf(vv.y, qs[id.y], fmaf(vv.z, qs[id.z], fmaf(vv.w, qs[id.w], acc))));
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (valid && lane == 0) u[n] = acc + ul;
+  }
+}
+
 // K4 "stream" variant for the block formats (B4: F = 1, U4: F = 3), PMFEM_K4_STREAM=1: a warp
 // owns RPW consecutive rows and streams their C_box blocks as ONE contiguous range
 // [c_ptr[r0], c_ptr[r0 + RPW]) -- 32 consecutive blocks per step, KB steps of index/value loads
@@ -1298,6 +1412,9 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   }
   D.launches_per_eval = 5 + (D.fused_tile ? 3 : 5) + (D.cbox_format == 3 ? 1 : 0);   // m4, K1, K2, FFT, (q4), K4, K5
   D.k4_vec = std::getenv("PMFEM_K4_VEC") != nullptr && std::atoi(std::getenv("PMFEM_K4_VEC")) == 1;
+  // K4 variants read per context (tests switch them between contexts of one process)
+  D.k4_stream = std::getenv("PMFEM_K4_STREAM") != nullptr && std::atoi(std::getenv("PMFEM_K4_STREAM")) == 1;
+  D.k4_kb4 = std::getenv("PMFEM_K4_KB") != nullptr && std::atoi(std::getenv("PMFEM_K4_KB")) == 4;
   D.row_split = 1;            // 2 measured slower on C2 (K1 0.067 -> 0.070 ms); kept for PMFEM_ROW_SPLIT=2
   if (const char* e = std::getenv("PMFEM_ROW_SPLIT")) {
     const int v = std::atoi(e);
@@ -1737,7 +1854,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
     k_q4<<<(unsigned)((4 * D.q4s + 255) / 256), 256, 0, st>>>(D.q4s, D.q, D.q4);
     CK(cudaGetLastError());
   }
-  static const bool k4_stream_on = std::getenv("PMFEM_K4_STREAM") != nullptr && std::atoi(std::getenv("PMFEM_K4_STREAM")) == 1;
+  const bool k4_stream_on = D.k4_stream;
   if (k4_stream_on && (D.cbox_format == 1 || D.cbox_format == 3)) {
     const unsigned blocks = (unsigned)std::max<int64_t>(1, (nrows + 8 * 64 - 1) / (8 * 64));
     const float* qv = D.cbox_format == 3 ? reinterpret_cast<const float*>(D.q4) : D.q;
@@ -1762,7 +1879,26 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
   } while (0)
 #define K4W_BY_G(PP) \
   if (D.k4_group == 8) K4W_LAUNCH(PP, 8); else if (D.k4_group == 16) K4W_LAUNCH(PP, 16); else K4W_LAUNCH(PP, 32)
-    if (D.w_ntiles > 0) {
+    if (D.w_ntiles > 0 && D.w_tma) {
+      const size_t smem_t = (size_t)W4_CCAP * 24 + sizeof(float) * ((size_t)D.w_max + D.w_umax);
+#define K4WT_LAUNCH(PP, GG)                                                                                 \
+  do {                                                                                                      \
+    CK(cudaFuncSetAttribute(k4_win_tma<PP, GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_t)); \
+    k4_win_tma<PP, GG><<<(unsigned)D.w_ntiles, 256, smem_t, st>>>(rr, D.Q, D.st_s, D.st_t, g, D.w_trow,       \
+                                                                 D.w_rptr, D.w_rstart, D.w_rlen, D.w_rloc,    \
+                                                                 D.c_ptr, v4, D.w_idx, D.q, D.uloc, D.u,      \
+                                                                 D.w_max, D.w_umax);                          \
+  } while (0)
+#define K4WT_BY_G(PP) \
+  if (D.k4_group == 8) K4WT_LAUNCH(PP, 8); else if (D.k4_group == 16) K4WT_LAUNCH(PP, 16); else K4WT_LAUNCH(PP, 32)
+      switch (D.order) {
+        case 1: K4WT_BY_G(1); break;
+        case 2: K4WT_BY_G(2); break;
+        default: K4WT_BY_G(3); break;
+      }
+#undef K4WT_BY_G
+#undef K4WT_LAUNCH
+    } else if (D.w_ntiles > 0) {
       switch (D.order) {
         case 1: K4W_BY_G(1); break;
         case 2: K4W_BY_G(2); break;
@@ -1791,7 +1927,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
 #undef K4S_BY_G
 #undef K4S_LAUNCH
   } else {
-  static const bool k4_kb4 = std::getenv("PMFEM_K4_KB") != nullptr && std::atoi(std::getenv("PMFEM_K4_KB")) == 4;
+  const bool k4_kb4 = D.k4_kb4;
   switch (D.order) {
 #define K4_LAUNCH(PP, GG)                                                                               \
   (D.cbox_format == 3                                                                                   \

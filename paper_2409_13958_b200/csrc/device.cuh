@@ -64,6 +64,7 @@ __host__ __device__ __forceinline__ int seg_at(const int* r, int i) {
 
 constexpr int W4_TMAX = 128;   // W4 C_box: rows per tile (cbox_gpu.cu builder, K4 k4_win)
 constexpr int W4_RMAX = 512;   // W4 C_box: runs per tile (the builder splits tiles above it)
+constexpr int W4_CCAP = 2048;  // W4 TMA variant: chunks per tile (the tile's block staged in shared memory)
 
 struct DeviceState {
   int device = -1;
@@ -105,6 +106,7 @@ struct DeviceState {
   int64_t w_ntiles = 0;
   int w_max = 0;                      // largest window (floats of shared memory)
   int w_umax = 0;                     // largest U sub-grid of a tile (odd line pitch x (P+1)^2 floats)
+  bool w_tma = false;                 // PMFEM_W4_TMA=1: k4_win_tma (the tile's chunk block by cp.async.bulk)
   int64_t* w_trow = nullptr;          // [ntiles+1] first internal row of each tile
   int* w_rptr = nullptr;              // [ntiles+1] run offsets
   int* w_rstart = nullptr;            // run first internal row
@@ -120,6 +122,8 @@ struct DeviceState {
   int row_split = 1;          // K1/K5 threads per row (2 for small meshes)
   bool yz_half = false;       // fused YZ FFT with the z axis split into even/odd halves (PMFEM_YZ_HALF=1)
   bool k4_vec = false;        // C4x: vector q gathers for run chunks (PMFEM_K4_VEC=1)
+  bool k4_stream = false;     // B4/U4: row-range streaming kernel (PMFEM_K4_STREAM=1)
+  bool k4_kb4 = false;        // C4x: 4 batched chunks per lane (PMFEM_K4_KB=4)
 
   float4* st_t = nullptr;     // local coordinates t - s
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32
