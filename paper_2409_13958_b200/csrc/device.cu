@@ -1489,7 +1489,7 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     if (D.cbox_format == 2) D.k4_group = 16;   // SEG: mask words per row (A/B: PMFEM_K4_GROUP)
     if (const char* e = std::getenv("PMFEM_K4_GROUP")) {
       const int gsel = std::atoi(e);
-      if (gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
+      if (gsel == 4 || gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
     }
   }
   // C_box per near pair: C4x 4-byte value + 2 bytes of chunk header, B4 4-byte value + 1 byte
@@ -1878,7 +1878,8 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
                                                             D.w_idx, D.q, D.uloc, D.u, D.w_max, D.w_umax);  \
   } while (0)
 #define K4W_BY_G(PP) \
-  if (D.k4_group == 8) K4W_LAUNCH(PP, 8); else if (D.k4_group == 16) K4W_LAUNCH(PP, 16); else K4W_LAUNCH(PP, 32)
+  if (D.k4_group == 4) K4W_LAUNCH(PP, 4); else if (D.k4_group == 8) K4W_LAUNCH(PP, 8);                   \
+  else if (D.k4_group == 16) K4W_LAUNCH(PP, 16); else K4W_LAUNCH(PP, 32)
     if (D.w_ntiles > 0 && D.w_tma) {
       const size_t smem_t = (size_t)W4_CCAP * 24 + sizeof(float) * ((size_t)D.w_max + D.w_umax);
 #define K4WT_LAUNCH(PP, GG)                                                                                 \
@@ -1890,7 +1891,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
                                                                  D.w_max, D.w_umax);                          \
   } while (0)
 #define K4WT_BY_G(PP) \
-  if (D.k4_group == 8) K4WT_LAUNCH(PP, 8); else if (D.k4_group == 16) K4WT_LAUNCH(PP, 16); else K4WT_LAUNCH(PP, 32)
+  if (D.k4_group <= 8) K4WT_LAUNCH(PP, 8); else if (D.k4_group == 16) K4WT_LAUNCH(PP, 16); else K4WT_LAUNCH(PP, 32)
       switch (D.order) {
         case 1: K4WT_BY_G(1); break;
         case 2: K4WT_BY_G(2); break;
@@ -1918,7 +1919,7 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
                                               D.seg_moff, D.c_ptr, D.seg_mask, D.c_val, D.q, D.uloc, D.u); \
   } while (0)
 #define K4S_BY_G(PP) \
-  if (G == 8) K4S_LAUNCH(PP, 8); else if (G == 16) K4S_LAUNCH(PP, 16); else K4S_LAUNCH(PP, 32)
+  if (G <= 8) K4S_LAUNCH(PP, 8); else if (G == 16) K4S_LAUNCH(PP, 16); else K4S_LAUNCH(PP, 32)
     switch (D.order) {
       case 1: K4S_BY_G(1); break;
       case 2: K4S_BY_G(2); break;
@@ -1946,7 +1947,8 @@ void device_eval(DeviceState& D, const float* m, float* H, cudaStream_t st, Eval
        : k4_interp_corr<PP, GG, 0><<<(unsigned)std::max<int64_t>(1, (nrows * GG + 255) / 256), 256, 0, st>>>(                \
              rr, D.Q, D.st_s, D.st_t, g, D.c_ptr, D.c_hdr, D.c_bidx, v4, D.q, D.uloc, D.u, (int64_t)0))
 #define K4_BY_G(PP)                                                                                     \
-  (D.k4_group == 8 ? K4_LAUNCH(PP, 8) : D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
+  (D.k4_group == 4 ? K4_LAUNCH(PP, 4) : D.k4_group == 8 ? K4_LAUNCH(PP, 8) :                           \
+   D.k4_group == 16 ? K4_LAUNCH(PP, 16) : K4_LAUNCH(PP, 32))
     case 1: K4_BY_G(1); break;
     case 2: K4_BY_G(2); break;
     default: K4_BY_G(3); break;
