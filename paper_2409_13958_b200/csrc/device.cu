@@ -1487,6 +1487,11 @@ void device_upload(DeviceState& D, const HostSetup& S) {
     const double row4 = (double)D.cbox_chunks / std::max<int64_t>(Np, 1);
     D.k4_group = row4 >= 96 ? 32 : (row4 >= 40 ? 16 : 8);
     if (D.cbox_format == 2) D.k4_group = 16;   // SEG: mask words per row (A/B: PMFEM_K4_GROUP)
+    // global-index formats (C4x, B4, U4): 8 lanes per row -- four rows per warp keep four
+    // independent header -> gather chains in flight (call 25: C4 K4 9.98 ms at 32 lanes, 8.80 at
+    // 16, 8.25 at 8, 8.54 at 4; C3 0.89 / 0.53 / 0.47 / 0.49 ms); W4 keeps the row-length rule
+    // (its gathers hit shared memory: C5 1.89 ms at 32 lanes vs 2.21 at 8)
+    if (D.cbox_format == 0 || D.cbox_format == 1 || D.cbox_format == 3) D.k4_group = 8;
     if (const char* e = std::getenv("PMFEM_K4_GROUP")) {
       const int gsel = std::atoi(e);
       if (gsel == 4 || gsel == 8 || gsel == 16 || gsel == 32) D.k4_group = gsel;
