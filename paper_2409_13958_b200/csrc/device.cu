@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(256) k4_interp_corr(RowRange rr, const float* 
     }
   } else {
     // C4x, batched like B4/U4: KB headers + values first, then their 4 KB scalar gathers
-    // (F = 4: KB = 4, PMFEM_K4_KB=4 -- fewer dependent round trips per row, more registers)
+    // (F = 4: KB = 4, the default since round 2 call 29 -- fewer dependent round trips per row; PMFEM_K4_KB=2 for F = 0)
     constexpr int KB = F == 4 ? 4 : 2;
     for (int64_t base = b + lane; base < e_end; base += KB * G) {
       unsigned long long h[KB];
@@ -1414,7 +1414,9 @@ void device_upload(DeviceState& D, const HostSetup& S) {
   D.k4_vec = std::getenv("PMFEM_K4_VEC") != nullptr && std::atoi(std::getenv("PMFEM_K4_VEC")) == 1;
   // K4 variants read per context (tests switch them between contexts of one process)
   D.k4_stream = std::getenv("PMFEM_K4_STREAM") != nullptr && std::atoi(std::getenv("PMFEM_K4_STREAM")) == 1;
-  D.k4_kb4 = std::getenv("PMFEM_K4_KB") != nullptr && std::atoi(std::getenv("PMFEM_K4_KB")) == 4;
+  // C4x: 4 batched chunks per lane by default (call 29, 8 lanes per row: C4 K4 8.18 -> 7.86 ms);
+  // PMFEM_K4_KB=2 selects 2
+  D.k4_kb4 = !(std::getenv("PMFEM_K4_KB") != nullptr && std::atoi(std::getenv("PMFEM_K4_KB")) == 2);
   D.row_split = 1;            // 2 measured slower on C2 (K1 0.067 -> 0.070 ms); kept for PMFEM_ROW_SPLIT=2
   if (const char* e = std::getenv("PMFEM_ROW_SPLIT")) {
     const int v = std::atoi(e);

@@ -123,7 +123,7 @@ struct DeviceState {
   bool yz_half = false;       // fused YZ FFT with the z axis split into even/odd halves (PMFEM_YZ_HALF=1)
   bool k4_vec = false;        // C4x: vector q gathers for run chunks (PMFEM_K4_VEC=1)
   bool k4_stream = false;     // B4/U4: row-range streaming kernel (PMFEM_K4_STREAM=1)
-  bool k4_kb4 = false;        // C4x: 4 batched chunks per lane (PMFEM_K4_KB=4)
+  bool k4_kb4 = true;         // C4x: 4 batched chunks per lane (default; PMFEM_K4_KB=2 for 2)
 
   float4* st_t = nullptr;     // local coordinates t - s
   // PGF spectrum [P2][P1][H0] / (P0 P1 P2), fp32

@@ -232,7 +232,7 @@ def test_slab_fft_simulated_ranks(key, world, monkeypatch):
     assert rel_l2(_run(ctx, "heff", m, rank), om.heff(m, "aim")) <= TOL
 
 
-@pytest.mark.parametrize("fmt", ["u4", "u4-stream", "b4-stream", "seg", "c4x", "c4x-vec", "c4x-kb4", "b4", "w4", "w4-tma"])
+@pytest.mark.parametrize("fmt", ["u4", "u4-stream", "b4-stream", "seg", "c4x", "c4x-vec", "c4x-kb2", "b4", "w4", "w4-tma"])
 @pytest.mark.parametrize("key", ["C2p2", "C3p1", "N1p2", "C4p3"])
 def test_cbox_formats(key, fmt, monkeypatch):
     """K4 streaming either packed C_box format (C4x also with vector gathers of run chunks; the
@@ -240,7 +240,7 @@ def test_cbox_formats(key, fmt, monkeypatch):
     monkeypatch.setenv("PMFEM_CBOX_FORMAT", fmt.split("-")[0])
     monkeypatch.setenv("PMFEM_K4_VEC", "1" if fmt.endswith("vec") else "0")
     monkeypatch.setenv("PMFEM_K4_STREAM", "1" if fmt.endswith("stream") else "0")
-    monkeypatch.setenv("PMFEM_K4_KB", "4" if fmt.endswith("kb4") else "2")
+    monkeypatch.setenv("PMFEM_K4_KB", "2" if fmt.endswith("kb2") else "4")
     monkeypatch.setenv("PMFEM_W4_TMA", "1" if fmt.endswith("tma") else "0")
     om = oracle_model(key)
     ctx = lib_context(key, device=0)
